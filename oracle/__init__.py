@@ -1,0 +1,191 @@
+"""oracle -- plain, slow, obviously-correct CPU reference of the encoder hot path.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  The product path (``paper_1311_1419_b200``) never imports it, and
+this package never imports the product path; the two share no code.  The
+only shared module is ``synth`` (seeded input generators, no method
+arithmetic).
+
+Everything is fp64 numpy.  Why fp64 is EXACT here (SURVEY.md sec.8(c),
+DESIGN.md "Exactness"): every fp16 value of Phi is an integer multiple of
+2^-24 and every residual r_j is an integer with |r_j| <= 255, so every product
+Phi_mj * r_j and every partial sum is a multiple of 2^-24; with |Phi| <= 2048
+and N <= 1024 every partial sum is below 2^29 in magnitude, so 29 + 24 = 53
+bits hold it exactly.  The fp64 result is therefore the exact real value in
+any summation order, and a library matmul (BLAS dgemm) may serve as the
+summation step without any rounding caveat.
+
+Paper passages followed (PAPER.md line numbers, section):
+  a1 GOP partition   -- P:25, sec.3.1 ("divided into key frame and several
+                        residual frames"), sec.3.2; short final GOP SPEC.md:385-390
+  a2 block vector    -- P:85 sec.3.2 (x is the vectorised signal); row-major
+                        vectorisation SPEC.md:89; B x B blocks with a shared Phi
+                        is BASELINE.json:5's adaptation (reading R1)
+  a3 residual        -- P:87 ("The CS frames all subtract the same key frame in
+                        a GOP"), Eq.(2)-(3) P:89-91 with the raw key pass-through
+                        (e_coding = e_decoding = 0, BASELINE.json:5)
+  a4 measurement     -- Eq.(1): y = A x, A in R^{m x n}
+  a5 Phi             -- fp16 bit patterns supplied by the caller (synth.phi_from_seed)
+  a6 output layout   -- y[s][g][c][by][bx][m], block-major (BASELINE.json:5 item 4)
+  a7 CR accounting   -- "original bits / (key bits + measurement bits)"
+                        (BASELINE.json:5); Table I closed form P:113-126
+"""
+from __future__ import annotations
+
+import numpy as np
+
+__all__ = [
+    "gop_partition", "cs_frame_count", "block_grid", "frame_blocks", "residual", "measure",
+    "tolerance_scale", "encode", "encode_stream", "phi_values", "compression_ratio", "total_cr",
+    "check_tolerance",
+]
+
+
+# -- a1 ------------------------------------------------------------------------------------------
+def gop_partition(T: int, G: int):
+    """GOPs of a T-frame sequence: list of (key frame index, [CS frame indices]).
+
+    P:71 sec.3.1 "we divide the source video into a key frame and several
+    residual frames"; sec.3.2 one key per GOP.  The final GOP may be short
+    (10 frames, G=4 -> lengths 4,4,2)."""
+    if T < 0 or G < 1:
+        raise ValueError("T >= 0 and G >= 1 required")
+    gops = []
+    for t0 in range(0, T, G):
+        gops.append((t0, list(range(t0 + 1, min(t0 + G, T)))))
+    return gops
+
+
+def cs_frame_count(T: int, G: int) -> int:
+    return sum(len(cs) for _, cs in gop_partition(T, G))
+
+
+# -- a2 ------------------------------------------------------------------------------------------
+def block_grid(W: int, H: int, B: int):
+    """(nby, nbx): B x B blocks covering the frame, partial blocks zero padded (reading R10)."""
+    return (H + B - 1) // B, (W + B - 1) // B
+
+
+def frame_blocks(frame: np.ndarray, B: int) -> np.ndarray:
+    """int64 [nby*nbx][B*B]: block (by,bx) in raster order, pixel j = yy*B + xx
+    (row-major inside the block).  Pixels outside the frame are 0."""
+    H, W = frame.shape
+    nby, nbx = block_grid(W, H, B)
+    pad = np.zeros((nby * B, nbx * B), dtype=np.int64)
+    pad[:H, :W] = frame
+    return pad.reshape(nby, B, nbx, B).transpose(0, 2, 1, 3).reshape(nby * nbx, B * B)
+
+
+# -- a3 ------------------------------------------------------------------------------------------
+def residual(cs_frame: np.ndarray, key_frame: np.ndarray) -> np.ndarray:
+    """D = F_cs - F_key as signed integers, no clamping (Eq.(3)).
+    With the raw key pass-through F_hat_key = F_key (Eq.(2) with zero codec error)."""
+    if cs_frame.shape != key_frame.shape:
+        raise ValueError("frame shapes differ")
+    return cs_frame.astype(np.int64) - key_frame.astype(np.int64)
+
+
+# -- a4 / a5 -------------------------------------------------------------------------------------
+def phi_values(phi_bits: np.ndarray) -> np.ndarray:
+    """fp64 values of the fp16 bit patterns (exact widening)."""
+    return np.asarray(phi_bits, dtype=np.uint16).view(np.float16).astype(np.float64)
+
+
+def measure(R: np.ndarray, phi: np.ndarray) -> np.ndarray:
+    """y_b = Phi r_b for every block row r_b of R (Eq.(1) constraint Ax = y).
+    R: integer [nblk][N]; phi: fp64 [M][N]; returns fp64 [nblk][M] (exact, see module doc)."""
+    return np.asarray(R, dtype=np.float64) @ np.asarray(phi, dtype=np.float64).T
+
+
+def tolerance_scale(R: np.ndarray, phi: np.ndarray) -> np.ndarray:
+    """S[b][m] = sum_j |Phi_mj * r_bj| -- the per-entry scale of BASELINE.json:5's
+    acceptance bound |dy| <= 1e-5 * S (exact in fp64 for the same reason)."""
+    return np.abs(np.asarray(R, dtype=np.float64)) @ np.abs(np.asarray(phi, dtype=np.float64)).T
+
+
+# -- a1..a6 --------------------------------------------------------------------------------------
+def encode_stream(frames: np.ndarray, phi_bits: np.ndarray, G: int, B: int, with_scale: bool = True):
+    """One stream, frames uint8 [T][H][W] -> (y, S) fp64 [n_cs][nblk][M].
+
+    For every GOP (a1), every CS frame minus the GOP's key frame (a3), cut into
+    blocks (a2), measured with the shared Phi (a4); output concatenated per GOP,
+    per CS frame, block-major (a6)."""
+    T, H, W = frames.shape
+    phi = phi_values(phi_bits)
+    M, N = phi.shape
+    if N != B * B:
+        raise ValueError("Phi must have B*B columns")
+    nby, nbx = block_grid(W, H, B)
+    n_cs = cs_frame_count(T, G)
+    y = np.empty((n_cs, nby * nbx, M), dtype=np.float64)
+    S = np.empty_like(y) if with_scale else None
+    i = 0
+    for key_t, cs_ts in gop_partition(T, G):
+        for t in cs_ts:
+            R = frame_blocks(residual(frames[t], frames[key_t]), B)
+            y[i] = measure(R, phi)
+            if with_scale:
+                S[i] = tolerance_scale(R, phi)
+            i += 1
+    return y, S
+
+
+def encode(frames: np.ndarray, phi_bits: np.ndarray, G: int, B: int, with_scale: bool = True):
+    """frames uint8 [S][T][H][W] -> (y, S) fp64 [S * n_cs][nblk][M] (streams concatenated)."""
+    ys, Ss = [], []
+    for s in range(frames.shape[0]):
+        y, S = encode_stream(frames[s], phi_bits, G, B, with_scale)
+        ys.append(y)
+        Ss.append(S)
+    y = np.concatenate(ys, axis=0)
+    return y, (np.concatenate(Ss, axis=0) if with_scale else None)
+
+
+# -- a7 ------------------------------------------------------------------------------------------
+def compression_ratio(W: int, H: int, G: int, B: int, M: int, T: int = 0, key_cr: float = 1.0,
+                      bits_per_measurement: int = 8) -> float:
+    """CR = original bits / (key-frame bits + measurement bits) (BASELINE.json:5).
+
+    Original: T frames of W*H 8-bit pixels.  Key frames: W*H*8/key_cr bits each
+    (key_cr = 1: raw pass-through).  CS frames: nblk*M measurements of
+    `bits_per_measurement` bits (8 = the paper's sample-count convention, under
+    which CR_cs = n/m as in P:99 "The compression ratio of all CS frames is 50").
+    T = 0 means one full GOP.  Real GOP composition and padded blocks counted."""
+    T = G if T == 0 else T
+    gops = gop_partition(T, G)
+    n_key = len(gops)
+    n_cs = sum(len(cs) for _, cs in gops)
+    nby, nbx = block_grid(W, H, B)
+    orig = T * W * H * 8.0
+    key_bits = n_key * W * H * 8.0 / key_cr
+    meas_bits = n_cs * nby * nbx * M * float(bits_per_measurement)
+    return orig / (key_bits + meas_bits)
+
+
+def total_cr(G: int, key_cr: float, cs_cr: float) -> float:
+    """Total CR of one GOP from the per-frame ratios: G frames cost 1/key_cr + (G-1)/cs_cr
+    frame-equivalents (Table I: reproduces all nine rows)."""
+    return G / (1.0 / key_cr + (G - 1) / cs_cr)
+
+
+# -- acceptance ----------------------------------------------------------------------------------
+def check_tolerance(y_gpu: np.ndarray, y: np.ndarray, S: np.ndarray, rel: float = 1e-5):
+    """BASELINE.json:5 acceptance: |y_gpu - y| <= rel * S per entry; S == 0 => y_gpu == 0.
+    Returns (ok, stats dict)."""
+    y_gpu = np.asarray(y_gpu, dtype=np.float64)
+    d = np.abs(y_gpu - y)
+    bound = rel * S
+    bad = d > bound
+    zero = S == 0
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ratio = np.where(zero, 0.0, d / np.where(zero, 1.0, S))
+    stats = {
+        "n": int(y.size),
+        "n_bad": int(bad.sum()),
+        "max_rel": float(ratio.max()) if ratio.size else 0.0,
+        "n_zero_scale": int(zero.sum()),
+        "max_abs_at_zero_scale": float(np.abs(y_gpu[zero]).max()) if zero.any() else 0.0,
+        "frac_bit_equal_rn32": float(np.mean(y_gpu.astype(np.float32) == y.astype(np.float32))) if y.size else 1.0,
+    }
+    return stats["n_bad"] == 0 and not np.isnan(y_gpu).any(), stats

@@ -1,0 +1,293 @@
+"""Pins of the fp64 oracle against what the paper and the mathematics fix (not against itself).
+
+Each test names the plausible oracle mistake it would catch.  No GPU needed.
+"""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from conftest import load_golden
+
+
+def fp16_bits(values):
+    return np.asarray(values, dtype=np.float64).astype(np.float16).view(np.uint16)
+
+
+def two_frame(key, cs):
+    return np.stack([np.asarray(key, np.uint8), np.asarray(cs, np.uint8)])
+
+
+# ---------------------------------------------------------------- worked examples (golden)
+@pytest.mark.parametrize("name", ["worked_e1.json", "worked_e2.json"])
+def test_worked_examples(name):
+    """Hand-worked examples: catch wrong block order, wrong in-block vectorisation,
+    a transposed Phi, a sign flip of the residual, wrong zero padding."""
+    g = load_golden(name)
+    frames = two_frame(g["key"], g["cs"])
+    phi = fp16_bits(g["phi"])
+    R = oracle.frame_blocks(oracle.residual(frames[1], frames[0]), g["B"])
+    assert R.tolist() == g["residual_blocks"]
+    y, S = oracle.encode_stream(frames, phi, g["G"], g["B"])
+    assert y.shape == (1, len(g["y"]), 2)
+    assert y[0].tolist() == g["y"]  # exact
+
+
+# ---------------------------------------------------------------- Table I (paper values)
+def test_table1_total_cr_closed_form():
+    """All nine Total-CR values printed in Table I."""
+    t = load_golden("table1_cr.json")
+    for r in t["rows"]:
+        v = oracle.total_cr(r["gop"], r["key_cr"], r["cs_cr"])
+        assert abs(v - r["total_cr"]) <= t["tolerance"], r
+
+
+def test_table1_via_bit_accounting():
+    """The bit-accounting CR (original bits / (key + measurement bits)) must reproduce
+    Table I when the frame has exactly n/m = cs_cr per CS frame and key CR 23 --
+    catches a wrong key count, wrong CS count, or counting the key as a CS frame."""
+    t = load_golden("table1_cr.json")
+    for r in t["rows"]:
+        cs = r["cs_cr"]
+        B = cs        # N = cs^2 pixels per block, M = cs measurements per block -> N/M = cs
+        W = H = 2 * B
+        v = oracle.compression_ratio(W, H, r["gop"], B, cs, T=0, key_cr=r["key_cr"], bits_per_measurement=8)
+        assert abs(v - r["total_cr"]) <= t["tolerance"], (r, v)
+
+
+def test_cr_special_cases():
+    # key-only GOP: total CR = key CR
+    assert oracle.total_cr(1, 23.0, 60.0) == 23.0
+    assert oracle.compression_ratio(32, 32, 1, 16, 4, T=0, key_cr=23.0) == pytest.approx(23.0, rel=1e-15)
+    # raw key, one full GOP: G*WH / (WH + (G-1)*nblk*M)   (SURVEY.md D2 "CR nominal")
+    assert oracle.compression_ratio(1920, 1080, 8, 16, 16) == pytest.approx(8 * 1920 * 1080 / (1920 * 1080 + 7 * 8160 * 16))
+    # C5: 10.894 nominal, not 60
+    assert round(oracle.compression_ratio(1280, 720, 32, 8, 4), 3) == 10.894
+
+
+def test_gop_partition():
+    """10 frames, G=4 -> GOP lengths 4,4,2; key = first frame of each."""
+    gops = oracle.gop_partition(10, 4)
+    assert [1 + len(cs) for _, cs in gops] == [4, 4, 2]
+    assert [k for k, _ in gops] == [0, 4, 8]
+    assert gops[0][1] == [1, 2, 3]
+    assert oracle.gop_partition(5, 1) == [(i, []) for i in range(5)]
+    assert oracle.cs_frame_count(300, 8) == 262 and oracle.cs_frame_count(600, 16) == 562
+    assert oracle.cs_frame_count(240, 8) == 210 and oracle.cs_frame_count(128, 32) == 124
+
+
+# ---------------------------------------------------------------- special cases / closed forms
+def rand_frames(rng, T, H, W):
+    return rng.integers(0, 256, size=(T, H, W), dtype=np.uint8)
+
+
+def test_zero_residual():
+    """key == CS frame -> y == 0 exactly and S == 0."""
+    rng = np.random.default_rng(1)
+    f = rand_frames(rng, 1, 40, 48)
+    frames = np.repeat(f, 5, axis=0)
+    phi = synth.phi_from_seed(7, 16, 256)
+    y, S = oracle.encode_stream(frames, phi, 5, 16)
+    assert np.all(y == 0) and np.all(S == 0)
+
+
+@pytest.mark.parametrize("B", [2, 8, 16])
+def test_identity_rows(B):
+    """Phi rows = unit vectors e_{j_m}: y_m = r_{j_m} exactly -- catches a wrong
+    in-block index map (row-major j = yy*B + xx) and transposition."""
+    N = B * B
+    rng = np.random.default_rng(B)
+    js = rng.choice(N, size=min(N, 5), replace=False)
+    phi = np.zeros((len(js), N))
+    phi[np.arange(len(js)), js] = 1.0
+    frames = rand_frames(rng, 2, 3 * B + 1, 2 * B + 3)  # ragged
+    y, _ = oracle.encode_stream(frames, fp16_bits(phi), 2, B)
+    H, W = frames.shape[1:]
+    nby, nbx = -(-H // B), -(-W // B)
+    r = frames[1].astype(int) - frames[0].astype(int)
+    for b in range(nby * nbx):
+        by, bx = divmod(b, nbx)
+        for m, j in enumerate(js):
+            yy, xx = divmod(int(j), B)
+            Y, X = by * B + yy, bx * B + xx
+            want = r[Y, X] if (Y < H and X < W) else 0
+            assert y[0, b, m] == want
+
+
+def test_full_identity_M_equals_N():
+    """M = N identity (lossless diagnostic): y is the residual block itself."""
+    B = 4
+    rng = np.random.default_rng(3)
+    frames = rand_frames(rng, 3, 8, 12)
+    y, _ = oracle.encode_stream(frames, fp16_bits(np.eye(B * B)), 3, B)
+    for i, t in enumerate([1, 2]):
+        r = frames[t].astype(int) - frames[0].astype(int)
+        blocks = r.reshape(2, B, 3, B).transpose(0, 2, 1, 3).reshape(6, B * B)
+        assert np.array_equal(y[i], blocks)
+
+
+def test_unit_residual_every_position():
+    """One pixel differs by v -> y = v * Phi[:, j] for the block holding it, 0 elsewhere
+    (SPEC.md:143 x = e_j -> column j).  Sweeps every in-block position."""
+    B, M = 8, 6
+    phi = synth.phi_from_seed(11, M, B * B)
+    phiv = oracle.phi_values(phi)
+    key = np.full((2 * B, 3 * B), 77, np.uint8)
+    for yy in range(B):
+        for xx in range(B):
+            cs = key.copy()
+            Y, X = B + yy, 2 * B + xx           # block (1, 2)
+            cs[Y, X] = 77 - 50
+            y, _ = oracle.encode_stream(two_frame(key, cs), phi, 2, B)
+            want = np.zeros((6, M))
+            want[1 * 3 + 2] = -50 * phiv[:, yy * B + xx]
+            assert np.array_equal(y[0], want), (yy, xx)
+
+
+def test_linearity():
+    """y(R1 + R2) = y(R1) + y(R2) exactly (all values exact in fp64)."""
+    rng = np.random.default_rng(5)
+    H, W, B = 33, 48, 16
+    K = rng.integers(60, 190, size=(H, W)).astype(np.int64)
+    d1 = rng.integers(-30, 31, size=(H, W))
+    d2 = rng.integers(-30, 31, size=(H, W))
+    F1, F2, F3 = K + d1, K + d2, K + d1 + d2
+    phi = synth.phi_from_seed(9, 32, 256)
+    mk = lambda F: two_frame(K, F)
+    y1, _ = oracle.encode_stream(mk(F1), phi, 2, B)
+    y2, _ = oracle.encode_stream(mk(F2), phi, 2, B)
+    y3, _ = oracle.encode_stream(mk(F3), phi, 2, B)
+    assert np.array_equal(y3, y1 + y2)
+
+
+def test_antisymmetry_and_pow2_scaling():
+    rng = np.random.default_rng(6)
+    f = rand_frames(rng, 2, 32, 32)
+    phi = synth.phi_from_seed(3, 16, 256)
+    y, _ = oracle.encode_stream(f, phi, 2, 16)
+    ys, _ = oracle.encode_stream(f[::-1].copy(), phi, 2, 16)
+    assert np.array_equal(ys, -y)            # swapping key and CS frame negates y
+    phi4 = (oracle.phi_values(phi) * 4.0).astype(np.float16).view(np.uint16)
+    y4, _ = oracle.encode_stream(f, phi4, 2, 16)
+    assert np.array_equal(y4, 4.0 * y)       # Phi * 2^k -> y * 2^k
+
+
+def test_block_translation():
+    """Shifting the whole scene by exactly B pixels permutes the blocks."""
+    rng = np.random.default_rng(8)
+    B = 8
+    big = rand_frames(rng, 2, 4 * B, 6 * B)
+    a = big[:, :, : 5 * B].copy()
+    b = big[:, :, B:].copy()
+    phi = synth.phi_from_seed(4, 5, 64)
+    ya, _ = oracle.encode_stream(a, phi, 2, B)
+    yb, _ = oracle.encode_stream(b, phi, 2, B)
+    ya = ya[0].reshape(4, 5, 5)
+    yb = yb[0].reshape(4, 5, 5)
+    assert np.array_equal(ya[:, 1:], yb[:, :4])
+
+
+def test_subnormal_and_saturation():
+    # smallest fp16 subnormal 2^-24 times r = 255 -> 255 * 2^-24 exactly (no flush to zero)
+    phi = np.zeros((1, 4), np.uint16)
+    phi[0, 2] = 0x0001
+    key = np.zeros((2, 2), np.uint8)
+    cs = key.copy()
+    cs[1, 0] = 255                           # j = 1*2 + 0 = 2
+    y, S = oracle.encode_stream(two_frame(key, cs), phi, 2, 2)
+    assert y[0, 0, 0] == 255 * 2.0 ** -24 and S[0, 0, 0] == 255 * 2.0 ** -24
+    # key = 0, CS = 255, Phi = 1 -> 255 * N
+    for B in (16, 32):
+        f = np.stack([np.zeros((B, B), np.uint8), np.full((B, B), 255, np.uint8)])
+        y, _ = oracle.encode_stream(f, fp16_bits(np.ones((3, B * B))), 2, B)
+        assert np.all(y == 255 * B * B)
+    assert 255 * 256 == 65280 and 255 * 1024 == 261120
+
+
+def test_exact_against_rational_brute_force():
+    """Pure-Python exact rational arithmetic on tiny random inputs, looping over the
+    definition y[c][b][m] = sum_{yy,xx} Phi[m][yy*B+xx] * (F_t - F_key)[..] -- independent
+    of numpy's matmul; the fp64 oracle must agree bit for bit (exactness claim)."""
+    rng = np.random.default_rng(12)
+    for trial in range(6):
+        B = int(rng.choice([2, 4, 8]))
+        H, W = int(rng.integers(1, 3 * B)), int(rng.integers(1, 3 * B))
+        T, G, M = int(rng.integers(1, 6)), int(rng.integers(1, 4)), int(rng.integers(1, B * B + 1))
+        frames = rand_frames(rng, T, H, W)
+        phi = synth.phi_from_seed(100 + trial, M, B * B)
+        phif = [[Fraction(float(v)) for v in row] for row in oracle.phi_values(phi)]
+        y, _ = oracle.encode_stream(frames, phi, G, B)
+        nby, nbx = -(-H // B), -(-W // B)
+        i = 0
+        for g0 in range(0, T, G):
+            for t in range(g0 + 1, min(g0 + G, T)):
+                for by in range(nby):
+                    for bx in range(nbx):
+                        for m in range(M):
+                            acc = Fraction(0)
+                            for yy in range(B):
+                                for xx in range(B):
+                                    Y, X = by * B + yy, bx * B + xx
+                                    if Y < H and X < W:
+                                        r = int(frames[t, Y, X]) - int(frames[g0, Y, X])
+                                        acc += phif[m][yy * B + xx] * r
+                            assert Fraction(float(y[i, by * nbx + bx, m])) == acc
+                i += 1
+        assert i == y.shape[0]
+
+
+def test_exact_against_int64_path():
+    """Phi * 2^24 is an integer matrix; integer matmul with the integer residual gives
+    y * 2^24 exactly -- a second exact path."""
+    cfg = synth.CONFIGS["C1"]
+    frames = synth.gen_video(cfg)[0]
+    phi = synth.phi_from_seed(synth.phi_seed(), cfg.M, cfg.B ** 2)
+    y, _ = oracle.encode_stream(frames, phi, cfg.G, cfg.B)
+    phi_int = (oracle.phi_values(phi) * 2.0 ** 24).astype(np.int64)
+    assert np.array_equal(phi_int.astype(np.float64), oracle.phi_values(phi) * 2.0 ** 24)
+    for i, t in enumerate([1, 2, 3]):
+        r = frames[t].astype(np.int64) - frames[0].astype(np.int64)
+        R = r.reshape(9, 16, 11, 16).transpose(0, 2, 1, 3).reshape(99, 256)
+        yint = R @ phi_int.T
+        assert np.array_equal(yint.astype(np.float64) / 2.0 ** 24, y[i])
+
+
+def test_output_order_streams_gops():
+    """Concatenation order: per stream, per GOP, per CS frame (a6).  Each CS frame t
+    differs from its key by exactly t at every pixel, Phi = one row e_0 -> y = t."""
+    T, G = 10, 4
+    frames = np.zeros((2, T, 4, 4), np.uint8)
+    for s in range(2):
+        for t in range(T):
+            frames[s, t] = 10 * s + t
+    phi = np.zeros((1, 4))
+    phi[0, 0] = 1.0
+    y, _ = oracle.encode(frames, fp16_bits(phi), G, 2)
+    # CS frames of T=10, G=4: GOP0 -> 1,2,3 (key 0); GOP1 -> 5,6,7 (key 4); GOP2 -> 9 (key 8)
+    want = [1, 2, 3, 1, 2, 3, 1] * 2
+    assert y[:, :, 0].tolist() == [[w] * 4 for w in want]
+
+
+def test_tolerance_scale_properties():
+    rng = np.random.default_rng(13)
+    f = rand_frames(rng, 3, 24, 40)
+    phi = synth.phi_from_seed(21, 8, 64)
+    y, S = oracle.encode_stream(f, phi, 3, 8)
+    assert np.all(S >= np.abs(y))
+    # all-positive Phi and non-negative residual: S == y
+    f2 = np.stack([np.zeros((8, 8), np.uint8), rng.integers(0, 256, (8, 8), dtype=np.uint8)])
+    y2, S2 = oracle.encode_stream(f2, fp16_bits(np.abs(oracle.phi_values(phi))), 2, 8)
+    assert np.array_equal(y2, S2)
+
+
+def test_check_tolerance_semantics():
+    y = np.array([1.0, 0.0, -2.0])
+    S = np.array([1.0, 0.0, 4.0])
+    ok, st = oracle.check_tolerance(np.array([1.0 + 5e-6, 0.0, -2.0]), y, S)
+    assert ok and st["n_zero_scale"] == 1
+    ok, _ = oracle.check_tolerance(np.array([1.0, 1e-30, -2.0]), y, S)   # S = 0 demands exact 0
+    assert not ok
+    ok, _ = oracle.check_tolerance(np.array([1.0 + 2e-5, 0.0, -2.0]), y, S)
+    assert not ok
