@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""bench.py -- CS-frame Gpixels/s of the fused residual + block-measurement encoder on B200.
+
+Default workload (BASELINE.json configs[3], the config the metric's target is quoted on):
+1080p 1920x1080 uint8, 240 frames, GOP 8, 16x16 blocks, M swept over {16,32,64,128}.  One
+"step" = the whole hot path over that sequence for every M of the sweep (4 kernel launches,
+one per measurement matrix), inputs resident in HBM.  value = CS pixels encoded / second
+(key frames pass through and are not counted), whole job (all ranks).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C4]
+
+Multi-GPU (torchrun): every rank encodes its own independent sequence (weak scaling; GOPs are
+independent, P:87 / SPEC.md:406) -- no data-path collective; a barrier and a MAX all-reduce of
+the device time are the only communication.
+
+--impl reference times the fp64 CPU oracle (oracle/, the slow correctness reference) on a
+bounded sample of the same workload; on N>1 only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+L2_BYTES = 126 * 1024 * 1024
+
+
+def alg_bytes(cfg, M, n_seq):
+    """Algorithmic HBM bytes of one launch: every frame read once + every fp32 measurement
+    written once."""
+    nblk = -(-cfg.W // cfg.B) * -(-cfg.H // cfg.B)
+    n_cs = cfg.T - -(-cfg.T // cfg.G)
+    return n_seq * (cfg.T * cfg.W * cfg.H + n_cs * nblk * M * 4)
+
+
+def cs_pixels(cfg, n_seq):
+    return n_seq * (cfg.T - -(-cfg.T // cfg.G)) * cfg.W * cfg.H
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML while the timed region runs."""
+
+    def __init__(self, device_index: int, period_s: float = 0.01):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.period = period_s
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_traffic(workload):
+    """Per-launch DRAM bytes from the committed ncu --set full summary (profiles/), if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(workload)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------------------ ours
+def run_ours(args, cfg, Ms):
+    import torch
+    import torch.distributed as dist
+    import paper_1311_1419_b200 as P
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    n_seq = cfg.S
+    # rank r encodes its own independent streams (weak scaling)
+    frames_h = synth.gen_video(cfg, streams=range(rank * n_seq, (rank + 1) * n_seq))
+    frames = torch.from_numpy(frames_h).to(dev)
+    encs, outs = [], []
+    for M in Ms:
+        phi = synth.phi_from_seed(synth.phi_seed(), M, cfg.B ** 2)
+        e = P.Encoder(cfg.W, cfg.H, cfg.G, cfg.B, M, phi)
+        encs.append(e)
+        outs.append(torch.empty(e.out_shape(n_seq, cfg.T), dtype=torch.float32, device=dev))
+    stream = torch.cuda.current_stream(dev)
+
+    def step(ev=None):
+        for i, e in enumerate(encs):
+            if ev is not None:
+                ev[i][0].record(stream)
+            e.encode_batch(frames, outs[i], stream)
+            if ev is not None:
+                ev[i][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    K = args.steps
+    evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in Ms]
+           for _ in range(K)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for k in range(K):
+            step(evs[k])
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms_total = t0.elapsed_time(t1)
+    launch_ms = [[evs[k][i][0].elapsed_time(evs[k][i][1]) for k in range(K)] for i in range(len(Ms))]
+    if world > 1:
+        tt = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_total = float(tt.item())
+
+    # ---- end to end through the public host-buffer C-ABI call (copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        pin_in = torch.from_numpy(frames_h).pin_memory()
+        pin_out = [torch.empty(o.shape, dtype=torch.float32).pin_memory() for o in outs]
+        for i, e in enumerate(encs):  # warm-up (workspace allocation)
+            e.encode_batch_host(pin_in, pin_out[i])
+        e2e_steps = max(1, min(args.e2e_steps, K))
+        if world > 1:
+            dist.barrier()
+        w0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            for i, e in enumerate(encs):
+                e.encode_batch_host(pin_in, pin_out[i])
+        w = (time.perf_counter() - w0) / e2e_steps
+        if world > 1:
+            tt = torch.tensor([w], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            w = float(tt.item())
+        h2d = len(Ms) * frames_h.nbytes
+        d2h = sum(o.numel() * 4 for o in outs)
+        e2e = {"value": world * len(Ms) * cs_pixels(cfg, n_seq) / w / 1e9, "unit": "Gpixel/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": w * 1e3,
+               "how": "cs_encode_batch_host (pinned host in/out, H2D+encode+D2H pipelined in GOP groups), "
+                      "wall clock around the synchronous C-ABI call"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return None
+
+    peak, peak_src = load_peaks()
+    per_m = {}
+    tot_bytes, tot_ms = 0.0, 0.0
+    for i, M in enumerate(Ms):
+        med = statistics.median(launch_ms[i])
+        avg = sum(launch_ms[i]) / K
+        b = alg_bytes(cfg, M, n_seq)
+        per_m[str(M)] = {"ms_median": med, "ms_mean": avg,
+                         "gpix_s": cs_pixels(cfg, n_seq) / (avg * 1e-3) / 1e9,
+                         "alg_gbs": b / (avg * 1e-3) / 1e9, "frac_of_peak": b / (avg * 1e-3) / 1e9 / peak,
+                         "alg_bytes": b, "plan": encs[i].plan()}
+        tot_bytes += b
+        tot_ms += avg
+    achieved = tot_bytes / (tot_ms * 1e-3) / 1e9
+    traffic = load_traffic(args.workload)
+    ms_step = ms_total / K
+    value = world * len(Ms) * cs_pixels(cfg, n_seq) / (ms_step * 1e-3) / 1e9
+    in_mb = cfg.T * cfg.W * cfg.H * n_seq / 2 ** 20
+    line = {
+        "metric": "CS-frame Gpixels/s encoded (residual vs GOP key + block measurement Y = Phi R)",
+        "value": value, "unit": "Gpixel/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u8 in, fp16 x fp16 -> fp32 (tensor core kind::f16)", "data": "synthetic (seeded surveillance-like video, synth/)",
+        "config": {"workload": args.workload, "W": cfg.W, "H": cfg.H, "T": cfg.T, "streams_per_gpu": n_seq,
+                   "G": cfg.G, "B": cfg.B, "M": list(Ms),
+                   "l2": f"inputs larger than L2 ({in_mb:.0f} MiB read per launch vs 126 MiB L2); no flush",
+                   "parallelism": f"dp{world} (independent sequences per GPU, no collective)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src,
+                     "kernel": "cs_measure_kernel (all launches of the step; alg bytes = frames read once + fp32 "
+                               "measurements written once)"},
+        "per_M": per_m,
+        "gpu_launches": K * len(Ms),
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, Ms, budget_s=args.cpu_budget)
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return line
+
+
+# ------------------------------------------------------------------------------------ oracle arm
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads") for i in threadpool_info() if i.get("user_api") == "blas"]
+        if n:
+            return int(max(n))
+    except Exception:
+        pass
+    return os.cpu_count() or 1
+
+
+def oracle_sample(cfg, Ms, n_gops=1, seed_stream=0):
+    """Encode the first n_gops GOPs of one stream with the oracle for every M; returns
+    (seconds, CS pixels)."""
+    import oracle
+    T = min(cfg.T, n_gops * cfg.G)
+    frames = synth.gen_stream(cfg, seed_stream, T=T)
+    phis = [synth.phi_from_seed(synth.phi_seed(), M, cfg.B ** 2) for M in Ms]
+    t0 = time.perf_counter()
+    for phi in phis:
+        oracle.encode_stream(frames, phi, cfg.G, cfg.B, with_scale=False)
+    dt = time.perf_counter() - t0
+    px = len(Ms) * (T - -(-T // cfg.G)) * cfg.W * cfg.H
+    return dt, px
+
+
+def cpu_baseline(cfg, Ms, budget_s=15.0):
+    n_gops, dt, px = 1, 0.0, 0
+    while True:
+        dt, px = oracle_sample(cfg, Ms, n_gops)
+        if dt * 2 > budget_s or n_gops * cfg.G >= cfg.T:
+            break
+        n_gops = min(-(-cfg.T // cfg.G), max(n_gops + 1, int(n_gops * budget_s / max(dt, 1e-3) / 2)))
+    return {"value": px / dt / 1e9, "unit": "Gpixel/s", "cores": cpu_threads(), "kind": "oracle",
+            "sample": f"fp64 numpy oracle (y only), first {n_gops} GOP(s) = {px // (cfg.W * cfg.H) // len(Ms)} CS "
+                      f"frames of one {cfg.W}x{cfg.H} stream x M in {list(Ms)}, {dt:.2f} s"}
+
+
+def run_reference(args, cfg, Ms):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return None
+    if args.warmup > 0:  # one untimed pass (page-in, BLAS thread start-up)
+        oracle_sample(cfg, Ms, 1)
+    times, pxs = [], []
+    for _ in range(args.steps):
+        dt, px = oracle_sample(cfg, Ms, 1)
+        times.append(dt)
+        pxs.append(px)
+    ms = 1e3 * sum(times) / len(times)
+    value = sum(pxs) / sum(times) / 1e9
+    cores = cpu_threads()
+    line = {
+        "impl": "reference",
+        "metric": "CS-frame Gpixels/s encoded (residual vs GOP key + block measurement Y = Phi R)",
+        "value": value, "unit": "Gpixel/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded surveillance-like video, synth/)",
+        "config": {"workload": args.workload, "W": cfg.W, "H": cfg.H, "T": cfg.T, "G": cfg.G, "B": cfg.B,
+                   "M": list(Ms), "sample_per_step": "first GOP of one stream, every M"},
+        "cpu_baseline": {"value": value, "unit": "Gpixel/s", "cores": cores, "kind": "oracle",
+                         "sample": "fp64 numpy oracle (y only) on the first GOP of one stream for every M, per step"},
+        "e2e": {"value": value, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line))
+    return line
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="C4", choices=list(synth.CONFIGS))
+    ap.add_argument("--M", default=None, help="comma-separated subset of the config's M values")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        ap.error("--warmup must be >= 3")
+    cfg = synth.CONFIGS[args.workload]
+    Ms = tuple(int(m) for m in args.M.split(",")) if args.M else cfg.Ms
+    if args.impl == "reference":
+        return run_reference(args, cfg, Ms)
+    return run_ours(args, cfg, Ms)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,167 @@
+/*
+ * cs_encoder.h -- C ABI of libcsenc.so, the B200 (sm_100a) encoder hot path of
+ * "Increasing Compression Ratio of Low Complexity Compressive Sensing Video
+ * Encoder with Application-Aware Configurable Mechanism" (arXiv 1311.1419).
+ *
+ * What one encode computes (PAPER.md line numbers, "P:n"):
+ *   For every stream s and GOP g of G frames (sec.3.1 "we divide the source
+ *   video into a key frame and several residual frames"; last GOP may be short),
+ *   every CS frame F_t of the GOP minus the GOP's key frame F_key (sec.3.2
+ *   "The CS frames all subtract the same key frame in a GOP"; Eq.(3) P:91 with
+ *   the key passed through raw, i.e. Eq.(2) with e_coding = e_decoding = 0),
+ *   cut into B x B blocks (block (by,bx) in raster order, pixel j = yy*B + xx
+ *   inside the block; pixels outside the frame count as 0), each block measured
+ *   with the same M x N matrix Phi, N = B*B (Eq.(1): y = A x):
+ *
+ *     y[s][g][c][by][bx][m] = sum_{j<N} Phi[m][j] * (F_{gG+1+c} - F_{gG})[by*B + j/B][bx*B + j%B]
+ *
+ *   Phi is IEEE fp16 (the caller's rounding of N(0,1/M) samples, "A
+ *   Gaussian random matrix is used to make the measurements"); residuals are
+ *   exact integers in [-255,255]; products are exact; accumulation is fp32 on
+ *   the tensor cores.  Output is fp32, block-major, concatenated per stream,
+ *   per GOP, per CS frame:
+ *     meas[((s*CS_s + g*(G-1) + c) * nblk + by*nbx + bx) * M + m],
+ *     CS_s = number of CS frames per stream, nbx = ceil(W/B), nby = ceil(H/B),
+ *     nblk = nby*nbx.
+ *   Accuracy contract: |y_gpu - y_exact| <= 1e-5 * sum_j |Phi[m][j] * r_j| per
+ *   entry (entries whose scale is 0 are exactly 0).
+ *
+ * Conventions: every function returns a status (CS_OK = 0) unless noted; on
+ * failure cs_last_error() returns a thread-local message.  No C++ exception
+ * crosses the ABI.  Device pointers are caller-owned CUDA device memory; host
+ * pointers are caller-owned host memory.  Encodes are asynchronous on the given
+ * stream (cudaStream_t; NULL = legacy default stream); kernel faults surface at
+ * the caller's next synchronisation.  The encoder is immutable after create
+ * (except its internal caches, guarded by a mutex), so concurrent encodes on
+ * different streams are safe.
+ */
+#ifndef CS_ENCODER_H
+#define CS_ENCODER_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cs_encoder cs_encoder;      /* opaque */
+typedef struct CUstream_st* cs_stream_t;   /* == cudaStream_t */
+
+enum {
+    CS_OK = 0,
+    CS_ERR_ARG = 1,          /* bad argument (NULL, out of range, misaligned) */
+    CS_ERR_UNSUPPORTED = 2,  /* valid but unsupported shape (B not in {8,16,32}, W % 16 != 0, M > 256 ...) */
+    CS_ERR_PHI = 3,          /* Phi has a non-finite entry or |entry| > 2048 */
+    CS_ERR_CUDA = 4,         /* CUDA runtime/driver error (message has the CUDA error string) */
+    CS_ERR_OOM = 5           /* device allocation failed */
+};
+
+/* Planner output (read-only diagnostics of how the kernel tiles the work). */
+typedef struct cs_plan_info {
+    int tile_block_rows;   /* block rows per tile (tiles are full-width) */
+    int folds;             /* tile blocks folded onto the 128 TMEM lanes */
+    int lanes;             /* lanes used per fold */
+    int chunk_rows;        /* pixel rows of a block per K-chunk (K-chunk = chunk_rows*B) */
+    int stages;            /* shared-memory ring depth */
+    int key_resident;      /* 1: key tile kept in SMEM per work unit; 0: streamed per chunk */
+    int box_w;             /* TMA box width (pixels) */
+    int smem_bytes;        /* dynamic shared memory per CTA */
+    int tmem_cols;         /* TMEM columns used */
+    int m_pad;             /* MMA N dimension (M rounded up to 16) */
+    int sms;               /* SMs of the device at create time */
+} cs_plan_info;
+
+/* ---- lifecycle ------------------------------------------------------------------------- */
+
+/* Create an encoder for W x H uint8 frames, GOP size gop (>= 1), B x B blocks and M
+ * measurements per block ("the GOP size and the measurement matrix size can be
+ * configured").
+ *   phi_fp16: HOST pointer, M*B*B IEEE fp16 bit patterns, row-major [M][B*B]; copied.
+ *   *out    : receives the encoder; left NULL on failure.
+ * Validation: W,H >= 1; gop >= 1; B in {8,16,32} (else CS_ERR_UNSUPPORTED);
+ * 1 <= M <= min(B*B, 256); W % 16 == 0 (TMA row pitch) else CS_ERR_UNSUPPORTED; Phi is kept
+ * in shared memory, so Mpad*B*B*2 <= 160 KB (Mpad = M rounded up to 16; B = 32 => M <= 80) else
+ * CS_ERR_UNSUPPORTED;
+ * Phi entries finite with |Phi| <= 2048 else CS_ERR_PHI.  Argument validation
+ * happens before any CUDA call.  Allocates the device copy of Phi on the current
+ * device. */
+int cs_encoder_create(int W, int H, int gop, int B, int M, const uint16_t* phi_fp16, cs_encoder** out);
+
+/* Free the encoder and its device memory.  NULL-safe.  The caller must have
+ * synchronised every stream that used it. */
+int cs_encoder_destroy(cs_encoder* enc);
+
+/* Fill *info with the tiling plan.  Host only. */
+int cs_encoder_plan(const cs_encoder* enc, cs_plan_info* info);
+
+/* ---- encode (device buffers; asynchronous) ---------------------------------------------- */
+
+/* Encode one GOP (SPEC.md:355-358 encode_gop): frames_dev = DEVICE [n_frames][H][W] uint8,
+ * 16-byte aligned, frame 0 is the key; 1 <= n_frames <= gop (a short final GOP is allowed).
+ * meas_dev = DEVICE fp32 [n_frames-1][nby][nbx][M], 16-byte aligned.  n_frames == 1 writes
+ * nothing.  One kernel launch on `stream`; no allocation. */
+int cs_encode_gop(cs_encoder* enc, const uint8_t* frames_dev, int n_frames, float* meas_dev, cs_stream_t stream);
+
+/* Encode n_seq independent streams of T frames each: frames_dev = DEVICE [n_seq][T][H][W]
+ * uint8; meas_dev = DEVICE fp32, cs_measurement_count(enc, n_seq, T) floats, layout above.
+ * ONE kernel launch covers every GOP of every stream (persistent grid of one CTA per SM).
+ * No allocation (graph-capturable after the first call for a given (frames_dev, n_seq, T),
+ * which encodes and caches the TMA descriptor on the host). */
+int cs_encode_batch(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, int T, float* meas_dev,
+                    cs_stream_t stream);
+
+/* Same, restricted to GOPs [gop_begin, gop_end) of every stream (GOP index within a stream);
+ * meas_dev receives only those GOPs' measurements, in the same order.  Used to shard a batch
+ * across devices or to pipeline host copies. */
+int cs_encode_batch_gops(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, int T, int gop_begin,
+                         int gop_end, float* meas_dev, cs_stream_t stream);
+
+/* ---- encode (HOST buffers; synchronous) ------------------------------------------------- */
+
+/* End-to-end call: frames_host = HOST [n_seq][T][H][W] uint8, meas_host = HOST fp32 output
+ * (cs_measurement_count floats).  Copies in, encodes, copies out, and returns after the
+ * result is in meas_host.  Pinned host memory gives full PCIe bandwidth; pageable works.
+ * Work is split into GOP groups and the host<->device copies of one group overlap the
+ * encode of another (internal streams and device workspace, allocated on first use and
+ * kept until destroy). */
+int cs_encode_batch_host(cs_encoder* enc, const uint8_t* frames_host, int n_seq, int T, float* meas_host);
+
+/* ---- accounting (host only) ------------------------------------------------------------- */
+
+/* Number of fp32 measurements cs_encode_batch writes for n_seq streams of T frames
+ * (-1 on bad arguments). */
+int64_t cs_measurement_count(const cs_encoder* enc, int n_seq, int T);
+
+/* CR = original bits / (key-frame bits + measurement bits) (BASELINE.json north_star;
+ * Table I).  T = 0 means one full GOP; key_cr = 1.0 means raw key frames;
+ * bits_per_measurement = 8 is the paper's sample-count convention (CR_cs = n/m),
+ * 32 gives the realised fp32 payload ratio.  Uses the real GOP composition and counts
+ * padded blocks.  Returns a negative value on bad arguments. */
+double cs_compression_ratio(const cs_encoder* enc, int T, double key_cr, int bits_per_measurement);
+
+/* Same accounting without an encoder (pure host arithmetic). */
+double cs_compression_ratio_cfg(int W, int H, int gop, int B, int M, int T, double key_cr,
+                                int bits_per_measurement);
+int64_t cs_measurement_count_cfg(int W, int H, int gop, int B, int M, int n_seq, int T);
+
+/* Table I closed form: G / (1/key_cr + (G-1)/cs_cr). Negative on bad arguments. */
+double cs_total_cr(int G, double key_cr, double cs_cr);
+
+/* Validate a configuration exactly as cs_encoder_create does, without touching CUDA.
+ * phi_fp16 may be NULL (then Phi is not checked). */
+int cs_validate_config(int W, int H, int gop, int B, int M, const uint16_t* phi_fp16);
+
+/* Planner without an encoder (pure host): the plan cs_encoder_create would pick on a device
+ * with `smem_limit` bytes of opt-in shared memory per block and `sms` SMs (B200: 232448, 148). */
+int cs_plan_cfg(int W, int H, int gop, int B, int M, int smem_limit, int sms, cs_plan_info* info);
+
+/* Thread-local message for the last non-OK status on this thread ("" if none). */
+const char* cs_last_error(void);
+
+/* Library version string. */
+const char* cs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CS_ENCODER_H */

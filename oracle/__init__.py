@@ -142,6 +142,30 @@ def encode(frames: np.ndarray, phi_bits: np.ndarray, G: int, B: int, with_scale:
     return y, (np.concatenate(Ss, axis=0) if with_scale else None)
 
 
+def measure_entries(frames: np.ndarray, phi_bits: np.ndarray, G: int, B: int, cs_index: np.ndarray,
+                    blocks: np.ndarray):
+    """y and S for selected (CS frame, block) pairs of one stream, one by one from the
+    definition (for full-size parity where encoding everything on the CPU is too slow).
+    cs_index: indices into the stream's CS-frame order (a1); blocks: raster block indices.
+    Returns fp64 arrays [len][M]."""
+    T, H, W = frames.shape
+    phi = phi_values(phi_bits)
+    nby, nbx = block_grid(W, H, B)
+    order = [(k, t) for k, cs in gop_partition(T, G) for t in cs]
+    ys, Ss = [], []
+    for i, b in zip(np.asarray(cs_index).ravel(), np.asarray(blocks).ravel()):
+        key_t, t = order[int(i)]
+        by, bx = divmod(int(b), nbx)
+        blk = np.zeros((B, B), dtype=np.int64)
+        y0, x0 = by * B, bx * B
+        h, w = min(B, H - y0), min(B, W - x0)
+        blk[:h, :w] = residual(frames[t, y0:y0 + h, x0:x0 + w], frames[key_t, y0:y0 + h, x0:x0 + w])
+        r = blk.reshape(1, B * B)
+        ys.append(measure(r, phi)[0])
+        Ss.append(tolerance_scale(r, phi)[0])
+    return np.asarray(ys), np.asarray(Ss)
+
+
 # -- a7 ------------------------------------------------------------------------------------------
 def compression_ratio(W: int, H: int, G: int, B: int, M: int, T: int = 0, key_cr: float = 1.0,
                       bits_per_measurement: int = 8) -> float:

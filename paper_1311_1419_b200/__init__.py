@@ -1,0 +1,213 @@
+"""paper_1311_1419_b200 -- B200-native encoder hot path of arXiv 1311.1419 (CS surveillance video).
+
+Thin Python binding over the C ABI in ``include/cs_encoder.h`` (libcsenc.so): argument
+marshalling only.  Every step of the path (GOP partition, block loads, residual, measurement,
+output) runs in the sm_100a kernel; there is no CPU fallback -- importing this package without
+the built library raises, and encoding on a machine without a B200 returns an error.
+
+PyTorch is used for device memory and streams only: ``Encoder.encode_batch`` takes CUDA uint8
+frame tensors and fills a CUDA float32 tensor on the current (or given) stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from ._build import LIB, build as build_library
+
+__all__ = ["Encoder", "CSError", "total_cr", "compression_ratio_cfg", "measurement_count_cfg", "plan_cfg",
+           "validate_config", "lib", "LIB", "build_library", "version"]
+
+CS_OK, CS_ERR_ARG, CS_ERR_UNSUPPORTED, CS_ERR_PHI, CS_ERR_CUDA, CS_ERR_OOM = range(6)
+_ERR_NAMES = {1: "CS_ERR_ARG", 2: "CS_ERR_UNSUPPORTED", 3: "CS_ERR_PHI", 4: "CS_ERR_CUDA", 5: "CS_ERR_OOM"}
+
+
+class CSError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_ERR_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in (
+        "tile_block_rows", "folds", "lanes", "chunk_rows", "stages", "key_resident", "box_w", "smem_bytes",
+        "tmem_cols", "m_pad", "sms")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libcsenc.so (raises if it was not built: no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise ImportError(f"libcsenc.so not built ({LIB}); run paper_1311_1419_b200.build_library() "
+                              "or __graft_entry__.build()")
+        L = ctypes.CDLL(LIB)
+        c_int, c_i64, c_dbl, vp = ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
+        sig = {
+            "cs_encoder_create": (c_int, [c_int, c_int, c_int, c_int, c_int, vp, ctypes.POINTER(vp)]),
+            "cs_encoder_destroy": (c_int, [vp]),
+            "cs_encoder_plan": (c_int, [vp, ctypes.POINTER(PlanInfo)]),
+            "cs_encode_gop": (c_int, [vp, vp, c_int, vp, vp]),
+            "cs_encode_batch": (c_int, [vp, vp, c_int, c_int, vp, vp]),
+            "cs_encode_batch_gops": (c_int, [vp, vp, c_int, c_int, c_int, c_int, vp, vp]),
+            "cs_encode_batch_host": (c_int, [vp, vp, c_int, c_int, vp]),
+            "cs_measurement_count": (c_i64, [vp, c_int, c_int]),
+            "cs_compression_ratio": (c_dbl, [vp, c_int, c_dbl, c_int]),
+            "cs_compression_ratio_cfg": (c_dbl, [c_int, c_int, c_int, c_int, c_int, c_int, c_dbl, c_int]),
+            "cs_measurement_count_cfg": (c_i64, [c_int] * 7),
+            "cs_total_cr": (c_dbl, [c_int, c_dbl, c_dbl]),
+            "cs_validate_config": (c_int, [c_int] * 5 + [vp]),
+            "cs_plan_cfg": (c_int, [c_int] * 7 + [ctypes.POINTER(PlanInfo)]),
+            "cs_last_error": (ctypes.c_char_p, []),
+            "cs_version": (ctypes.c_char_p, []),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype, fn.argtypes = res, args
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != CS_OK:
+        raise CSError(rc, lib().cs_last_error().decode())
+
+
+def version() -> str:
+    return lib().cs_version().decode()
+
+
+def total_cr(G: int, key_cr: float, cs_cr: float) -> float:
+    return lib().cs_total_cr(G, key_cr, cs_cr)
+
+
+def compression_ratio_cfg(W, H, gop, B, M, T=0, key_cr=1.0, bits_per_measurement=8) -> float:
+    return lib().cs_compression_ratio_cfg(W, H, gop, B, M, T, key_cr, bits_per_measurement)
+
+
+def measurement_count_cfg(W, H, gop, B, M, n_seq, T) -> int:
+    return lib().cs_measurement_count_cfg(W, H, gop, B, M, n_seq, T)
+
+
+def validate_config(W, H, gop, B, M, phi_bits=None) -> int:
+    """Status code of cs_validate_config (0 = OK)."""
+    if phi_bits is None:
+        return lib().cs_validate_config(W, H, gop, B, M, None)
+    phi = np.ascontiguousarray(phi_bits, dtype=np.uint16)
+    return lib().cs_validate_config(W, H, gop, B, M, phi.ctypes.data)
+
+
+def plan_cfg(W, H, gop, B, M, smem_limit=232448, sms=148) -> dict:
+    info = PlanInfo()
+    _check(lib().cs_plan_cfg(W, H, gop, B, M, smem_limit, sms, ctypes.byref(info)))
+    return info.as_dict()
+
+
+def _ptr(t) -> int:
+    return int(t.data_ptr())
+
+
+def _stream_handle(stream) -> int:
+    if stream is None:
+        import torch
+        return int(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return stream
+    return int(stream.cuda_stream)
+
+
+class Encoder:
+    """cs_encoder_create(W, H, gop, B, M, phi) -- phi: uint16 [M][B*B] fp16 bit patterns (host)."""
+
+    def __init__(self, W: int, H: int, gop: int, B: int, M: int, phi_bits):
+        phi = np.ascontiguousarray(phi_bits, dtype=np.uint16)
+        if phi.shape != (M, B * B):
+            raise ValueError(f"phi must have shape ({M}, {B * B}), got {phi.shape}")
+        self.W, self.H, self.G, self.B, self.M = W, H, gop, B, M
+        self.nbx, self.nby = -(-W // B), -(-H // B)
+        self.nblk = self.nbx * self.nby
+        h = ctypes.c_void_p()
+        _check(lib().cs_encoder_create(W, H, gop, B, M, phi.ctypes.data, ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().cs_encoder_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- accounting
+    def plan(self) -> dict:
+        info = PlanInfo()
+        _check(lib().cs_encoder_plan(self._h, ctypes.byref(info)))
+        return info.as_dict()
+
+    def measurement_count(self, n_seq: int, T: int) -> int:
+        return lib().cs_measurement_count(self._h, n_seq, T)
+
+    def compression_ratio(self, T: int = 0, key_cr: float = 1.0, bits_per_measurement: int = 8) -> float:
+        return lib().cs_compression_ratio(self._h, T, key_cr, bits_per_measurement)
+
+    def out_shape(self, n_seq: int, T: int):
+        n_cs = n_seq * (T - -(-T // self.G))
+        return (n_cs, self.nblk, self.M)
+
+    # -- encode (device tensors)
+    def encode_batch(self, frames, out=None, stream=None):
+        """frames: CUDA uint8 [n_seq][T][H][W] (contiguous); returns CUDA float32 [n_cs][nblk][M]."""
+        import torch
+        assert frames.is_cuda and frames.dtype == torch.uint8 and frames.is_contiguous()
+        n_seq, T, H, W = frames.shape
+        assert (H, W) == (self.H, self.W)
+        if out is None:
+            out = torch.empty(self.out_shape(n_seq, T), dtype=torch.float32, device=frames.device)
+        assert out.is_cuda and out.dtype == torch.float32 and out.is_contiguous()
+        assert out.numel() >= self.measurement_count(n_seq, T)
+        _check(lib().cs_encode_batch(self._h, _ptr(frames), n_seq, T, _ptr(out), _stream_handle(stream)))
+        return out
+
+    def encode_batch_gops(self, frames, gop_begin: int, gop_end: int, out, stream=None):
+        n_seq, T = frames.shape[:2]
+        _check(lib().cs_encode_batch_gops(self._h, _ptr(frames), n_seq, T, gop_begin, gop_end, _ptr(out),
+                                          _stream_handle(stream)))
+        return out
+
+    def encode_gop(self, frames, out=None, stream=None):
+        """frames: CUDA uint8 [n][H][W], 1 <= n <= gop, frame 0 = key; returns [n-1][nblk][M]."""
+        import torch
+        n = frames.shape[0]
+        if out is None:
+            out = torch.empty((max(n - 1, 0), self.nblk, self.M), dtype=torch.float32, device=frames.device)
+        _check(lib().cs_encode_gop(self._h, _ptr(frames), n, _ptr(out), _stream_handle(stream)))
+        return out
+
+    # -- encode (host buffers)
+    def encode_batch_host(self, frames, out=None):
+        """frames: host uint8 [n_seq][T][H][W] (numpy or CPU tensor, pinned for full bandwidth);
+        copies in, encodes, copies out; returns host float32 [n_cs][nblk][M]."""
+        n_seq, T = frames.shape[:2]
+        if out is None:
+            out = np.empty(self.out_shape(n_seq, T), dtype=np.float32)
+        fp = frames.ctypes.data if isinstance(frames, np.ndarray) else _ptr(frames)
+        op = out.ctypes.data if isinstance(out, np.ndarray) else _ptr(out)
+        _check(lib().cs_encode_batch_host(self._h, fp, n_seq, T, op))
+        return out

@@ -1,0 +1,664 @@
+// cs_encoder.cu -- libcsenc.so: C ABI (include/cs_encoder.h), planner, TMA descriptors, launch.
+//
+// Host logic only; the device work is the single kernel in cs_measure_kernel.cuh.  No CPU
+// fallback exists: every encode runs the sm_100a kernel or returns an error.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/cs_encoder.h"
+#include "cs_measure_kernel.cuh"
+
+using csenc::KParams;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(CS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+constexpr long kMaxPhiBytes = 160 * 1024;  // Phi is SMEM-resident for the whole kernel
+
+inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
+
+float half_bits_to_float(uint16_t h) {
+    uint32_t s = (h >> 15) & 1u, e = (h >> 10) & 0x1Fu, m = h & 0x3FFu;
+    float v;
+    if (e == 0)
+        v = std::ldexp((float)m, -24);
+    else if (e == 31)
+        v = m ? NAN : INFINITY;
+    else
+        v = std::ldexp((float)(m | 0x400u), (int)e - 25);
+    return s ? -v : v;
+}
+
+// ------------------------------------------------------------------------------------ planner
+struct Plan {
+    int T_r = 0, F = 0, L = 0, n_tiles = 0;
+    int chunk_rows = 0, n_chunks = 0, chunk_k = 0;
+    int box_w = 0, n_box = 0, box_rows = 0, pieces = 0, single_piece = 0;
+    uint32_t box_bytes = 0, stage_cs_bytes = 0, stage_bytes = 0, key_bytes = 0;
+    int key_resident = 0, n_stages = 0;
+    uint32_t off_phi = 0, off_key = 0, off_stage = 0, smem_bytes = 0;
+    int a_cols = 0, d_cols = 0, tmem_cols = 0, n_abuf = 2, n_dbuf = 2;
+    double score = -1.0;
+};
+
+struct Geometry {
+    int W, H, G, B, M, N, Mpad, nbx, nby, nblk;
+};
+
+int pick_box_w(const Geometry& g) {
+    // multiple of lcm(16, B), <= 256; prefer exact cover of nbx*B, then fewest boxes
+    const int unit = std::max(16, g.B);
+    const int need = g.nbx * g.B;
+    int best = unit, best_waste = 1 << 30, best_n = 1 << 30;
+    for (int bw = unit; bw <= 256; bw += unit) {
+        int n = cdiv(need, bw);
+        int waste = n * bw - need;
+        if (waste < best_waste || (waste == best_waste && n < best_n)) {
+            best = bw;
+            best_waste = waste;
+            best_n = n;
+        }
+    }
+    return best;
+}
+
+bool try_plan(const Geometry& g, int T_r, int chunk_rows, bool key_res, int smem_limit, Plan& p) {
+    p = Plan();
+    const int words = g.B / 2;          // fp16x2 columns per pixel row
+    const int rows_per_st = 32 / words;
+    if (g.B % chunk_rows != 0 || chunk_rows % rows_per_st != 0) return false;
+    if ((chunk_rows * g.B) % 16 != 0) return false;
+    const int tile_blocks = T_r * g.nbx;
+    p.T_r = T_r;
+    p.F = cdiv(tile_blocks, 128);
+    if (p.F > csenc::kMaxFolds) return false;
+    p.L = cdiv(tile_blocks, p.F);
+    p.n_tiles = cdiv(g.nby, T_r);
+    p.chunk_rows = chunk_rows;
+    p.n_chunks = g.B / chunk_rows;
+    p.chunk_k = chunk_rows * g.B;
+    p.a_cols = p.F * p.chunk_k / 2;
+    p.d_cols = p.F * g.Mpad;
+    p.n_abuf = 2;
+    p.n_dbuf = 2;
+    if (2 * p.a_cols + 2 * p.d_cols > (int)csenc::kTmemCols) p.n_dbuf = 1;  // large M: one accumulator
+    p.tmem_cols = p.n_abuf * p.a_cols + p.n_dbuf * p.d_cols;
+    if (p.tmem_cols > (int)csenc::kTmemCols) return false;
+    p.box_w = pick_box_w(g);
+    p.n_box = cdiv(g.nbx * g.B, p.box_w);
+    if (p.n_chunks == 1 && T_r * g.B <= 256) {
+        p.pieces = 1;
+        p.single_piece = 1;
+        p.box_rows = T_r * g.B;
+    } else {
+        p.pieces = T_r;
+        p.box_rows = chunk_rows;
+    }
+    if (p.box_rows > 256) return false;
+    p.box_bytes = align_up((uint32_t)(p.box_rows * p.box_w), 128);
+    p.stage_cs_bytes = (uint32_t)(p.pieces * p.n_box) * p.box_bytes;
+    p.key_resident = key_res ? 1 : 0;
+    p.key_bytes = key_res ? (uint32_t)p.n_chunks * p.stage_cs_bytes : 0;
+    p.stage_bytes = key_res ? p.stage_cs_bytes : 2 * p.stage_cs_bytes;
+    const uint32_t phi_bytes = (uint32_t)g.Mpad * (uint32_t)g.N * 2u;
+    p.off_phi = 1024;  // barriers live in the first KB
+    p.off_key = align_up(p.off_phi + phi_bytes, 1024);
+    p.off_stage = align_up(p.off_key + 2 * p.key_bytes, 1024);
+    const long avail = (long)smem_limit - 1024 /*alignment slack*/ - (long)p.off_stage;
+    if (avail < (long)p.stage_bytes * 2) return false;
+    p.n_stages = (int)std::min<long>(csenc::kMaxStages, avail / p.stage_bytes);
+    p.smem_bytes = p.off_stage + (uint32_t)p.n_stages * p.stage_bytes + 1024;
+    // score: lane utilisation x key residency x bytes in flight x per-stage overhead
+    const double util = (double)tile_blocks / (p.F * 128.0);
+    const double inflight = (double)(p.n_stages - 1) * p.stage_cs_bytes;
+    double s = util * (key_res ? 1.0 : 0.8) * std::min(1.0, inflight / 98304.0);
+    s *= std::min(1.0, p.stage_cs_bytes / 12288.0);
+    if (p.n_stages < 3) s *= 0.7;
+    if (p.n_dbuf < 2) s *= 0.8;
+    s *= 1.0 + 1e-3 * chunk_rows;  // tie-break: fewer, larger pipeline handoffs
+    p.score = s;
+    return true;
+}
+
+bool make_plan(const Geometry& g, int smem_limit, Plan& best) {
+    best = Plan();
+    for (int T_r = 1; T_r <= g.nby; ++T_r) {
+        if (T_r * g.nbx > 128 * csenc::kMaxFolds) break;
+        for (int cr = g.B; cr >= 1; --cr) {
+            for (int kr = 1; kr >= 0; --kr) {
+                Plan p;
+                if (!try_plan(g, T_r, cr, kr == 1, smem_limit, p)) continue;
+                if (p.score > best.score + 1e-9) best = p;
+            }
+        }
+    }
+    return best.score > 0;
+}
+
+struct WorkSplit {
+    int n_splits, cs_per_unit, n_units;
+};
+
+WorkSplit choose_split(const Geometry& g, const Plan& p, int n_seq, int n_gops_sel, int sms) {
+    const long base = (long)n_seq * n_gops_sel * p.n_tiles;
+    WorkSplit best{1, std::max(1, g.G - 1), (int)base};
+    if (g.G <= 1) return best;
+    double best_cost = 1e300;
+    const double key_cost = p.key_resident ? 1.0 : 0.0;
+    for (int ns = 1; ns <= g.G - 1; ++ns) {
+        int cpu = cdiv(g.G - 1, ns);
+        if (ns > 1 && cdiv(g.G - 1, cpu) != ns) continue;  // identical to a smaller ns
+        long units = base * ns;
+        if (units > (1L << 30)) break;
+        double rounds = std::ceil((double)units / sms);
+        double cost = rounds * (cpu + key_cost);
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best = WorkSplit{ns, cpu, (int)units};
+        }
+    }
+    return best;
+}
+
+// ------------------------------------------------------------------------- driver entry point
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encode_tiled() {
+    static PFN_encodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(ptr);
+    });
+    return fn;
+}
+
+int validate(int W, int H, int gop, int B, int M, const uint16_t* phi) {
+    if (W < 1 || H < 1 || gop < 1 || M < 1) return fail(CS_ERR_ARG, "W, H, gop and M must be >= 1");
+    if (B != 8 && B != 16 && B != 32) return fail(CS_ERR_UNSUPPORTED, "B must be 8, 16 or 32");
+    if (M > B * B) return fail(CS_ERR_ARG, "M must be <= N = B*B");
+    if (M > 256) return fail(CS_ERR_UNSUPPORTED, "M must be <= 256 (UMMA N limit)");
+    if (W % 16 != 0) return fail(CS_ERR_UNSUPPORTED, "W must be a multiple of 16 (TMA row pitch)");
+    {
+        const long mpad = std::max(16, (M + 15) / 16 * 16);
+        if (mpad * B * B * 2 > kMaxPhiBytes)
+            return fail(CS_ERR_UNSUPPORTED, "Phi (Mpad*B*B fp16) must fit in 160 KB of shared memory (B=32: M <= 80)");
+    }
+    if ((long long)W * H > (1LL << 31)) return fail(CS_ERR_UNSUPPORTED, "frame too large");
+    if (phi) {
+        for (long i = 0; i < (long)M * B * B; ++i) {
+            float v = half_bits_to_float(phi[i]);
+            if (!std::isfinite(v) || std::fabs(v) > 2048.0f)
+                return fail(CS_ERR_PHI, "Phi entries must be finite with |Phi| <= 2048");
+        }
+    }
+    return CS_OK;
+}
+
+Geometry make_geometry(int W, int H, int gop, int B, int M) {
+    Geometry g;
+    g.W = W;
+    g.H = H;
+    g.G = gop;
+    g.B = B;
+    g.M = M;
+    g.N = B * B;
+    g.Mpad = std::max(16, (M + 15) / 16 * 16);
+    g.nbx = cdiv(W, B);
+    g.nby = cdiv(H, B);
+    g.nblk = g.nbx * g.nby;
+    return g;
+}
+
+long long cs_frames_per_stream(int T, int G) { return (long long)T - cdiv(T, G); }
+long long cs_frames_in_gops(int T, int G, int g0, int g1) {
+    long long n = 0;
+    for (int g = g0; g < g1; ++g) n += std::max(0, std::min(G, T - g * G) - 1);
+    return n;
+}
+
+double cr_formula(const Geometry& g, int T, double key_cr, int bits) {
+    if (T == 0) T = g.G;
+    const long long n_key = cdiv(T, g.G);
+    const long long n_cs = (long long)T - n_key;
+    const double orig = (double)T * g.W * g.H * 8.0;
+    const double key_bits = (double)n_key * g.W * g.H * 8.0 / key_cr;
+    const double meas_bits = (double)n_cs * g.nblk * g.M * (double)bits;
+    return orig / (key_bits + meas_bits);
+}
+
+}  // namespace
+
+// ====================================================================================== encoder
+struct cs_encoder {
+    Geometry geo{};
+    Plan plan{};
+    int device = 0;
+    int sms = 0;
+    int smem_limit = 0;
+    void* phi_dev = nullptr;
+    uint32_t phi_bytes = 0;
+    uint32_t idesc = 0, lbo = 0, sbo = 0;
+    std::mutex mu;     // tensor-map cache
+    std::mutex ws_mu;  // host-path workspace
+    struct MapEntry {
+        const void* ptr;
+        long long n_frames;
+        CUtensorMap map;
+    };
+    std::vector<MapEntry> maps;  // small LRU of tensor maps
+    // host-path workspace
+    uint8_t* ws_frames = nullptr;
+    float* ws_out = nullptr;
+    size_t ws_frames_bytes = 0, ws_out_bytes = 0;
+    cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
+    std::vector<cudaEvent_t> hev;
+};
+
+namespace {
+
+int get_tmap(cs_encoder* e, const uint8_t* frames, long long n_frames, CUtensorMap* out) {
+    std::lock_guard<std::mutex> lk(e->mu);
+    for (auto& m : e->maps)
+        if (m.ptr == frames && m.n_frames == n_frames) {
+            *out = m.map;
+            return CS_OK;
+        }
+    PFN_encodeTiled enc = get_encode_tiled();
+    if (!enc) return fail(CS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const Geometry& g = e->geo;
+    const Plan& p = e->plan;
+    CUtensorMap map;
+    cuuint64_t dims[3] = {(cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)n_frames};
+    cuuint64_t strides[2] = {(cuuint64_t)g.W, (cuuint64_t)g.W * (cuuint64_t)g.H};
+    cuuint32_t box[3] = {(cuuint32_t)p.box_w, (cuuint32_t)p.box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(frames), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(CS_ERR_CUDA, "cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
+    if (e->maps.size() >= 16) e->maps.erase(e->maps.begin());
+    e->maps.push_back({frames, n_frames, map});
+    *out = map;
+    return CS_OK;
+}
+
+int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g1, float* out, cudaStream_t stream) {
+    const Geometry& g = e->geo;
+    const Plan& pl = e->plan;
+    if (g1 <= g0 || g.G == 1) return CS_OK;
+    if (cs_frames_in_gops(T, g.G, g0, g1) == 0) return CS_OK;
+    CUtensorMap map;
+    int rc = get_tmap(e, frames, (long long)n_seq * T, &map);
+    if (rc != CS_OK) return rc;
+    KParams kp;
+    std::memset(&kp, 0, sizeof(kp));
+    kp.out = out;
+    kp.phi = (const uint16_t*)e->phi_dev;
+    kp.phi_bytes = e->phi_bytes;
+    kp.M = g.M;
+    kp.Mpad = g.Mpad;
+    kp.N = g.N;
+    kp.nbx = g.nbx;
+    kp.nby = g.nby;
+    kp.nblk = g.nblk;
+    kp.T_r = pl.T_r;
+    kp.F = pl.F;
+    kp.L = pl.L;
+    kp.n_tiles = pl.n_tiles;
+    kp.chunk_rows = pl.chunk_rows;
+    kp.n_chunks = pl.n_chunks;
+    kp.chunk_k = pl.chunk_k;
+    kp.box_w = pl.box_w;
+    kp.n_box = pl.n_box;
+    kp.box_rows = pl.box_rows;
+    kp.pieces = pl.pieces;
+    kp.single_piece = pl.single_piece;
+    kp.box_bytes = pl.box_bytes;
+    kp.stage_cs_bytes = pl.stage_cs_bytes;
+    kp.stage_bytes = pl.stage_bytes;
+    kp.key_bytes = pl.key_bytes;
+    kp.key_resident = pl.key_resident;
+    kp.n_stages = pl.n_stages;
+    kp.off_phi = pl.off_phi;
+    kp.off_key = pl.off_key;
+    kp.off_stage = pl.off_stage;
+    kp.G = g.G;
+    kp.T = T;
+    kp.gop_begin = g0;
+    kp.n_gops_sel = g1 - g0;
+    kp.cs_per_stream_sel = (int)cs_frames_in_gops(T, g.G, g0, g1);
+    WorkSplit ws = choose_split(g, pl, n_seq, g1 - g0, e->sms);
+    kp.n_splits = ws.n_splits;
+    kp.cs_per_unit = ws.cs_per_unit;
+    kp.n_units = ws.n_units;
+    kp.idesc = e->idesc;
+    kp.lbo = e->lbo;
+    kp.sbo = e->sbo;
+    kp.a_cols = pl.a_cols;
+    kp.d_cols = pl.d_cols;
+    kp.n_abuf = pl.n_abuf;
+    kp.n_dbuf = pl.n_dbuf;
+    const int grid = std::max(1, std::min(e->sms, kp.n_units));
+    cudaError_t err;
+    switch (g.B) {
+        case 8:
+            csenc::cs_measure_kernel<8><<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(map, kp);
+            break;
+        case 16:
+            csenc::cs_measure_kernel<16><<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(map, kp);
+            break;
+        default:
+            csenc::cs_measure_kernel<32><<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(map, kp);
+            break;
+    }
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return cuda_fail(err, "kernel launch");
+    return CS_OK;
+}
+
+template <int B>
+cudaError_t set_smem_attr(int bytes) {
+    return cudaFuncSetAttribute(csenc::cs_measure_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+// ============================================================================================ ABI
+extern "C" {
+
+const char* cs_last_error(void) { return g_err.c_str(); }
+const char* cs_version(void) { return "csenc 0.1 (sm_100a, tcgen05/TMEM/TMA)"; }
+
+int cs_validate_config(int W, int H, int gop, int B, int M, const uint16_t* phi_fp16) {
+    return validate(W, H, gop, B, M, phi_fp16);
+}
+
+double cs_total_cr(int G, double key_cr, double cs_cr) {
+    if (G < 1 || !(key_cr > 0) || !(cs_cr > 0)) return -1.0;
+    return (double)G / (1.0 / key_cr + (double)(G - 1) / cs_cr);
+}
+
+double cs_compression_ratio_cfg(int W, int H, int gop, int B, int M, int T, double key_cr, int bits) {
+    if (W < 1 || H < 1 || gop < 1 || B < 1 || M < 1 || T < 0 || !(key_cr > 0) || bits < 1) return -1.0;
+    return cr_formula(make_geometry(W, H, gop, B, M), T, key_cr, bits);
+}
+
+int64_t cs_measurement_count_cfg(int W, int H, int gop, int B, int M, int n_seq, int T) {
+    if (W < 1 || H < 1 || gop < 1 || B < 1 || M < 1 || n_seq < 0 || T < 0) return -1;
+    Geometry g = make_geometry(W, H, gop, B, M);
+    return (int64_t)n_seq * cs_frames_per_stream(T, gop) * g.nblk * M;
+}
+
+int cs_encoder_create(int W, int H, int gop, int B, int M, const uint16_t* phi_fp16, cs_encoder** out) {
+    if (!out) return fail(CS_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (!phi_fp16) return fail(CS_ERR_ARG, "phi is NULL");
+    int rc = validate(W, H, gop, B, M, phi_fp16);
+    if (rc != CS_OK) return rc;
+    cs_encoder* e = new (std::nothrow) cs_encoder();
+    if (!e) return fail(CS_ERR_OOM, "host allocation failed");
+    e->geo = make_geometry(W, H, gop, B, M);
+    cudaError_t err = cudaGetDevice(&e->device);
+    if (err != cudaSuccess) {
+        delete e;
+        return cuda_fail(err, "cudaGetDevice");
+    }
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, e->device);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, e->device);
+    if (major != 10 || minor != 0) {
+        delete e;
+        return fail(CS_ERR_UNSUPPORTED, "device is not sm_100 (B200); this library is built for sm_100a only");
+    }
+    cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, e->device);
+    cudaDeviceGetAttribute(&e->smem_limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device);
+    if (!make_plan(e->geo, e->smem_limit, e->plan)) {
+        delete e;
+        return fail(CS_ERR_UNSUPPORTED, "no tiling fits shared memory / TMEM for this configuration");
+    }
+    switch (B) {
+        case 8: err = set_smem_attr<8>((int)e->plan.smem_bytes); break;
+        case 16: err = set_smem_attr<16>((int)e->plan.smem_bytes); break;
+        default: err = set_smem_attr<32>((int)e->plan.smem_bytes); break;
+    }
+    if (err != cudaSuccess) {
+        delete e;
+        return cuda_fail(err, "cudaFuncSetAttribute");
+    }
+    // Phi -> canonical no-swizzle K-major UMMA layout, zero-padded to Mpad rows:
+    //   byte(n, k) = (k/8)*LBO + (n/8)*SBO + (n%8)*16 + (k%8)*2,  SBO = 128, LBO = Mpad*16.
+    const Geometry& g = e->geo;
+    e->sbo = 128;
+    e->lbo = (uint32_t)g.Mpad * 16u;
+    e->phi_bytes = (uint32_t)g.Mpad * (uint32_t)g.N * 2u;
+    std::vector<uint16_t> arranged((size_t)g.Mpad * g.N, 0);
+    for (int n = 0; n < M; ++n)
+        for (int k = 0; k < g.N; ++k) {
+            size_t byte = (size_t)(k / 8) * e->lbo + (size_t)(n / 8) * e->sbo + (size_t)(n % 8) * 16 + (size_t)(k % 8) * 2;
+            arranged[byte / 2] = phi_fp16[(size_t)n * g.N + k];
+        }
+    // instruction descriptor, kind::f16: D fp32 (bit 4), A/B fp16 (0), K-major (0),
+    // N>>3 at bits 17-22, M>>4 at bits 24-28 (M = 128 lanes).
+    e->idesc = (1u << 4) | ((uint32_t)(g.Mpad >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    err = cudaMalloc(&e->phi_dev, e->phi_bytes);
+    if (err != cudaSuccess) {
+        delete e;
+        return fail(CS_ERR_OOM, std::string("cudaMalloc(Phi): ") + cudaGetErrorString(err));
+    }
+    err = cudaMemcpy(e->phi_dev, arranged.data(), e->phi_bytes, cudaMemcpyHostToDevice);
+    if (err != cudaSuccess) {
+        cudaFree(e->phi_dev);
+        delete e;
+        return cuda_fail(err, "cudaMemcpy(Phi)");
+    }
+    *out = e;
+    return CS_OK;
+}
+
+int cs_encoder_destroy(cs_encoder* e) {
+    if (!e) return CS_OK;
+    if (e->phi_dev) cudaFree(e->phi_dev);
+    if (e->ws_frames) cudaFree(e->ws_frames);
+    if (e->ws_out) cudaFree(e->ws_out);
+    for (auto& s : e->hs)
+        if (s) cudaStreamDestroy(s);
+    for (auto& ev : e->hev) cudaEventDestroy(ev);
+    delete e;
+    return CS_OK;
+}
+
+static void fill_info(const Plan& p, const Geometry& g, int sms, cs_plan_info* info) {
+    info->tile_block_rows = p.T_r;
+    info->folds = p.F;
+    info->lanes = p.L;
+    info->chunk_rows = p.chunk_rows;
+    info->stages = p.n_stages;
+    info->key_resident = p.key_resident;
+    info->box_w = p.box_w;
+    info->smem_bytes = (int)p.smem_bytes;
+    info->tmem_cols = p.tmem_cols;
+    info->m_pad = g.Mpad;
+    info->sms = sms;
+}
+
+int cs_plan_cfg(int W, int H, int gop, int B, int M, int smem_limit, int sms, cs_plan_info* info) {
+    if (!info) return fail(CS_ERR_ARG, "NULL argument");
+    int rc = validate(W, H, gop, B, M, nullptr);
+    if (rc != CS_OK) return rc;
+    Geometry g = make_geometry(W, H, gop, B, M);
+    Plan p;
+    if (!make_plan(g, smem_limit, p)) return fail(CS_ERR_UNSUPPORTED, "no tiling fits shared memory / TMEM");
+    fill_info(p, g, sms, info);
+    return CS_OK;
+}
+
+int cs_encoder_plan(const cs_encoder* e, cs_plan_info* info) {
+    if (!e || !info) return fail(CS_ERR_ARG, "NULL argument");
+    fill_info(e->plan, e->geo, e->sms, info);
+    return CS_OK;
+}
+
+int64_t cs_measurement_count(const cs_encoder* e, int n_seq, int T) {
+    if (!e || n_seq < 0 || T < 0) return -1;
+    return (int64_t)n_seq * cs_frames_per_stream(T, e->geo.G) * e->geo.nblk * e->geo.M;
+}
+
+double cs_compression_ratio(const cs_encoder* e, int T, double key_cr, int bits) {
+    if (!e || T < 0 || !(key_cr > 0) || bits < 1) return -1.0;
+    return cr_formula(e->geo, T, key_cr, bits);
+}
+
+int cs_encode_batch_gops(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g1, float* out,
+                         cs_stream_t stream) {
+    if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
+    if (n_seq < 0 || T < 0) return fail(CS_ERR_ARG, "n_seq and T must be >= 0");
+    const int n_gops = cdiv(T, e->geo.G);
+    if (g0 < 0 || g1 > n_gops || g0 > g1) return fail(CS_ERR_ARG, "GOP range out of bounds");
+    if (n_seq == 0 || T == 0 || g0 == g1 || cs_frames_in_gops(T, e->geo.G, g0, g1) == 0) return CS_OK;
+    if (!frames || !out) return fail(CS_ERR_ARG, "NULL buffer");
+    if (!aligned16(frames) || !aligned16(out)) return fail(CS_ERR_ARG, "buffers must be 16-byte aligned");
+    if ((long long)n_seq * T > 0x7FFFFFFFLL) return fail(CS_ERR_UNSUPPORTED, "too many frames");
+    return launch(e, frames, n_seq, T, g0, g1, out, (cudaStream_t)stream);
+}
+
+int cs_encode_batch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, float* out, cs_stream_t stream) {
+    if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
+    if (T < 0) return fail(CS_ERR_ARG, "T must be >= 0");
+    return cs_encode_batch_gops(e, frames, n_seq, T, 0, cdiv(T, e->geo.G), out, stream);
+}
+
+int cs_encode_gop(cs_encoder* e, const uint8_t* frames, int n_frames, float* out, cs_stream_t stream) {
+    if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
+    if (n_frames < 1 || n_frames > e->geo.G) return fail(CS_ERR_ARG, "n_frames must be in [1, gop]");
+    return cs_encode_batch_gops(e, frames, 1, n_frames, 0, 1, out, stream);
+}
+
+int cs_encode_batch_host(cs_encoder* e, const uint8_t* frames_host, int n_seq, int T, float* out_host) {
+    if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
+    if (n_seq < 0 || T < 0) return fail(CS_ERR_ARG, "n_seq and T must be >= 0");
+    const Geometry& g = e->geo;
+    const long long cs_s = cs_frames_per_stream(T, g.G);
+    if (n_seq == 0 || T == 0 || cs_s == 0) return CS_OK;
+    if (!frames_host || !out_host) return fail(CS_ERR_ARG, "NULL buffer");
+    const size_t frame_bytes = (size_t)g.W * g.H;
+    const size_t in_bytes = (size_t)n_seq * T * frame_bytes;
+    const size_t cs_meas = (size_t)g.nblk * g.M;  // floats per CS frame
+    const size_t out_bytes = (size_t)n_seq * cs_s * cs_meas * sizeof(float);
+    std::lock_guard<std::mutex> lk(e->ws_mu);  // the workspace is per encoder
+    cudaError_t err;
+    if (e->ws_frames_bytes < in_bytes) {
+        if (e->ws_frames) cudaFree(e->ws_frames);
+        e->ws_frames = nullptr;
+        e->ws_frames_bytes = 0;
+        if ((err = cudaMalloc(&e->ws_frames, in_bytes)) != cudaSuccess)
+            return fail(CS_ERR_OOM, std::string("workspace: ") + cudaGetErrorString(err));
+        e->ws_frames_bytes = in_bytes;
+    }
+    if (e->ws_out_bytes < out_bytes) {
+        if (e->ws_out) cudaFree(e->ws_out);
+        e->ws_out = nullptr;
+        e->ws_out_bytes = 0;
+        if ((err = cudaMalloc(&e->ws_out, out_bytes)) != cudaSuccess)
+            return fail(CS_ERR_OOM, std::string("workspace: ") + cudaGetErrorString(err));
+        e->ws_out_bytes = out_bytes;
+    }
+    for (auto& s : e->hs)
+        if (!s && (err = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(err, "cudaStreamCreate");
+    // Groups: chunks of streams (n_seq > 1) or of GOPs (n_seq == 1).  Copy-in of group i+1
+    // overlaps the encode of group i and the copy-out of group i-1.
+    struct Grp {
+        int s0, s1, g0, g1;
+    };
+    std::vector<Grp> groups;
+    const int n_gops = cdiv(T, g.G);
+    if (n_seq > 1) {
+        const int per = std::max(1, n_seq / 8);
+        for (int s = 0; s < n_seq; s += per) groups.push_back({s, std::min(n_seq, s + per), 0, n_gops});
+    } else {
+        const int per = std::max(1, n_gops / 8);
+        for (int gg = 0; gg < n_gops; gg += per) groups.push_back({0, 1, gg, std::min(n_gops, gg + per)});
+    }
+    while (e->hev.size() < 2 * groups.size()) {
+        cudaEvent_t ev;
+        if ((err = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
+            return cuda_fail(err, "cudaEventCreate");
+        e->hev.push_back(ev);
+    }
+    cudaStream_t s_in = e->hs[0], s_run = e->hs[1], s_out = e->hs[2];
+    int rc = CS_OK;
+    for (size_t i = 0; i < groups.size() && rc == CS_OK; ++i) {
+        const Grp& gr = groups[i];
+        size_t f0, f1;  // frame range (global, [s][t] order) of this group
+        if (n_seq > 1) {
+            f0 = (size_t)gr.s0 * T;
+            f1 = (size_t)gr.s1 * T;
+        } else {
+            f0 = (size_t)gr.g0 * g.G;
+            f1 = std::min((size_t)gr.g1 * g.G, (size_t)T);
+        }
+        err = cudaMemcpyAsync(e->ws_frames + f0 * frame_bytes, frames_host + f0 * frame_bytes,
+                              (f1 - f0) * frame_bytes, cudaMemcpyHostToDevice, s_in);
+        if (err != cudaSuccess) {
+            rc = cuda_fail(err, "H2D");
+            break;
+        }
+        cudaEventRecord(e->hev[2 * i], s_in);
+        cudaStreamWaitEvent(s_run, e->hev[2 * i], 0);
+        size_t o0, o1;  // output float range
+        if (n_seq > 1) {
+            o0 = (size_t)gr.s0 * cs_s * cs_meas;
+            o1 = (size_t)gr.s1 * cs_s * cs_meas;
+            rc = cs_encode_batch(e, e->ws_frames + f0 * frame_bytes, gr.s1 - gr.s0, T, e->ws_out + o0, s_run);
+        } else {
+            o0 = (size_t)cs_frames_in_gops(T, g.G, 0, gr.g0) * cs_meas;
+            o1 = (size_t)cs_frames_in_gops(T, g.G, 0, gr.g1) * cs_meas;
+            rc = cs_encode_batch_gops(e, e->ws_frames, 1, T, gr.g0, gr.g1, e->ws_out + o0, s_run);
+        }
+        if (rc != CS_OK) break;
+        cudaEventRecord(e->hev[2 * i + 1], s_run);
+        cudaStreamWaitEvent(s_out, e->hev[2 * i + 1], 0);
+        if (o1 > o0) {
+            err = cudaMemcpyAsync(out_host + o0, e->ws_out + o0, (o1 - o0) * sizeof(float), cudaMemcpyDeviceToHost,
+                                  s_out);
+            if (err != cudaSuccess) {
+                rc = cuda_fail(err, "D2H");
+                break;
+            }
+        }
+    }
+    cudaError_t e1 = cudaStreamSynchronize(s_in), e2 = cudaStreamSynchronize(s_run), e3 = cudaStreamSynchronize(s_out);
+    if (rc != CS_OK) return rc;
+    if (e1 != cudaSuccess) return cuda_fail(e1, "sync");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "encode");
+    if (e3 != cudaSuccess) return cuda_fail(e3, "sync");
+    return CS_OK;
+}
+
+}  // extern "C"
