@@ -64,10 +64,12 @@ typedef struct cs_plan_info {
     int chunk_rows;        /* pixel rows of a block per K-chunk (K-chunk = chunk_rows*B) */
     int stages;            /* shared-memory ring depth */
     int key_resident;      /* 1: key tile kept in SMEM per work unit; 0: streamed per chunk */
-    int box_w;             /* TMA box width (pixels) */
+    int box_w;             /* bytes per strip row (= W: strips are full-width frame rows) */
     int smem_bytes;        /* dynamic shared memory per CTA */
     int tmem_cols;         /* TMEM columns used */
     int m_pad;             /* MMA N dimension (M rounded up to 16) */
+    int chains;            /* independent TMEM accumulation chains per block (summed in the epilogue) */
+    int prefetch_items;    /* items the producer prefetches into L2 ahead of the SMEM loads */
     int sms;               /* SMs of the device at create time */
 } cs_plan_info;
 
@@ -93,6 +95,16 @@ int cs_encoder_destroy(cs_encoder* enc);
 
 /* Fill *info with the tiling plan.  Host only. */
 int cs_encoder_plan(const cs_encoder* enc, cs_plan_info* info);
+
+/* Debug timeline (tracing subsystem): when cap > 0, every subsequent encode launch records, for
+ * CTA 0 only, the SM clock (clock64) of each pipeline event into trace_dev (DEVICE, caller-owned,
+ * CS_TRACE_EVENTS * cap uint64): trace_dev[event * cap + i] = i-th occurrence of the event.
+ * Events: 0 producer slot free, 1 producer TMA issued, 2 converter data landed, 3 converter A
+ * buffer free, 4 converter A written, 5 MMA A ready, 6 MMA issued+committed, 7 epilogue
+ * accumulator ready, 8 epilogue done, 9 converter tcgen05.st issued.  cap = 0 disables (default).  Not thread-safe with
+ * concurrent encodes of the same encoder. */
+#define CS_TRACE_EVENTS 10
+int cs_encoder_set_trace(cs_encoder* enc, unsigned long long* trace_dev, int cap);
 
 /* ---- encode (device buffers; asynchronous) ---------------------------------------------- */
 

@@ -33,7 +33,7 @@ class CSError(RuntimeError):
 class PlanInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int) for n in (
         "tile_block_rows", "folds", "lanes", "chunk_rows", "stages", "key_resident", "box_w", "smem_bytes",
-        "tmem_cols", "m_pad", "sms")]
+        "tmem_cols", "m_pad", "chains", "prefetch_items", "sms")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -55,6 +55,7 @@ def lib() -> ctypes.CDLL:
             "cs_encoder_create": (c_int, [c_int, c_int, c_int, c_int, c_int, vp, ctypes.POINTER(vp)]),
             "cs_encoder_destroy": (c_int, [vp]),
             "cs_encoder_plan": (c_int, [vp, ctypes.POINTER(PlanInfo)]),
+            "cs_encoder_set_trace": (c_int, [vp, vp, c_int]),
             "cs_encode_gop": (c_int, [vp, vp, c_int, vp, vp]),
             "cs_encode_batch": (c_int, [vp, vp, c_int, c_int, vp, vp]),
             "cs_encode_batch_gops": (c_int, [vp, vp, c_int, c_int, c_int, c_int, vp, vp]),
@@ -154,6 +155,14 @@ class Encoder:
 
     def __exit__(self, *a):
         self.close()
+
+    # -- tracing (debug timeline of CTA 0; see include/cs_encoder.h)
+    TRACE_EVENTS = ("p_empty", "p_issued", "c_full", "c_aempty", "c_done", "m_afull", "m_issued", "e_dfull",
+                    "e_done", "c_conv")
+
+    def set_trace(self, buf=None, cap: int = 0):
+        """buf: CUDA int64 tensor of len(TRACE_EVENTS) * cap elements (None/0 disables)."""
+        _check(lib().cs_encoder_set_trace(self._h, _ptr(buf) if buf is not None else None, cap))
 
     # -- accounting
     def plan(self) -> dict:

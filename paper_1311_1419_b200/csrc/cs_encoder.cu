@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -51,10 +52,10 @@ float half_bits_to_float(uint16_t h) {
 struct Plan {
     int T_r = 0, F = 0, L = 0, n_tiles = 0;
     int chunk_rows = 0, n_chunks = 0, chunk_k = 0;
-    int box_w = 0, n_box = 0, box_rows = 0, pieces = 0, single_piece = 0;
-    uint32_t box_bytes = 0, stage_cs_bytes = 0, stage_bytes = 0, key_bytes = 0;
-    int key_resident = 0, n_stages = 0;
-    uint32_t off_phi = 0, off_key = 0, off_stage = 0, smem_bytes = 0;
+    int pieces = 0, piece_rows = 0, single_piece = 0;
+    uint32_t piece_bytes = 0, stage_cs_bytes = 0, stage_bytes = 0, key_bytes = 0;
+    int key_resident = 0, n_stages = 0, prefetch_items = 0;
+    uint32_t off_tab = 0, off_epi = 0, off_phi = 0, off_key = 0, off_stage = 0, smem_bytes = 0;
     int a_cols = 0, d_cols = 0, tmem_cols = 0, n_abuf = 2, n_dbuf = 2;
     double score = -1.0;
 };
@@ -62,23 +63,6 @@ struct Plan {
 struct Geometry {
     int W, H, G, B, M, N, Mpad, nbx, nby, nblk;
 };
-
-int pick_box_w(const Geometry& g) {
-    // multiple of lcm(16, B), <= 256; prefer exact cover of nbx*B, then fewest boxes
-    const int unit = std::max(16, g.B);
-    const int need = g.nbx * g.B;
-    int best = unit, best_waste = 1 << 30, best_n = 1 << 30;
-    for (int bw = unit; bw <= 256; bw += unit) {
-        int n = cdiv(need, bw);
-        int waste = n * bw - need;
-        if (waste < best_waste || (waste == best_waste && n < best_n)) {
-            best = bw;
-            best_waste = waste;
-            best_n = n;
-        }
-    }
-    return best;
-}
 
 bool try_plan(const Geometry& g, int T_r, int chunk_rows, bool key_res, int smem_limit, Plan& p) {
     p = Plan();
@@ -96,56 +80,79 @@ bool try_plan(const Geometry& g, int T_r, int chunk_rows, bool key_res, int smem
     p.n_chunks = g.B / chunk_rows;
     p.chunk_k = chunk_rows * g.B;
     p.a_cols = p.F * p.chunk_k / 2;
-    p.d_cols = p.F * g.Mpad;
     p.n_abuf = 2;
-    p.n_dbuf = 2;
-    if (2 * p.a_cols + 2 * p.d_cols > (int)csenc::kTmemCols) p.n_dbuf = 1;  // large M: one accumulator
+    // Two accumulators (epilogue of frame i overlaps the MMAs of frame i+1) when TMEM allows.
+    // (Measured, tools/mma_microbench*.cu: dependent MMAs into one accumulator issue back to
+    // back, so no split-K accumulation chains are needed.)
+    p.n_dbuf = (p.n_abuf * p.a_cols + 2 * p.F * g.Mpad <= (int)csenc::kTmemCols) ? 2 : 1;
+    p.d_cols = p.F * g.Mpad;
     p.tmem_cols = p.n_abuf * p.a_cols + p.n_dbuf * p.d_cols;
     if (p.tmem_cols > (int)csenc::kTmemCols) return false;
-    p.box_w = pick_box_w(g);
-    p.n_box = cdiv(g.nbx * g.B, p.box_w);
-    if (p.n_chunks == 1 && T_r * g.B <= 256) {
+    // Stage layout: [piece][piece_rows][W] -- each piece is one contiguous strip of full-width
+    // frame rows, moved by a single bulk copy.
+    if (p.n_chunks == 1) {
         p.pieces = 1;
         p.single_piece = 1;
-        p.box_rows = T_r * g.B;
+        p.piece_rows = T_r * g.B;
     } else {
         p.pieces = T_r;
-        p.box_rows = chunk_rows;
+        p.piece_rows = chunk_rows;
     }
-    if (p.box_rows > 256) return false;
-    p.box_bytes = align_up((uint32_t)(p.box_rows * p.box_w), 128);
-    p.stage_cs_bytes = (uint32_t)(p.pieces * p.n_box) * p.box_bytes;
+    p.piece_bytes = align_up((uint32_t)(p.piece_rows * g.W), 128);
+    p.stage_cs_bytes = (uint32_t)p.pieces * p.piece_bytes;
     p.key_resident = key_res ? 1 : 0;
     p.key_bytes = key_res ? (uint32_t)p.n_chunks * p.stage_cs_bytes : 0;
     p.stage_bytes = key_res ? p.stage_cs_bytes : 2 * p.stage_cs_bytes;
     const uint32_t phi_bytes = (uint32_t)g.Mpad * (uint32_t)g.N * 2u;
-    p.off_phi = 1024;  // barriers live in the first KB
+    p.off_tab = 1024;  // barriers live in the first KB, then the converter offset table (8 KB)
+    p.off_epi = 1024 + 8192;  // epilogue staging tiles (4 warps x 4 KB)
+    p.off_phi = 1024 + 8192 + 16384;
     p.off_key = align_up(p.off_phi + phi_bytes, 1024);
     p.off_stage = align_up(p.off_key + 2 * p.key_bytes, 1024);
     const long avail = (long)smem_limit - 1024 /*alignment slack*/ - (long)p.off_stage;
     if (avail < (long)p.stage_bytes * 2) return false;
     p.n_stages = (int)std::min<long>(csenc::kMaxStages, avail / p.stage_bytes);
     p.smem_bytes = p.off_stage + (uint32_t)p.n_stages * p.stage_bytes + 1024;
-    // score: lane utilisation x key residency x bytes in flight x per-stage overhead
+    // L2 prefetch of future strips: measured no benefit once the SMEM ring holds >= ~100 KB
+    // (tools/sweep.sh); kept as a knob (CSENC_PREFETCH), off by default.
+    p.prefetch_items = 0;
+    // Score (measured on B200, tools/sweep.sh): every item (ring slot) costs a fixed ~1k cycles
+    // of pipeline handoffs, so larger strips win until ~30 KB; >= 3 slots are enough once the
+    // producer is warp-uniform; a resident key beats re-streaming it by ~25%.
     const double util = (double)tile_blocks / (p.F * 128.0);
+    double s = util * (key_res ? 1.0 : 0.75);
+    s *= std::pow(std::min(1.0, p.stage_cs_bytes / 30720.0), 0.7);
+    if (p.n_stages < 3) s *= 0.9;
     const double inflight = (double)(p.n_stages - 1) * p.stage_cs_bytes;
-    double s = util * (key_res ? 1.0 : 0.8) * std::min(1.0, inflight / 98304.0);
-    s *= std::min(1.0, p.stage_cs_bytes / 12288.0);
-    if (p.n_stages < 3) s *= 0.7;
+    s *= std::min(1.0, inflight / 61440.0);
     if (p.n_dbuf < 2) s *= 0.8;
-    s *= 1.0 + 1e-3 * chunk_rows;  // tie-break: fewer, larger pipeline handoffs
     p.score = s;
     return true;
 }
 
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+}
+
 bool make_plan(const Geometry& g, int smem_limit, Plan& best) {
     best = Plan();
+    // experiment knobs (tools/sweep.sh): force a tile-row count / chunk size / key residency
+    const int f_tr = env_int("CSENC_TILE_ROWS", 0), f_cr = env_int("CSENC_CHUNK_ROWS", 0);
+    const int f_kr = env_int("CSENC_KEY_RESIDENT", -1), f_st = env_int("CSENC_STAGES", 0);
     for (int T_r = 1; T_r <= g.nby; ++T_r) {
         if (T_r * g.nbx > 128 * csenc::kMaxFolds) break;
+        if (f_tr && T_r != f_tr) continue;
         for (int cr = g.B; cr >= 1; --cr) {
+            if (f_cr && cr != f_cr) continue;
             for (int kr = 1; kr >= 0; --kr) {
+                if (f_kr >= 0 && kr != f_kr) continue;
                 Plan p;
                 if (!try_plan(g, T_r, cr, kr == 1, smem_limit, p)) continue;
+                if (f_st > 0 && f_st < p.n_stages) {
+                    p.smem_bytes -= (uint32_t)(p.n_stages - f_st) * p.stage_bytes;
+                    p.n_stages = f_st;
+                }
                 if (p.score > best.score + 1e-9) best = p;
             }
         }
@@ -178,30 +185,12 @@ WorkSplit choose_split(const Geometry& g, const Plan& p, int n_seq, int n_gops_s
     return best;
 }
 
-// ------------------------------------------------------------------------- driver entry point
-typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-PFN_encodeTiled get_encode_tiled() {
-    static PFN_encodeTiled fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void* ptr = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_encodeTiled>(ptr);
-    });
-    return fn;
-}
-
 int validate(int W, int H, int gop, int B, int M, const uint16_t* phi) {
     if (W < 1 || H < 1 || gop < 1 || M < 1) return fail(CS_ERR_ARG, "W, H, gop and M must be >= 1");
     if (B != 8 && B != 16 && B != 32) return fail(CS_ERR_UNSUPPORTED, "B must be 8, 16 or 32");
     if (M > B * B) return fail(CS_ERR_ARG, "M must be <= N = B*B");
     if (M > 256) return fail(CS_ERR_UNSUPPORTED, "M must be <= 256 (UMMA N limit)");
-    if (W % 16 != 0) return fail(CS_ERR_UNSUPPORTED, "W must be a multiple of 16 (TMA row pitch)");
+    if (W % 16 != 0) return fail(CS_ERR_UNSUPPORTED, "W must be a multiple of 16 (16-byte aligned bulk-copy rows)");
     {
         const long mpad = std::max(16, (M + 15) / 16 * 16);
         if (mpad * B * B * 2 > kMaxPhiBytes)
@@ -262,61 +251,31 @@ struct cs_encoder {
     void* phi_dev = nullptr;
     uint32_t phi_bytes = 0;
     uint32_t idesc = 0, lbo = 0, sbo = 0;
-    std::mutex mu;     // tensor-map cache
     std::mutex ws_mu;  // host-path workspace
-    struct MapEntry {
-        const void* ptr;
-        long long n_frames;
-        CUtensorMap map;
-    };
-    std::vector<MapEntry> maps;  // small LRU of tensor maps
     // host-path workspace
     uint8_t* ws_frames = nullptr;
     float* ws_out = nullptr;
     size_t ws_frames_bytes = 0, ws_out_bytes = 0;
     cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
+    int prefetch_override = -1;  // tuning knob (CSENC_PREFETCH env at create), -1 = planner's
+    unsigned long long* trace = nullptr;  // device buffer (debug timeline), caller-owned
+    int trace_cap = 0;
     std::vector<cudaEvent_t> hev;
 };
 
 namespace {
-
-int get_tmap(cs_encoder* e, const uint8_t* frames, long long n_frames, CUtensorMap* out) {
-    std::lock_guard<std::mutex> lk(e->mu);
-    for (auto& m : e->maps)
-        if (m.ptr == frames && m.n_frames == n_frames) {
-            *out = m.map;
-            return CS_OK;
-        }
-    PFN_encodeTiled enc = get_encode_tiled();
-    if (!enc) return fail(CS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    const Geometry& g = e->geo;
-    const Plan& p = e->plan;
-    CUtensorMap map;
-    cuuint64_t dims[3] = {(cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)n_frames};
-    cuuint64_t strides[2] = {(cuuint64_t)g.W, (cuuint64_t)g.W * (cuuint64_t)g.H};
-    cuuint32_t box[3] = {(cuuint32_t)p.box_w, (cuuint32_t)p.box_rows, 1};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(frames), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(CS_ERR_CUDA, "cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
-    if (e->maps.size() >= 16) e->maps.erase(e->maps.begin());
-    e->maps.push_back({frames, n_frames, map});
-    *out = map;
-    return CS_OK;
-}
 
 int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g1, float* out, cudaStream_t stream) {
     const Geometry& g = e->geo;
     const Plan& pl = e->plan;
     if (g1 <= g0 || g.G == 1) return CS_OK;
     if (cs_frames_in_gops(T, g.G, g0, g1) == 0) return CS_OK;
-    CUtensorMap map;
-    int rc = get_tmap(e, frames, (long long)n_seq * T, &map);
-    if (rc != CS_OK) return rc;
     KParams kp;
     std::memset(&kp, 0, sizeof(kp));
+    kp.frames = frames;
     kp.out = out;
+    kp.W = g.W;
+    kp.H = g.H;
     kp.phi = (const uint16_t*)e->phi_dev;
     kp.phi_bytes = e->phi_bytes;
     kp.M = g.M;
@@ -332,12 +291,11 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.chunk_rows = pl.chunk_rows;
     kp.n_chunks = pl.n_chunks;
     kp.chunk_k = pl.chunk_k;
-    kp.box_w = pl.box_w;
-    kp.n_box = pl.n_box;
-    kp.box_rows = pl.box_rows;
     kp.pieces = pl.pieces;
+    kp.piece_rows = pl.piece_rows;
     kp.single_piece = pl.single_piece;
-    kp.box_bytes = pl.box_bytes;
+    kp.piece_bytes = pl.piece_bytes;
+    kp.prefetch_items = e->prefetch_override >= 0 ? e->prefetch_override : pl.prefetch_items;
     kp.stage_cs_bytes = pl.stage_cs_bytes;
     kp.stage_bytes = pl.stage_bytes;
     kp.key_bytes = pl.key_bytes;
@@ -362,17 +320,22 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.d_cols = pl.d_cols;
     kp.n_abuf = pl.n_abuf;
     kp.n_dbuf = pl.n_dbuf;
+    kp.off_tab = pl.off_tab;
+    kp.off_epi = pl.off_epi;
+    kp.dbg_load_only = env_int("CSENC_DBG_LOAD_ONLY", 0);
+    kp.trace = e->trace;
+    kp.trace_cap = e->trace_cap;
     const int grid = std::max(1, std::min(e->sms, kp.n_units));
     cudaError_t err;
     switch (g.B) {
         case 8:
-            csenc::cs_measure_kernel<8><<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(map, kp);
+            csenc::cs_measure_kernel<8><<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(kp);
             break;
         case 16:
-            csenc::cs_measure_kernel<16><<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(map, kp);
+            csenc::cs_measure_kernel<16><<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(kp);
             break;
         default:
-            csenc::cs_measure_kernel<32><<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(map, kp);
+            csenc::cs_measure_kernel<32><<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(kp);
             break;
     }
     err = cudaGetLastError();
@@ -438,14 +401,17 @@ int cs_encoder_create(int W, int H, int gop, int B, int M, const uint16_t* phi_f
     }
     cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, e->device);
     cudaDeviceGetAttribute(&e->smem_limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device);
+    if (const char* pf = std::getenv("CSENC_PREFETCH")) e->prefetch_override = std::atoi(pf);
     if (!make_plan(e->geo, e->smem_limit, e->plan)) {
         delete e;
         return fail(CS_ERR_UNSUPPORTED, "no tiling fits shared memory / TMEM for this configuration");
     }
+    // The attribute is per kernel (not per encoder): set the device maximum so encoders with
+    // different plans can coexist.
     switch (B) {
-        case 8: err = set_smem_attr<8>((int)e->plan.smem_bytes); break;
-        case 16: err = set_smem_attr<16>((int)e->plan.smem_bytes); break;
-        default: err = set_smem_attr<32>((int)e->plan.smem_bytes); break;
+        case 8: err = set_smem_attr<8>(e->smem_limit); break;
+        case 16: err = set_smem_attr<16>(e->smem_limit); break;
+        default: err = set_smem_attr<32>(e->smem_limit); break;
     }
     if (err != cudaSuccess) {
         delete e;
@@ -500,10 +466,12 @@ static void fill_info(const Plan& p, const Geometry& g, int sms, cs_plan_info* i
     info->chunk_rows = p.chunk_rows;
     info->stages = p.n_stages;
     info->key_resident = p.key_resident;
-    info->box_w = p.box_w;
+    info->box_w = g.W;  /* strips are full-width rows */
+    info->prefetch_items = p.prefetch_items;
     info->smem_bytes = (int)p.smem_bytes;
     info->tmem_cols = p.tmem_cols;
     info->m_pad = g.Mpad;
+    info->chains = 1;
     info->sms = sms;
 }
 
@@ -515,6 +483,13 @@ int cs_plan_cfg(int W, int H, int gop, int B, int M, int smem_limit, int sms, cs
     Plan p;
     if (!make_plan(g, smem_limit, p)) return fail(CS_ERR_UNSUPPORTED, "no tiling fits shared memory / TMEM");
     fill_info(p, g, sms, info);
+    return CS_OK;
+}
+
+int cs_encoder_set_trace(cs_encoder* e, unsigned long long* trace_dev, int cap) {
+    if (!e || cap < 0 || (cap > 0 && !trace_dev)) return fail(CS_ERR_ARG, "bad trace buffer");
+    e->trace = cap > 0 ? trace_dev : nullptr;
+    e->trace_cap = cap;
     return CS_OK;
 }
 

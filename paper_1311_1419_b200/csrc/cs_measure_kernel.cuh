@@ -1,61 +1,98 @@
 // cs_measure_kernel.cuh -- K1: fused GOP residual formation + block CS measurement on sm_100a.
 //
-// One persistent, warp-specialised kernel per encode call.  Per work unit
-// (stream s, GOP g, tile t of full-width block rows, range of CS frames of the GOP):
+// One persistent, warp-specialised kernel per encode call.  Work unit =
+// (stream s, GOP g, tile t of full-width block rows, range of CS frames of the GOP).  Item =
+// one K-chunk (chunk_rows pixel rows of every block) of one CS frame of the unit's tile.
 //
-//   warp 0        TMA producer: Phi -> SMEM once; the key tile (double buffered) and the CS
-//                 tiles (ring of n_stages) with 3-D tiled tensor-map loads [frame][y][x] whose
-//                 out-of-bounds rows/columns are zero-filled (partial blocks, reading R10).
-//   warps 4..7    converters ("im2col + residual", a2+a3): thread = TMEM lane = block of the
-//                 tile.  Reads its B x B block of the CS frame and of the key frame from SMEM,
-//                 forms the exact residual r = F - F_key as fp16 (magic-number trick) and
+//   warp 12       TMA producer: Phi -> SMEM once (bulk copy).  Per item the tile strip of the
+//                 CS frame -- contiguous in HBM, rows [y0, y0+rows) x all W columns -- arrives
+//                 in ONE cp.async.bulk per piece into a ring slot; the key strip of the unit is
+//                 kept in a double-buffered SMEM region (or streamed with every item when it does
+//                 not fit).  Strips `prefetch_items` ahead are pulled into L2 with
+//                 cp.async.bulk.prefetch.L2, so HBM latency is covered by L2, not by SMEM depth.
+//   warps 0..7    converters (a2 im2col + a3 residual), two warpgroups splitting each item's row
+//                 groups; thread = TMEM lane = block of the tile.  Reads its block's row segments
+//                 of the CS and key strips from SMEM, forms r = F - F_key exactly in fp16 (magic
+//                 number 0x64XX = 1024 + XX), zero for rows >= H / columns >= W (reading R10), and
 //                 writes it with tcgen05.st as the MMA A operand in TMEM (row = block, K = the
 //                 row-major pixel index j = yy*B + xx, two fp16 per 32-bit column).
-//   warp 1        MMA issuer (a4): D[tmem, fp32] = A[tmem, fp16] x Phi^T[smem, fp16], one
-//                 tcgen05.mma.kind::f16 (M=128 lanes, N=Mpad, K=16) per 16 pixels, chained
-//                 over the block; commit -> mbarriers.
-//   warps 8..11   epilogue (a6): tcgen05.ld of the fp32 accumulators, vectorised stores of
-//                 y[s][g][c][by][bx][0..M) (block-major, M*4 contiguous bytes per block).
-//   warp 2        TMEM allocator.
+//   warp 13       MMA issuer (a4) + TMEM allocator: D[tmem, fp32] += A[tmem, fp16] x
+//                 Phi^T[smem, fp16], one tcgen05.mma.kind::f16 (M=128 lanes, N=Mpad, K=16) per
+//                 16 pixels; commit -> mbarriers.  Warp-uniform loop, one elected issuing lane.
+//   warps 8..11   epilogue (a6): tcgen05.ld of the fp32 accumulators -> (swizzled SMEM tile) ->
+//                 row-contiguous vector stores of y[s][g][c][by][bx][0..M) (block-major).
+//
+// The warp scheduler arbitrates highest-warp-id first, so the single-thread roles (MMA issue,
+// TMA issue) have the highest ids and are never starved by the converter warps.
 //
 // Pipelines (mbarrier phase/parity rings): stage_full/empty (TMA <-> converters), key_full/
 // empty (double-buffered key tile), a_full/empty (converters <-> MMA, 2 TMEM A buffers),
-// d_full/empty (MMA <-> epilogue, 2 TMEM accumulators).  Paper passages: Eq.(1) P:83-85,
+// d_full/empty (MMA <-> epilogue, 1-2 TMEM accumulators).  Paper passages: Eq.(1) P:83-85,
 // P:87 and Eq.(2)-(3) P:89-91 (see include/cs_encoder.h).
 #pragma once
-#include <cuda.h>
 #include <cstdint>
 
 #include "ptx_sm100.cuh"
 
 namespace csenc {
 
-constexpr int kThreads = 384;
+constexpr int kConvWarps = 8;                    // warps 0..7: two converter warpgroups
+constexpr int kEpiWarp0 = 8;                     // warps 8..11: epilogue warpgroup
+constexpr int kProducerWarp = 12;                // TMA producer
+constexpr int kMmaWarp = 13;                     // MMA issuer + TMEM allocator
+constexpr int kThreads = 14 * 32;
 constexpr int kMaxFolds = 8;
 constexpr int kMaxStages = 8;
 constexpr uint32_t kTmemCols = 512;
 
 struct KParams {
+    const uint8_t* frames;    // device [n_seq][T][H][W]
     float* out;
     const uint16_t* phi;      // device, canonical UMMA layout, phi_bytes
     uint32_t phi_bytes;
-    int M, Mpad, N;
+    int W, H, M, Mpad, N;
     int nbx, nby, nblk;
     // tiling
     int T_r, F, L, n_tiles;
     int chunk_rows, n_chunks, chunk_k;
-    int box_w, n_box, box_rows, pieces;
-    int single_piece;         // 1: one box row-range covers all T_r*B rows of the tile (n_chunks == 1)
-    uint32_t box_bytes, stage_cs_bytes, stage_bytes, key_bytes;
-    int key_resident, n_stages;
-    uint32_t off_phi, off_key, off_stage;
+    int pieces;               // strips per stage: 1 (all T_r*B rows, n_chunks == 1) or T_r
+    int piece_rows;           // rows per strip
+    int single_piece;
+    uint32_t piece_bytes, stage_cs_bytes, stage_bytes, key_bytes;
+    int key_resident, n_stages, prefetch_items;
+    uint32_t off_tab, off_epi, off_phi, off_key, off_stage;
     // work
     int G, T, gop_begin, n_gops_sel, cs_per_stream_sel, n_splits, cs_per_unit, n_units;
     // MMA
     uint32_t idesc, lbo, sbo;
     int a_cols, d_cols;
-    int n_abuf, n_dbuf;       // TMEM ring depths (1 or 2)
+    int n_abuf, n_dbuf;
+    // optional timeline trace (CTA 0 only): trace[event * trace_cap + i] = clock64 of the i-th
+    // occurrence of the event; nullptr disables (the default)
+    unsigned long long* trace;
+    int trace_cap;
+    int dbg_load_only;        // debug: converters release stages without converting; no MMA/epilogue
 };
+
+// trace events
+enum : int {
+    EV_P_EMPTY = 0,   // producer: stage slot free
+    EV_P_ISSUED,      // producer: stage copies issued
+    EV_C_FULL,        // converter: stage data landed
+    EV_C_AEMPTY,      // converter: A buffer free
+    EV_C_DONE,        // converter: A written (before a_full arrive)
+    EV_M_AFULL,       // MMA: A ready
+    EV_M_ISSUED,      // MMA: chunk MMAs issued + committed
+    EV_E_DFULL,       // epilogue: accumulator ready
+    EV_E_DONE,        // epilogue: stores issued, D released
+    EV_C_CONV,        // converter: all tcgen05.st issued (before wait::st)
+    EV_COUNT
+};
+
+__device__ __forceinline__ void trace_ev(const KParams& p, int ev, int i) {
+    if (p.trace != nullptr && blockIdx.x == 0 && i < p.trace_cap)
+        p.trace[(size_t)ev * p.trace_cap + i] = clock64();
+}
 
 struct Unit {
     int s, g, t, c0, c1;
@@ -76,26 +113,83 @@ __device__ __forceinline__ bool decode_unit(const KParams& p, int u, Unit& w) {
     return w.c1 > w.c0;
 }
 
-// Issue the TMA boxes of one K-chunk of one tile of frame z into dst (layout [piece][box][rows][box_w]).
-__device__ __forceinline__ void load_tile_chunk(const KParams& p, const CUtensorMap* tmap, uint32_t dst, int z,
-                                                int t, int k, uint32_t bar, uint64_t policy) {
-    const int B_rows_tile = p.T_r * (p.chunk_k / p.chunk_rows);  // T_r * B
-    for (int pc = 0; pc < p.pieces; ++pc) {
-        int y = p.single_piece ? t * B_rows_tile : (t * p.T_r + pc) * (p.chunk_k / p.chunk_rows) + k * p.chunk_rows;
-        for (int b = 0; b < p.n_box; ++b) {
-            ptx::tma_load_3d(dst + (uint32_t)(pc * p.n_box + b) * p.box_bytes, tmap, bar, b * p.box_w, y, z, policy);
+// Iterator over this CTA's items (unit, CS frame, K-chunk) in schedule order.
+struct ItemIter {
+    int u, c, k;
+    Unit w;
+    bool ok;
+    __device__ __forceinline__ void skip_empty(const KParams& p) {
+        while (u < p.n_units && !decode_unit(p, u, w)) u += gridDim.x;
+        ok = u < p.n_units;
+        if (ok) {
+            c = w.c0;
+            k = 0;
         }
+    }
+    __device__ __forceinline__ void first(const KParams& p) {
+        u = blockIdx.x;
+        skip_empty(p);
+    }
+    __device__ __forceinline__ void next(const KParams& p) {
+        if (++k < p.n_chunks) return;
+        k = 0;
+        if (++c < w.c1) return;
+        u += gridDim.x;
+        skip_empty(p);
+    }
+};
+
+__device__ __forceinline__ int key_frame(const KParams& p, const Unit& w) { return w.s * p.T + w.g * p.G; }
+
+// First global row and row count of strip `pc` of K-chunk k of tile t (rows >= H are not copied).
+template <int B>
+__device__ __forceinline__ void strip_rows(const KParams& p, int t, int k, int pc, int& y0, int& rows) {
+    y0 = p.single_piece ? t * p.T_r * B : (t * p.T_r + pc) * B + k * p.chunk_rows;
+    rows = max(0, min(p.piece_rows, p.H - y0));
+}
+
+// Bytes a (tile, chunk) strip set delivers (the mbarrier transaction count).
+template <int B>
+__device__ __forceinline__ uint32_t strip_bytes(const KParams& p, int t, int k) {
+    uint32_t b = 0;
+    for (int pc = 0; pc < p.pieces; ++pc) {
+        int y0, rows;
+        strip_rows<B>(p, t, k, pc, y0, rows);
+        b += (uint32_t)rows * (uint32_t)p.W;
+    }
+    return b;
+}
+
+template <int B>
+__device__ __forceinline__ void load_strips(const KParams& p, uint32_t dst, const uint8_t* frame, int t, int k,
+                                            uint32_t bar, uint64_t policy) {
+    for (int pc = 0; pc < p.pieces; ++pc) {
+        int y0, rows;
+        strip_rows<B>(p, t, k, pc, y0, rows);
+        if (rows > 0)
+            ptx::bulk_load_hint(dst + (uint32_t)pc * p.piece_bytes, frame + (size_t)y0 * p.W, (uint32_t)rows * p.W,
+                                bar, policy);
     }
 }
 
-// Converter: one block-row segment of B pixels -> B/2 fp16x2 residual words.
+template <int B>
+__device__ __forceinline__ void prefetch_strips(const KParams& p, const uint8_t* frame, int t, int k) {
+    for (int pc = 0; pc < p.pieces; ++pc) {
+        int y0, rows;
+        strip_rows<B>(p, t, k, pc, y0, rows);
+        if (rows > 0) ptx::prefetch_l2(frame + (size_t)y0 * p.W, (uint32_t)rows * p.W);
+    }
+}
+
+// Converter: one block row segment of B pixels -> B/2 fp16x2 residual words.  `half2` (B=32 only)
+// is false when the block's right 16 columns lie beyond W (they are then zero in both frames).
 template <int B>
 struct RowConv;
 
 template <>
 struct RowConv<8> {
     static constexpr int kWords = 4;
-    __device__ __forceinline__ static void run(uint32_t cs, uint32_t key, uint32_t* w) {
+    __device__ __forceinline__ static void run(uint32_t cs, uint32_t key, uint32_t* w, bool) {
         uint2 c = ptx::lds64(cs), k = ptx::lds64(key);
         ptx::residual4(c.x, k.x, w[0], w[1]);
         ptx::residual4(c.y, k.y, w[2], w[3]);
@@ -104,7 +198,7 @@ struct RowConv<8> {
 template <>
 struct RowConv<16> {
     static constexpr int kWords = 8;
-    __device__ __forceinline__ static void run(uint32_t cs, uint32_t key, uint32_t* w) {
+    __device__ __forceinline__ static void run(uint32_t cs, uint32_t key, uint32_t* w, bool) {
         uint4 c = ptx::lds128(cs), k = ptx::lds128(key);
         ptx::residual4(c.x, k.x, w[0], w[1]);
         ptx::residual4(c.y, k.y, w[2], w[3]);
@@ -115,15 +209,64 @@ struct RowConv<16> {
 template <>
 struct RowConv<32> {
     static constexpr int kWords = 16;
-    __device__ __forceinline__ static void run(uint32_t cs, uint32_t key, uint32_t* w) {
-        RowConv<16>::run(cs, key, w);
-        RowConv<16>::run(cs + 16, key + 16, w + 8);
+    __device__ __forceinline__ static void run(uint32_t cs, uint32_t key, uint32_t* w, bool half2) {
+        RowConv<16>::run(cs, key, w, true);
+        if (half2) {
+            RowConv<16>::run(cs + 16, key + 16, w + 8, true);
+        } else {
+#pragma unroll
+            for (int i = 8; i < 16; ++i) w[i] = 0u;
+        }
     }
 };
 
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P1;\n\telect.sync _|P1, 0xffffffff;\n\tselp.b32 %0, 1, 0, P1;\n\t}"
+                 : "=r"(pred));
+    return pred != 0;
+}
+
+// KS MMAs of one fold of one K-chunk, straight-line: A advances 8 TMEM columns (16 fp16) per
+// K step, Phi's descriptor advances 2 core matrices.  Called by one elected thread.
+template <int KS>
+__device__ __forceinline__ void issue_chunk(uint32_t d, uint32_t a, uint64_t bdesc, uint64_t bstep, uint32_t idesc,
+                                            uint32_t acc0) {
+#pragma unroll
+    for (int s = 0; s < KS; ++s)
+        ptx::mma_f16_ts(d, a + (uint32_t)(s * 8), bdesc + (uint64_t)s * bstep, idesc, s == 0 ? acc0 : 1u);
+}
+
+// Epilogue helper: a warp's 32 accumulator rows x CW columns (CW = 16 or 32) -> global, through a
+// 4 KB XOR-swizzled SMEM tile so every st.global.v4 writes whole 64/128-byte row segments.
+// v = this lane's CW values (its row); rows r < rows_valid are stored at dst_row0 + r*M + col.
+template <int CW>
+__device__ __forceinline__ void stage_store(const uint32_t* v, uint32_t tile, uint32_t lane, float* dst_row0, int M,
+                                            int j0, int rows_valid) {
+    constexpr int CPR = CW / 4;           // 16-byte chunks per row
+    constexpr uint32_t PITCH = CW * 4;    // staged row pitch
+    constexpr int RPI = 32 / CPR;         // rows per store instruction
+#pragma unroll
+    for (int q = 0; q < CPR; ++q) {
+        const int slot = (CPR == 8) ? (q ^ (int)(lane & 7u)) : (q ^ (int)((lane >> 1) & 3u));
+        ptx::sts128(tile + lane * PITCH + (uint32_t)slot * 16u, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+    __syncwarp();
+    const int cc = (int)(lane % CPR);
+    const int col = j0 + cc * 4;
+    const int rsub = (int)(lane / CPR);
+#pragma unroll
+    for (int it = 0; it < CPR; ++it) {
+        const int r = it * RPI + rsub;
+        const int slot = (CPR == 8) ? (cc ^ (r & 7)) : (cc ^ ((r >> 1) & 3));
+        uint4 t = ptx::lds128(tile + (uint32_t)r * PITCH + (uint32_t)slot * 16u);
+        if (r < rows_valid && col < M) ptx::stg128(dst_row0 + (long long)r * M + col, t.x, t.y, t.z, t.w);
+    }
+    __syncwarp();
+}
+
 template <int B>
-__global__ void __launch_bounds__(kThreads, 1)
-    cs_measure_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ KParams p) {
+__global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_constant__ KParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t sbase = (ptx::smem_addr(smem_raw) + 1023u) & ~1023u;
     const int warp = threadIdx.x >> 5;
@@ -148,12 +291,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         for (int i = 0; i < p.n_stages; ++i) {
             ptx::mbar_init(bar_stage_full + 8 * i, 1);
-            ptx::mbar_init(bar_stage_empty + 8 * i, 4);
+            ptx::mbar_init(bar_stage_empty + 8 * i, kConvWarps);
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(bar_key_full + 8 * i, 1);
-            ptx::mbar_init(bar_key_empty + 8 * i, 4);
-            ptx::mbar_init(bar_a_full + 8 * i, 4);
+            ptx::mbar_init(bar_key_empty + 8 * i, kConvWarps);
+            ptx::mbar_init(bar_a_full + 8 * i, kConvWarps);
             ptx::mbar_init(bar_a_empty + 8 * i, 1);
             ptx::mbar_init(bar_d_full + 8 * i, 1);
             ptx::mbar_init(bar_d_empty + 8 * i, 4);
@@ -161,11 +304,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_init(bar_phi, 1);
         ptx::fence_mbarrier_init();
     }
-    if (warp == 2) {
+    if (warp == kMmaWarp) {
         ptx::tmem_alloc(tmem_slot, kTmemCols);
         ptx::tmem_relinquish();
     }
-    if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap);
+    if (warp < 4) {
+        // Per (fold, lane) table: byte offset of the lane's block (its row 0 in the chunk) inside
+        // a stage, and meta = row offset of the block within the tile | B=32 right-half-valid
+        // (bit 16) | lane-valid (bit 17).
+        const int lane_idx = threadIdx.x;
+        for (int f = 0; f < p.F; ++f) {
+            uint32_t off = 0, meta = 0;
+            const int b = f * p.L + lane_idx;
+            if (lane_idx < p.L && b < p.T_r * p.nbx) {
+                const int brow = b / p.nbx, bx = b - brow * p.nbx;
+                const int pc = p.single_piece ? 0 : brow;
+                const int row = p.single_piece ? brow * B : 0;
+                off = (uint32_t)pc * p.piece_bytes + (uint32_t)(row * p.W + bx * B);
+                meta = (uint32_t)(brow * B) | ((bx * B + B <= p.W) ? (1u << 16) : 0u) | (1u << 17);
+            }
+            const uint32_t e = sbase + p.off_tab + (uint32_t)(f * 128 + lane_idx) * 8u;
+            asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(e), "r"(off), "r"(meta));
+        }
+    }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -175,146 +336,232 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t a_col0 = 0;
     const uint32_t d_col0 = (uint32_t)(p.n_abuf * p.a_cols);
 
-    if (warp == 0) {
+    if (warp == kProducerWarp) {
         // ================================================================ TMA producer
-        if (lane == 0) {
-            const uint64_t pol_stream = ptx::policy_evict_first();
-            const uint64_t pol_key = ptx::policy_evict_last();
+        // Warp-uniform schedule walk (keeps addresses in uniform registers); one elected lane
+        // issues the copies.
+        const uint64_t pol_stream = ptx::policy_evict_first();
+        const uint64_t pol_key = ptx::policy_evict_last();
+        const size_t frame_bytes = (size_t)p.W * (size_t)p.H;
+        if (elect_one()) {
             ptx::mbar_arrive_expect_tx(bar_phi, p.phi_bytes);
             ptx::bulk_load(s_phi, p.phi, p.phi_bytes, bar_phi);
-            int st = 0;
-            uint32_t ph = 0;
-            int kb = 0;
-            uint32_t kph = 0;
-            for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-                Unit w;
-                if (!decode_unit(p, u, w)) continue;
-                const int zkey = w.s * p.T + w.g * p.G;
-                if (p.key_resident) {
-                    ptx::mbar_wait(bar_key_empty + 8 * kb, kph ^ 1u);
-                    ptx::mbar_arrive_expect_tx(bar_key_full + 8 * kb, p.key_bytes);
+        }
+        __syncwarp();
+        // optional L2 prefetch `prefetch_items` items ahead of the SMEM loads
+        ItemIter ahead;
+        ahead.first(p);
+        auto prefetch_one = [&]() {
+            if (!ahead.ok) return;
+            const uint8_t* kf = p.frames + (size_t)key_frame(p, ahead.w) * frame_bytes;
+            if (elect_one()) {
+                if (ahead.c == ahead.w.c0 && ahead.k == 0)  // entering a unit: its key strips
+                    for (int k = 0; k < p.n_chunks; ++k) prefetch_strips<B>(p, kf, ahead.w.t, k);
+                prefetch_strips<B>(p, kf + (size_t)(1 + ahead.c) * frame_bytes, ahead.w.t, ahead.k);
+            }
+            __syncwarp();
+            ahead.next(p);
+        };
+        for (int i = 0; i < p.prefetch_items; ++i) prefetch_one();
+        int st = 0;
+        uint32_t ph = 0;
+        int kb = 0;
+        uint32_t kph = 0;
+        int n_items = 0;
+        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+            Unit w;
+            if (!decode_unit(p, u, w)) continue;
+            const uint8_t* key_f = p.frames + (size_t)key_frame(p, w) * frame_bytes;
+            if (p.key_resident) {
+                ptx::mbar_wait(bar_key_empty + 8 * kb, kph ^ 1u);
+                uint32_t kbytes = 0;
+                for (int k = 0; k < p.n_chunks; ++k) kbytes += strip_bytes<B>(p, w.t, k);
+                if (elect_one()) {
+                    ptx::mbar_arrive_expect_tx(bar_key_full + 8 * kb, kbytes);
                     for (int k = 0; k < p.n_chunks; ++k)
-                        load_tile_chunk(p, &tmap, s_key + (uint32_t)kb * p.key_bytes + (uint32_t)k * p.stage_cs_bytes,
-                                        zkey, w.t, k, bar_key_full + 8 * kb, pol_key);
-                    kb ^= 1;
-                    if (kb == 0) kph ^= 1u;
+                        load_strips<B>(p, s_key + (uint32_t)kb * p.key_bytes + (uint32_t)k * p.stage_cs_bytes, key_f,
+                                       w.t, k, bar_key_full + 8 * kb, pol_key);
                 }
-                for (int c = w.c0; c < w.c1; ++c) {
-                    const int zcs = zkey + 1 + c;
-                    for (int k = 0; k < p.n_chunks; ++k) {
-                        ptx::mbar_wait(bar_stage_empty + 8 * st, ph ^ 1u);
-                        const uint32_t dst = s_stage + (uint32_t)st * p.stage_bytes;
-                        ptx::mbar_arrive_expect_tx(bar_stage_full + 8 * st, p.stage_bytes);
-                        load_tile_chunk(p, &tmap, dst, zcs, w.t, k, bar_stage_full + 8 * st, pol_stream);
+                __syncwarp();
+                kb ^= 1;
+                if (kb == 0) kph ^= 1u;
+            }
+            for (int c = w.c0; c < w.c1; ++c) {
+                const uint8_t* cs_f = key_f + (size_t)(1 + c) * frame_bytes;
+                for (int k = 0; k < p.n_chunks; ++k) {
+                    if (p.prefetch_items > 0) prefetch_one();
+                    const uint32_t sb = strip_bytes<B>(p, w.t, k);
+                    ptx::mbar_wait(bar_stage_empty + 8 * st, ph ^ 1u);
+                    if (lane == 0) trace_ev(p, EV_P_EMPTY, n_items);
+                    const uint32_t dst = s_stage + (uint32_t)st * p.stage_bytes;
+                    if (elect_one()) {
+                        ptx::mbar_arrive_expect_tx(bar_stage_full + 8 * st, p.key_resident ? sb : 2u * sb);
+                        load_strips<B>(p, dst, cs_f, w.t, k, bar_stage_full + 8 * st, pol_stream);
                         if (!p.key_resident)
-                            load_tile_chunk(p, &tmap, dst + p.stage_cs_bytes, zkey, w.t, k, bar_stage_full + 8 * st,
-                                            pol_key);
-                        if (++st == p.n_stages) {
-                            st = 0;
-                            ph ^= 1u;
-                        }
+                            load_strips<B>(p, dst + p.stage_cs_bytes, key_f, w.t, k, bar_stage_full + 8 * st, pol_key);
+                    }
+                    __syncwarp();
+                    if (lane == 0) trace_ev(p, EV_P_ISSUED, n_items);
+                    ++n_items;
+                    if (++st == p.n_stages) {
+                        st = 0;
+                        ph ^= 1u;
                     }
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == kMmaWarp && !p.dbg_load_only) {
         // ================================================================ MMA issuer
-        if (lane == 0) {
-            ptx::mbar_wait(bar_phi, 0);
-            ptx::tc_fence_after();
-            int ab = 0, db = 0;
-            uint32_t aph = 0, dph = 0;
-            const int ksteps = p.chunk_k / 16;
-            for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-                Unit w;
-                if (!decode_unit(p, u, w)) continue;
-                for (int c = w.c0; c < w.c1; ++c) {
-                    ptx::mbar_wait(bar_d_empty + 8 * db, dph ^ 1u);
+        // The whole warp walks the schedule (warp-uniform control flow keeps every operand in
+        // uniform registers); one elected lane issues the tcgen05 instructions.
+        ptx::mbar_wait(bar_phi, 0);
+        ptx::tc_fence_after();
+        int ab = 0, db = 0;
+        uint32_t aph = 0, dph = 0;
+        const int ksteps = p.chunk_k / 16;
+        // descriptor of Phi's first K step; K step kg starts 2*kg core matrices (2*kg*lbo bytes)
+        // further, i.e. +2*lbo>>4 in the 14-bit start-address field (no carry: smem < 256 KB)
+        const uint64_t desc0 = ptx::smem_desc_noswizzle(s_phi, p.lbo, p.sbo);
+        const uint64_t desc_step = (uint64_t)((2u * p.lbo) >> 4);
+        const uint64_t desc_chunk = desc_step * (uint64_t)ksteps;
+        const uint32_t a_fold = (uint32_t)(p.chunk_k / 2);
+        int n_items = 0;
+        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+            Unit w;
+            if (!decode_unit(p, u, w)) continue;
+            for (int c = w.c0; c < w.c1; ++c) {
+                ptx::mbar_wait(bar_d_empty + 8 * db, dph ^ 1u);
+                ptx::tc_fence_after();
+                const uint32_t d_tm = tmem_base + d_col0 + (uint32_t)db * (uint32_t)p.d_cols;
+                uint64_t dk = desc0;
+                for (int k = 0; k < p.n_chunks; ++k, dk += desc_chunk) {
+                    ptx::mbar_wait(bar_a_full + 8 * ab, aph);
                     ptx::tc_fence_after();
-                    const uint32_t d_tm = tmem_base + d_col0 + (uint32_t)db * (uint32_t)p.d_cols;
-                    for (int k = 0; k < p.n_chunks; ++k) {
-                        ptx::mbar_wait(bar_a_full + 8 * ab, aph);
-                        ptx::tc_fence_after();
-                        const uint32_t a_tm = tmem_base + a_col0 + (uint32_t)ab * (uint32_t)p.a_cols;
+                    if (lane == 0) trace_ev(p, EV_M_AFULL, n_items);
+                    const uint32_t a_tm = tmem_base + a_col0 + (uint32_t)ab * (uint32_t)p.a_cols;
+                    const uint32_t acc0 = k > 0 ? 1u : 0u;
+                    if (elect_one()) {
                         for (int f = 0; f < p.F; ++f) {
-                            for (int s = 0; s < ksteps; ++s) {
-                                const int kg = k * ksteps + s;  // global K step (16 pixels)
-                                const uint64_t bdesc =
-                                    ptx::smem_desc_noswizzle(s_phi + (uint32_t)(2 * kg) * p.lbo, p.lbo, p.sbo);
-                                ptx::mma_f16_ts(d_tm + (uint32_t)(f * p.Mpad),
-                                                a_tm + (uint32_t)(f * (p.chunk_k / 2) + s * 8), bdesc, p.idesc,
-                                                (k > 0 || s > 0) ? 1u : 0u);
+                            const uint32_t d_f = d_tm + (uint32_t)(f * p.Mpad);
+                            const uint32_t a_f = a_tm + (uint32_t)f * a_fold;
+                            switch (ksteps) {
+                                case 4: issue_chunk<4>(d_f, a_f, dk, desc_step, p.idesc, acc0); break;
+                                case 8: issue_chunk<8>(d_f, a_f, dk, desc_step, p.idesc, acc0); break;
+                                case 16: issue_chunk<16>(d_f, a_f, dk, desc_step, p.idesc, acc0); break;
+                                default:
+                                    for (int s2 = 0; s2 < ksteps; ++s2)
+                                        ptx::mma_f16_ts(d_f, a_f + (uint32_t)(s2 * 8), dk + (uint64_t)s2 * desc_step,
+                                                        p.idesc, (k > 0 || s2 > 0) ? 1u : 0u);
                             }
                         }
                         ptx::tc_commit(bar_a_empty + 8 * ab);
-                        if (++ab == p.n_abuf) {
-                            ab = 0;
-                            aph ^= 1u;
-                        }
                     }
-                    ptx::tc_commit(bar_d_full + 8 * db);
-                    if (++db == p.n_dbuf) {
-                        db = 0;
-                        dph ^= 1u;
+                    __syncwarp();
+                    if (lane == 0) trace_ev(p, EV_M_ISSUED, n_items);
+                    ++n_items;
+                    if (++ab == p.n_abuf) {
+                        ab = 0;
+                        aph ^= 1u;
                     }
+                }
+                if (elect_one()) ptx::tc_commit(bar_d_full + 8 * db);
+                __syncwarp();
+                if (++db == p.n_dbuf) {
+                    db = 0;
+                    dph ^= 1u;
                 }
             }
         }
-    } else if (warp >= 4 && warp < 8) {
+    } else if (warp < kConvWarps) {
         // ================================================================ converters (a2 + a3)
-        const int lane_idx = (warp - 4) * 32 + (int)lane;       // TMEM lane = block slot
-        const uint32_t lane_bits = (uint32_t)((warp - 4) * 32) << 16;
-        const int Bconst = B;
-        // per-fold SMEM offset of this lane's block (row yy = 0) inside a stage
-        uint32_t off[kMaxFolds];
-#pragma unroll
-        for (int f = 0; f < kMaxFolds; ++f) {
-            off[f] = 0;
-            if (f < p.F) {
-                int b = f * p.L + lane_idx;
-                if (lane_idx < p.L && b < p.T_r * p.nbx) {
-                    int brow = b / p.nbx, bx = b % p.nbx;
-                    int pc = p.single_piece ? 0 : brow;
-                    int row0 = p.single_piece ? brow * Bconst : 0;
-                    int x = bx * Bconst;
-                    int box = x / p.box_w, xo = x % p.box_w;
-                    off[f] = (uint32_t)(pc * p.n_box + box) * p.box_bytes + (uint32_t)(row0 * p.box_w + xo);
-                }
-            }
-        }
+        const int wg = warp >> 2;                                // converter warpgroup 0/1
+        const int lane_idx = (warp & 3) * 32 + (int)lane;       // TMEM lane = block slot
+        const uint32_t lane_bits = (uint32_t)((warp & 3) * 32) << 16;
         constexpr int kWords = RowConv<B>::kWords;      // fp16x2 words per pixel row
         constexpr int kRowsPerSt = 32 / kWords;         // rows per 32-column TMEM store
+        const int groups = p.chunk_rows / kRowsPerSt;   // row groups per fold per chunk
+        const int n_groups = p.F * groups;
+        const int Bi = B;
         int st = 0, ab = 0, kb = 0;
         uint32_t ph = 0, aph = 0, kph = 0;
+        int n_items = 0;
+        const bool tr = (warp == 0 && lane == 0);
+        const uint32_t tab_lane = sbase + p.off_tab + (uint32_t)lane_idx * 8u;
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             Unit w;
             if (!decode_unit(p, u, w)) continue;
             if (p.key_resident) ptx::mbar_wait(bar_key_full + 8 * kb, kph);
+            const int tile_y0 = w.t * p.T_r * Bi;
             for (int c = w.c0; c < w.c1; ++c) {
                 for (int k = 0; k < p.n_chunks; ++k) {
                     ptx::mbar_wait(bar_stage_full + 8 * st, ph);
+                    if (tr) trace_ev(p, EV_C_FULL, n_items);
+                    if (p.dbg_load_only) {
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(bar_stage_empty + 8 * st);
+                        if (++st == p.n_stages) {
+                            st = 0;
+                            ph ^= 1u;
+                        }
+                        ++n_items;
+                        continue;
+                    }
                     ptx::mbar_wait(bar_a_empty + 8 * ab, aph ^ 1u);
                     ptx::tc_fence_after();
+                    if (tr) trace_ev(p, EV_C_AEMPTY, n_items);
                     const uint32_t cs_base = s_stage + (uint32_t)st * p.stage_bytes;
                     const uint32_t key_base = p.key_resident
                                                   ? s_key + (uint32_t)kb * p.key_bytes + (uint32_t)k * p.stage_cs_bytes
                                                   : cs_base + p.stage_cs_bytes;
                     const uint32_t a_tm = tmem_base + lane_bits + a_col0 + (uint32_t)ab * (uint32_t)p.a_cols;
-                    for (int f = 0; f < p.F; ++f) {
-                        const uint32_t cs_a = cs_base + off[f], key_a = key_base + off[f];
-                        const uint32_t a_f = a_tm + (uint32_t)(f * (p.chunk_k / 2));
-                        for (int r0 = 0; r0 < p.chunk_rows; r0 += kRowsPerSt) {
-                            uint32_t v[32];
+                    const int chunk_y = tile_y0 + k * p.chunk_rows;  // global row of chunk row 0 (block row 0)
+                    // row groups g = f*groups + gi, round-robin over the two warpgroups
+                    int f = 0, gi = wg;
+                    while (gi >= groups && f < p.F) {
+                        gi -= groups;
+                        ++f;
+                    }
+                    for (int g = wg; g < n_groups; g += 2) {
+                        const int r0 = gi * kRowsPerSt;
+                        uint32_t off, meta;
+                        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                                     : "=r"(off), "=r"(meta)
+                                     : "r"(tab_lane + (uint32_t)(f * 1024)));
+                        off += (uint32_t)(r0 * p.W);
+                        const bool half2 = (meta >> 16) & 1u;
+                        // rows of this group that lie inside the frame (the rest are zero)
+                        const int rows_in = p.H - (chunk_y + (int)(meta & 0xFFFFu) + r0);
+                        uint32_t v[32];
+                        if (rows_in >= kRowsPerSt) {
 #pragma unroll
                             for (int rr = 0; rr < kRowsPerSt; ++rr) {
-                                const uint32_t ro = (uint32_t)((r0 + rr) * p.box_w);
-                                RowConv<B>::run(cs_a + ro, key_a + ro, v + rr * kWords);
+                                const uint32_t ro = off + (uint32_t)(rr * p.W);
+                                RowConv<B>::run(cs_base + ro, key_base + ro, v + rr * kWords, half2);
                             }
-                            ptx::tmem_st_32x32b_x32(a_f + (uint32_t)(r0 * kWords), v);
+                        } else {
+#pragma unroll
+                            for (int rr = 0; rr < kRowsPerSt; ++rr) {
+                                if (rr < rows_in) {
+                                    const uint32_t ro = off + (uint32_t)(rr * p.W);
+                                    RowConv<B>::run(cs_base + ro, key_base + ro, v + rr * kWords, half2);
+                                } else {
+#pragma unroll
+                                    for (int i = 0; i < kWords; ++i) v[rr * kWords + i] = 0u;
+                                }
+                            }
+                        }
+                        ptx::tmem_st_32x32b_x32(a_tm + (uint32_t)(f * (p.chunk_k / 2) + r0 * kWords), v);
+                        gi += 2;
+                        while (gi >= groups) {
+                            gi -= groups;
+                            ++f;
                         }
                     }
+                    if (tr) trace_ev(p, EV_C_CONV, n_items);
                     ptx::tc_wait_st();
                     ptx::tc_fence_before();
+                    if (tr) trace_ev(p, EV_C_DONE, n_items);
+                    ++n_items;
                     __syncwarp();
                     if (lane == 0) {
                         ptx::mbar_arrive(bar_a_full + 8 * ab);
@@ -337,13 +584,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (kb == 0) kph ^= 1u;
             }
         }
-    } else if (warp >= 8) {
+    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4 && !p.dbg_load_only) {
         // ================================================================ epilogue (a6)
-        const int lane_idx = (warp - 8) * 32 + (int)lane;
-        const uint32_t lane_bits = (uint32_t)((warp - 8) * 32) << 16;
-        const bool vec = (p.M & 3) == 0;
+        // Output rows (blocks) are M*4 bytes apart.  For M == 4 a thread's row is one 16-byte
+        // vector and the warp's 32 rows are contiguous: store straight from registers.  For other
+        // M % 4 == 0 each 32-row x (16|32)-column accumulator chunk goes through a 4 KB
+        // XOR-swizzled SMEM tile so that every st.global.v4 instruction writes whole 64/128-byte
+        // row segments (bank-conflict-free on both sides).  Other M: scalar stores.
+        const int ew = warp - kEpiWarp0;
+        const int lane_idx = ew * 32 + (int)lane;
+        const uint32_t lane_bits = (uint32_t)(ew * 32) << 16;
+        const uint32_t stage_tile = sbase + p.off_epi + (uint32_t)ew * 4096u;
+        const int mode = (p.M == 4) ? 0 : ((p.M & 3) == 0 ? 1 : 2);
         int db = 0;
         uint32_t dph = 0;
+        int n_items = 0;
+        const bool tr = (warp == kEpiWarp0 && lane == 0);
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             Unit w;
             if (!decode_unit(p, u, w)) continue;
@@ -353,34 +609,54 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int c = w.c0; c < w.c1; ++c) {
                 ptx::mbar_wait(bar_d_full + 8 * db, dph);
                 ptx::tc_fence_after();
+                if (tr) trace_ev(p, EV_E_DFULL, n_items);
                 const long long cs_global = (long long)w.s * p.cs_per_stream_sel +
                                             (long long)(w.g - p.gop_begin) * (p.G - 1) + c;
+                float* const out_cs = p.out + (cs_global * p.nblk + blk0) * (long long)p.M;
                 const uint32_t d_tm = tmem_base + lane_bits + d_col0 + (uint32_t)db * (uint32_t)p.d_cols;
                 for (int f = 0; f < p.F; ++f) {
-                    const int b = f * p.L + lane_idx;
+                    const int row0 = f * p.L + ew * 32;            // tile block of this warp's lane 0
+                    const int b = row0 + (int)lane;
                     const bool valid = lane_idx < p.L && b < blocks_here;
-                    float* dst = p.out + (cs_global * p.nblk + blk0 + b) * (long long)p.M;
-                    for (int j = 0; j < p.Mpad; j += 16) {
+                    const int rows_valid = min(32, min(p.L - ew * 32, blocks_here - row0));
+                    if (mode == 0) {
                         uint32_t v[16];
-                        ptx::tmem_ld_32x32b_x16(d_tm + (uint32_t)(f * p.Mpad + j), v);
+                        ptx::tmem_ld_32x32b_x16(d_tm + (uint32_t)(f * p.Mpad), v);
                         ptx::tc_wait_ld();
-                        if (valid) {
-                            const int nm = min(16, p.M - j);
-                            if (vec) {
-#pragma unroll
-                                for (int q = 0; q < 16; q += 4)
-                                    if (q < nm) ptx::stg128(dst + j + q, v[q], v[q + 1], v[q + 2], v[q + 3]);
-                            } else {
-#pragma unroll
-                                for (int q = 0; q < 16; ++q)
-                                    if (q < nm) dst[j + q] = __uint_as_float(v[q]);
-                            }
+                        if (valid) ptx::stg128(out_cs + (long long)b * 4, v[0], v[1], v[2], v[3]);
+                        continue;
+                    }
+                    for (int j0 = 0; j0 < p.Mpad; j0 += 32) {
+                        const int cw = min(32, p.Mpad - j0);     // 16 or 32 columns
+                        uint32_t v[32];
+                        if (cw == 32) {
+                            ptx::tmem_ld_32x32b_x32(d_tm + (uint32_t)(f * p.Mpad + j0), v);
+                        } else {
+                            ptx::tmem_ld_32x32b_x16(d_tm + (uint32_t)(f * p.Mpad + j0),
+                                                    *reinterpret_cast<uint32_t(*)[16]>(v));
                         }
+                        ptx::tc_wait_ld();
+                        if (mode == 2) {
+                            if (valid) {
+                                float* dst = out_cs + (long long)b * p.M + j0;
+#pragma unroll
+                                for (int q = 0; q < 32; ++q)
+                                    if (q < cw && j0 + q < p.M) dst[q] = __uint_as_float(v[q]);
+                            }
+                            continue;
+                        }
+                        float* dst_row0 = out_cs + (long long)row0 * p.M;
+                        if (cw == 32)
+                            stage_store<32>(v, stage_tile, lane, dst_row0, p.M, j0, rows_valid);
+                        else
+                            stage_store<16>(v, stage_tile, lane, dst_row0, p.M, j0, rows_valid);
                     }
                 }
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(bar_d_empty + 8 * db);
+                if (tr) trace_ev(p, EV_E_DONE, n_items);
+                ++n_items;
                 if (++db == p.n_dbuf) {
                     db = 0;
                     dph ^= 1u;
@@ -392,7 +668,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    if (warp == 2) ptx::tmem_dealloc(tmem_base, kTmemCols);
+    if (warp == kMmaWarp) ptx::tmem_dealloc(tmem_base, kTmemCols);
 }
 
 }  // namespace csenc

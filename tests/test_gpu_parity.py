@@ -261,3 +261,19 @@ def test_bad_arguments_fail_loudly():
     with pytest.raises(P.CSError) as e:
         P.Encoder(64, 32, 4, 16, 16, bad)
     assert e.value.code == P.CS_ERR_PHI
+
+
+def test_encoders_with_different_plans_coexist():
+    """Regression: creating a second encoder with a smaller shared-memory plan must not break
+    launches of the first (the max-dynamic-smem attribute is per kernel, not per encoder)."""
+    cfg = synth.CONFIGS["C4"].with_(T=3)
+    frames = synth.gen_video(cfg)
+    fd = torch.from_numpy(frames).cuda()
+    encs = [P.Encoder(cfg.W, cfg.H, cfg.G, cfg.B, M, synth.phi_from_seed(synth.phi_seed(), M, 256))
+            for M in (16, 128)]
+    assert encs[0].plan()["smem_bytes"] != encs[1].plan()["smem_bytes"]
+    for M, e in zip((16, 128), encs):
+        out = e.encode_batch(fd)
+        torch.cuda.synchronize()
+        phi = synth.phi_from_seed(synth.phi_seed(), M, 256)
+        assert_parity(out.cpu().numpy(), frames, phi, cfg.G, cfg.B)
