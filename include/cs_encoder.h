@@ -63,13 +63,15 @@ typedef struct cs_plan_info {
     int lanes;             /* lanes used per fold */
     int chunk_rows;        /* pixel rows of a block per K-chunk (K-chunk = chunk_rows*B) */
     int stages;            /* shared-memory ring depth */
-    int key_resident;      /* 1: key tile kept in SMEM per work unit; 0: streamed per chunk */
+    int key_resident;      /* key strip: 2 = converter registers, 1 = resident in SMEM, 0 = streamed per chunk */
     int box_w;             /* bytes per strip row (= W: strips are full-width frame rows) */
     int smem_bytes;        /* dynamic shared memory per CTA */
     int tmem_cols;         /* TMEM columns used */
     int m_pad;             /* MMA N dimension (M rounded up to 16) */
     int chains;            /* independent TMEM accumulation chains per block (summed in the epilogue) */
     int prefetch_items;    /* items the producer prefetches into L2 ahead of the SMEM loads */
+    int a_bufs;            /* TMEM A-operand ring depth (converters -> MMA) */
+    int d_bufs;            /* TMEM accumulator ring depth (MMA -> epilogue) */
     int sms;               /* SMs of the device at create time */
 } cs_plan_info;
 

@@ -54,7 +54,7 @@ struct Plan {
     int chunk_rows = 0, n_chunks = 0, chunk_k = 0;
     int pieces = 0, piece_rows = 0, single_piece = 0;
     uint32_t piece_bytes = 0, stage_cs_bytes = 0, stage_bytes = 0, key_bytes = 0;
-    int key_resident = 0, n_stages = 0, prefetch_items = 0;
+    int key_resident = 0, key_regs = 0, n_stages = 0, prefetch_items = 0;
     uint32_t off_tab = 0, off_epi = 0, off_phi = 0, off_key = 0, off_stage = 0, smem_bytes = 0;
     int a_cols = 0, d_cols = 0, tmem_cols = 0, n_abuf = 2, n_dbuf = 2;
     double score = -1.0;
@@ -64,7 +64,10 @@ struct Geometry {
     int W, H, G, B, M, N, Mpad, nbx, nby, nblk;
 };
 
-bool try_plan(const Geometry& g, int T_r, int chunk_rows, bool key_res, int smem_limit, Plan& p) {
+// key_mode: 0 = key strip streamed with every item, 1 = resident in SMEM (double-buffered),
+//           2 = in converter registers (arrives once per unit through a ring slot)
+bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem_limit, Plan& p) {
+    const bool key_res = key_mode == 1;
     p = Plan();
     const int words = g.B / 2;          // fp16x2 columns per pixel row
     const int rows_per_st = 32 / words;
@@ -80,14 +83,34 @@ bool try_plan(const Geometry& g, int T_r, int chunk_rows, bool key_res, int smem
     p.n_chunks = g.B / chunk_rows;
     p.chunk_k = chunk_rows * g.B;
     p.a_cols = p.F * p.chunk_k / 2;
-    p.n_abuf = 2;
-    // Two accumulators (epilogue of frame i overlaps the MMAs of frame i+1) when TMEM allows.
-    // (Measured, tools/mma_microbench*.cu: dependent MMAs into one accumulator issue back to
-    // back, so no split-K accumulation chains are needed.)
-    p.n_dbuf = (p.n_abuf * p.a_cols + 2 * p.F * g.Mpad <= (int)csenc::kTmemCols) ? 2 : 1;
+    // TMEM rings: A buffers (converter -> MMA) and accumulators (MMA -> epilogue).  Deeper rings
+    // decouple the converter and epilogue latencies (measured: with 2+2 a slow converter OR a
+    // slow epilogue stalls the chain).  Prefer (3+, 3+), then (2, 2).  (Dependent MMAs into one
+    // accumulator issue back to back -- tools/mma_microbench*.cu -- so no split-K chains.)
+    {
+        const int dc = p.F * g.Mpad;
+        const int cands[][2] = {{4, 4}, {4, 3}, {3, 4}, {3, 3}, {4, 2}, {3, 2}, {2, 3}, {2, 2}, {2, 1}, {1, 1}};
+        p.n_abuf = 0;
+        for (auto& c : cands)
+            if (c[0] * p.a_cols + c[1] * dc <= (int)csenc::kTmemCols) {
+                p.n_abuf = c[0];
+                p.n_dbuf = c[1];
+                break;
+            }
+        if (p.n_abuf == 0) return false;
+        if (const char* e = std::getenv("CSENC_TMEM_BUFS")) {  // experiment knob "A,D"
+            int a = 0, d = 0;
+            if (std::sscanf(e, "%d,%d", &a, &d) == 2 && a >= 1 && d >= 1 && a <= 4 && d <= 4 &&
+                a * p.a_cols + d * dc <= (int)csenc::kTmemCols) {
+                p.n_abuf = a;
+                p.n_dbuf = d;
+            }
+        }
+    }
     p.d_cols = p.F * g.Mpad;
     p.tmem_cols = p.n_abuf * p.a_cols + p.n_dbuf * p.d_cols;
     if (p.tmem_cols > (int)csenc::kTmemCols) return false;
+    const double ring_q = std::min(p.n_abuf, 3) * std::min(p.n_dbuf, 3) / 9.0;  // prefer 3+3
     // Stage layout: [piece][piece_rows][W] -- each piece is one contiguous strip of full-width
     // frame rows, moved by a single bulk copy.
     if (p.n_chunks == 1) {
@@ -101,8 +124,14 @@ bool try_plan(const Geometry& g, int T_r, int chunk_rows, bool key_res, int smem
     p.piece_bytes = align_up((uint32_t)(p.piece_rows * g.W), 128);
     p.stage_cs_bytes = (uint32_t)p.pieces * p.piece_bytes;
     p.key_resident = key_res ? 1 : 0;
+    p.key_regs = key_mode == 2 ? 1 : 0;
+    if (p.key_regs) {
+        // each converter warpgroup holds <= 2 row groups (16 u8 words each) of the key
+        const int groups_per_fold = chunk_rows / rows_per_st;
+        if (p.n_chunks != 1 || p.F * groups_per_fold > 4) return false;
+    }
     p.key_bytes = key_res ? (uint32_t)p.n_chunks * p.stage_cs_bytes : 0;
-    p.stage_bytes = key_res ? p.stage_cs_bytes : 2 * p.stage_cs_bytes;
+    p.stage_bytes = (key_res || p.key_regs) ? p.stage_cs_bytes : 2 * p.stage_cs_bytes;
     const uint32_t phi_bytes = (uint32_t)g.Mpad * (uint32_t)g.N * 2u;
     p.off_tab = 1024;  // barriers live in the first KB, then the converter offset table (8 KB)
     p.off_epi = 1024 + 8192;  // epilogue staging tiles (4 warps x 4 KB)
@@ -120,12 +149,14 @@ bool try_plan(const Geometry& g, int T_r, int chunk_rows, bool key_res, int smem
     // of pipeline handoffs, so larger strips win until ~30 KB; >= 3 slots are enough once the
     // producer is warp-uniform; a resident key beats re-streaming it by ~25%.
     const double util = (double)tile_blocks / (p.F * 128.0);
-    double s = util * (key_res ? 1.0 : 0.75);
+    double s = util * ((key_res || p.key_regs) ? 1.0 : 0.75);
+    if (p.key_regs) s *= 1.02;  // no key LDS per item, no key SMEM
     s *= std::pow(std::min(1.0, p.stage_cs_bytes / 30720.0), 0.7);
     if (p.n_stages < 3) s *= 0.9;
     const double inflight = (double)(p.n_stages - 1) * p.stage_cs_bytes;
     s *= std::min(1.0, inflight / 61440.0);
     if (p.n_dbuf < 2) s *= 0.8;
+    s *= 0.85 + 0.15 * ring_q;
     p.score = s;
     return true;
 }
@@ -145,10 +176,10 @@ bool make_plan(const Geometry& g, int smem_limit, Plan& best) {
         if (f_tr && T_r != f_tr) continue;
         for (int cr = g.B; cr >= 1; --cr) {
             if (f_cr && cr != f_cr) continue;
-            for (int kr = 1; kr >= 0; --kr) {
+            for (int kr = 2; kr >= 0; --kr) {
                 if (f_kr >= 0 && kr != f_kr) continue;
                 Plan p;
-                if (!try_plan(g, T_r, cr, kr == 1, smem_limit, p)) continue;
+                if (!try_plan(g, T_r, cr, kr, smem_limit, p)) continue;
                 if (f_st > 0 && f_st < p.n_stages) {
                     p.smem_bytes -= (uint32_t)(p.n_stages - f_st) * p.stage_bytes;
                     p.n_stages = f_st;
@@ -169,7 +200,7 @@ WorkSplit choose_split(const Geometry& g, const Plan& p, int n_seq, int n_gops_s
     WorkSplit best{1, std::max(1, g.G - 1), (int)base};
     if (g.G <= 1) return best;
     double best_cost = 1e300;
-    const double key_cost = p.key_resident ? 1.0 : 0.0;
+    const double key_cost = (p.key_resident || p.key_regs) ? 1.0 : 0.0;
     for (int ns = 1; ns <= g.G - 1; ++ns) {
         int cpu = cdiv(g.G - 1, ns);
         if (ns > 1 && cdiv(g.G - 1, cpu) != ns) continue;  // identical to a smaller ns
@@ -300,6 +331,7 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.stage_bytes = pl.stage_bytes;
     kp.key_bytes = pl.key_bytes;
     kp.key_resident = pl.key_resident;
+    kp.key_regs = pl.key_regs;
     kp.n_stages = pl.n_stages;
     kp.off_phi = pl.off_phi;
     kp.off_key = pl.off_key;
@@ -323,6 +355,7 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.off_tab = pl.off_tab;
     kp.off_epi = pl.off_epi;
     kp.dbg_load_only = env_int("CSENC_DBG_LOAD_ONLY", 0);
+    kp.dbg_flags = env_int("CSENC_DBG_FLAGS", 0);
     kp.trace = e->trace;
     kp.trace_cap = e->trace_cap;
     const int grid = std::max(1, std::min(e->sms, kp.n_units));
@@ -423,11 +456,16 @@ int cs_encoder_create(int W, int H, int gop, int B, int M, const uint16_t* phi_f
     e->sbo = 128;
     e->lbo = (uint32_t)g.Mpad * 16u;
     e->phi_bytes = (uint32_t)g.Mpad * (uint32_t)g.N * 2u;
+    // The converters emit each group of four pixels j = 4q..4q+3 of a block row in K order
+    // (4q, 4q+2, 4q+1, 4q+3) (see ptx::residual4), so MMA K index k holds pixel
+    // j = 4(k/4) + {0,2,1,3}[k%4]; Phi's column k must be pixel j's column.
+    static const int kPerm[4] = {0, 2, 1, 3};
     std::vector<uint16_t> arranged((size_t)g.Mpad * g.N, 0);
     for (int n = 0; n < M; ++n)
         for (int k = 0; k < g.N; ++k) {
+            const int j = (k & ~3) | kPerm[k & 3];
             size_t byte = (size_t)(k / 8) * e->lbo + (size_t)(n / 8) * e->sbo + (size_t)(n % 8) * 16 + (size_t)(k % 8) * 2;
-            arranged[byte / 2] = phi_fp16[(size_t)n * g.N + k];
+            arranged[byte / 2] = phi_fp16[(size_t)n * g.N + j];
         }
     // instruction descriptor, kind::f16: D fp32 (bit 4), A/B fp16 (0), K-major (0),
     // N>>3 at bits 17-22, M>>4 at bits 24-28 (M = 128 lanes).
@@ -465,9 +503,11 @@ static void fill_info(const Plan& p, const Geometry& g, int sms, cs_plan_info* i
     info->lanes = p.L;
     info->chunk_rows = p.chunk_rows;
     info->stages = p.n_stages;
-    info->key_resident = p.key_resident;
+    info->key_resident = p.key_regs ? 2 : p.key_resident;
     info->box_w = g.W;  /* strips are full-width rows */
     info->prefetch_items = p.prefetch_items;
+    info->a_bufs = p.n_abuf;
+    info->d_bufs = p.n_dbuf;
     info->smem_bytes = (int)p.smem_bytes;
     info->tmem_cols = p.tmem_cols;
     info->m_pad = g.Mpad;

@@ -43,6 +43,7 @@ constexpr int kMmaWarp = 13;                     // MMA issuer + TMEM allocator
 constexpr int kThreads = 14 * 32;
 constexpr int kMaxFolds = 8;
 constexpr int kMaxStages = 8;
+constexpr int kMaxTmemBufs = 4;                  // TMEM A buffers / accumulators (ring depth)
 constexpr uint32_t kTmemCols = 512;
 
 struct KParams {
@@ -60,18 +61,20 @@ struct KParams {
     int single_piece;
     uint32_t piece_bytes, stage_cs_bytes, stage_bytes, key_bytes;
     int key_resident, n_stages, prefetch_items;
+    int key_regs;             // 1: the unit's key strip arrives in a ring slot and lives in converter registers
     uint32_t off_tab, off_epi, off_phi, off_key, off_stage;
     // work
     int G, T, gop_begin, n_gops_sel, cs_per_stream_sel, n_splits, cs_per_unit, n_units;
     // MMA
     uint32_t idesc, lbo, sbo;
     int a_cols, d_cols;
-    int n_abuf, n_dbuf;
+    int n_abuf, n_dbuf;       // TMEM ring depths (1..kMaxTmemBufs)
     // optional timeline trace (CTA 0 only): trace[event * trace_cap + i] = clock64 of the i-th
     // occurrence of the event; nullptr disables (the default)
     unsigned long long* trace;
     int trace_cap;
     int dbg_load_only;        // debug: converters release stages without converting; no MMA/epilogue
+    int dbg_flags;            // debug ablations: 2 = converters skip SMEM reads/ALU (A = 0), 4 = early slot release
 };
 
 // trace events
@@ -220,6 +223,59 @@ struct RowConv<32> {
     }
 };
 
+// Same as RowConv, with the key row's u8 words already in registers (kw: B/4 words).
+template <int B>
+struct RowConvK;
+template <>
+struct RowConvK<8> {
+    __device__ __forceinline__ static void run(uint32_t cs, const uint32_t* kw, uint32_t* w, bool) {
+        uint2 c = ptx::lds64(cs);
+        ptx::residual4(c.x, kw[0], w[0], w[1]);
+        ptx::residual4(c.y, kw[1], w[2], w[3]);
+    }
+};
+template <>
+struct RowConvK<16> {
+    __device__ __forceinline__ static void run(uint32_t cs, const uint32_t* kw, uint32_t* w, bool) {
+        uint4 c = ptx::lds128(cs);
+        ptx::residual4(c.x, kw[0], w[0], w[1]);
+        ptx::residual4(c.y, kw[1], w[2], w[3]);
+        ptx::residual4(c.z, kw[2], w[4], w[5]);
+        ptx::residual4(c.w, kw[3], w[6], w[7]);
+    }
+};
+template <>
+struct RowConvK<32> {
+    __device__ __forceinline__ static void run(uint32_t cs, const uint32_t* kw, uint32_t* w, bool half2) {
+        RowConvK<16>::run(cs, kw, w, true);
+        if (half2) {
+            RowConvK<16>::run(cs + 16, kw + 4, w + 8, true);
+        } else {
+#pragma unroll
+            for (int i = 8; i < 16; ++i) w[i] = 0u;
+        }
+    }
+};
+
+// u8 words of one row segment of B pixels (B/4 words) from SMEM
+template <int B>
+__device__ __forceinline__ void load_row_words(uint32_t addr, uint32_t* kw) {
+    if constexpr (B == 8) {
+        uint2 k = ptx::lds64(addr);
+        kw[0] = k.x;
+        kw[1] = k.y;
+    } else {
+#pragma unroll
+        for (int h = 0; h < B / 16; ++h) {
+            uint4 k = ptx::lds128(addr + 16 * h);
+            kw[4 * h] = k.x;
+            kw[4 * h + 1] = k.y;
+            kw[4 * h + 2] = k.z;
+            kw[4 * h + 3] = k.w;
+        }
+    }
+}
+
 __device__ __forceinline__ bool elect_one() {
     uint32_t pred = 0;
     asm volatile("{\n\t.reg .pred P1;\n\telect.sync _|P1, 0xffffffff;\n\tselp.b32 %0, 1, 0, P1;\n\t}"
@@ -242,7 +298,7 @@ __device__ __forceinline__ void issue_chunk(uint32_t d, uint32_t a, uint64_t bde
 // v = this lane's CW values (its row); rows r < rows_valid are stored at dst_row0 + r*M + col.
 template <int CW>
 __device__ __forceinline__ void stage_store(const uint32_t* v, uint32_t tile, uint32_t lane, float* dst_row0, int M,
-                                            int j0, int rows_valid) {
+                                            int j0, int rows_valid, bool skip = false) {
     constexpr int CPR = CW / 4;           // 16-byte chunks per row
     constexpr uint32_t PITCH = CW * 4;    // staged row pitch
     constexpr int RPI = 32 / CPR;         // rows per store instruction
@@ -260,7 +316,7 @@ __device__ __forceinline__ void stage_store(const uint32_t* v, uint32_t tile, ui
         const int r = it * RPI + rsub;
         const int slot = (CPR == 8) ? (cc ^ (r & 7)) : (cc ^ ((r >> 1) & 3));
         uint4 t = ptx::lds128(tile + (uint32_t)r * PITCH + (uint32_t)slot * 16u);
-        if (r < rows_valid && col < M) ptx::stg128(dst_row0 + (long long)r * M + col, t.x, t.y, t.z, t.w);
+        if (r < rows_valid && col < M && !skip) ptx::stg128(dst_row0 + (long long)r * M + col, t.x, t.y, t.z, t.w);
     }
     __syncwarp();
 }
@@ -273,17 +329,17 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
     const uint32_t lane = threadIdx.x & 31u;
 
     // barrier block at sbase: [stage_full x8][stage_empty x8][key_full x2][key_empty x2]
-    //                         [a_full x2][a_empty x2][d_full x2][d_empty x2][phi_full][tmem slot]
+    //                         [a_full x4][a_empty x4][d_full x4][d_empty x4][phi_full][tmem slot]
     const uint32_t bar_stage_full = sbase;
     const uint32_t bar_stage_empty = sbase + 8 * kMaxStages;
     const uint32_t bar_key_full = sbase + 16 * kMaxStages;
     const uint32_t bar_key_empty = bar_key_full + 16;
     const uint32_t bar_a_full = bar_key_full + 32;
-    const uint32_t bar_a_empty = bar_key_full + 48;
-    const uint32_t bar_d_full = bar_key_full + 64;
-    const uint32_t bar_d_empty = bar_key_full + 80;
-    const uint32_t bar_phi = bar_key_full + 96;
-    const uint32_t tmem_slot = bar_key_full + 104;
+    const uint32_t bar_a_empty = bar_a_full + 8 * kMaxTmemBufs;
+    const uint32_t bar_d_full = bar_a_empty + 8 * kMaxTmemBufs;
+    const uint32_t bar_d_empty = bar_d_full + 8 * kMaxTmemBufs;
+    const uint32_t bar_phi = bar_d_empty + 8 * kMaxTmemBufs;
+    const uint32_t tmem_slot = bar_phi + 8;
     const uint32_t s_phi = sbase + p.off_phi;
     const uint32_t s_key = sbase + p.off_key;
     const uint32_t s_stage = sbase + p.off_stage;
@@ -296,6 +352,8 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(bar_key_full + 8 * i, 1);
             ptx::mbar_init(bar_key_empty + 8 * i, kConvWarps);
+        }
+        for (int i = 0; i < kMaxTmemBufs; ++i) {
             ptx::mbar_init(bar_a_full + 8 * i, kConvWarps);
             ptx::mbar_init(bar_a_empty + 8 * i, 1);
             ptx::mbar_init(bar_d_full + 8 * i, 1);
@@ -372,7 +430,20 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
             Unit w;
             if (!decode_unit(p, u, w)) continue;
             const uint8_t* key_f = p.frames + (size_t)key_frame(p, w) * frame_bytes;
-            if (p.key_resident) {
+            if (p.key_regs) {  // the key strip is the unit's first ring item
+                const uint32_t kbytes = strip_bytes<B>(p, w.t, 0);
+                ptx::mbar_wait(bar_stage_empty + 8 * st, ph ^ 1u);
+                if (elect_one()) {
+                    ptx::mbar_arrive_expect_tx(bar_stage_full + 8 * st, kbytes);
+                    load_strips<B>(p, s_stage + (uint32_t)st * p.stage_bytes, key_f, w.t, 0, bar_stage_full + 8 * st,
+                                   pol_key);
+                }
+                __syncwarp();
+                if (++st == p.n_stages) {
+                    st = 0;
+                    ph ^= 1u;
+                }
+            } else if (p.key_resident) {
                 ptx::mbar_wait(bar_key_empty + 8 * kb, kph ^ 1u);
                 uint32_t kbytes = 0;
                 for (int k = 0; k < p.n_chunks; ++k) kbytes += strip_bytes<B>(p, w.t, k);
@@ -395,9 +466,9 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                     if (lane == 0) trace_ev(p, EV_P_EMPTY, n_items);
                     const uint32_t dst = s_stage + (uint32_t)st * p.stage_bytes;
                     if (elect_one()) {
-                        ptx::mbar_arrive_expect_tx(bar_stage_full + 8 * st, p.key_resident ? sb : 2u * sb);
+                        ptx::mbar_arrive_expect_tx(bar_stage_full + 8 * st, (p.key_resident || p.key_regs) ? sb : 2u * sb);
                         load_strips<B>(p, dst, cs_f, w.t, k, bar_stage_full + 8 * st, pol_stream);
-                        if (!p.key_resident)
+                        if (!p.key_resident && !p.key_regs)
                             load_strips<B>(p, dst + p.stage_cs_bytes, key_f, w.t, k, bar_stage_full + 8 * st, pol_key);
                     }
                     __syncwarp();
@@ -487,11 +558,49 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
         int n_items = 0;
         const bool tr = (warp == 0 && lane == 0);
         const uint32_t tab_lane = sbase + p.off_tab + (uint32_t)lane_idx * 8u;
+        // key_regs mode: this thread's key rows for its (<= 2) row groups, u8 words; the groups'
+        // geometry is constant for the whole kernel
+        uint32_t kreg[2][16];
+        uint32_t g_off[2] = {0, 0}, g_meta[2] = {0, 0}, g_acol[2] = {0, 0};
+        int g_r0[2] = {0, 0};
+        if (p.key_regs) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int g = wg + 2 * j;
+                if (g < n_groups) {
+                    const int f = g / groups, r0 = (g - f * groups) * kRowsPerSt;
+                    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                                 : "=r"(g_off[j]), "=r"(g_meta[j])
+                                 : "r"(tab_lane + (uint32_t)(f * 1024)));
+                    g_off[j] += (uint32_t)(r0 * p.W);
+                    g_r0[j] = r0 + (int)(g_meta[j] & 0xFFFFu);
+                    g_acol[j] = (uint32_t)(f * (p.chunk_k / 2) + r0 * kWords);
+                }
+            }
+        }
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             Unit w;
             if (!decode_unit(p, u, w)) continue;
             if (p.key_resident) ptx::mbar_wait(bar_key_full + 8 * kb, kph);
             const int tile_y0 = w.t * p.T_r * Bi;
+            if (p.key_regs) {
+                ptx::mbar_wait(bar_stage_full + 8 * st, ph);
+                const uint32_t kbase = s_stage + (uint32_t)st * p.stage_bytes;
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    if (wg + 2 * j < n_groups) {
+#pragma unroll
+                        for (int rr = 0; rr < kRowsPerSt; ++rr)
+                            load_row_words<B>(kbase + g_off[j] + (uint32_t)(rr * p.W), &kreg[j][rr * (B / 4)]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(bar_stage_empty + 8 * st);
+                if (++st == p.n_stages) {
+                    st = 0;
+                    ph ^= 1u;
+                }
+            }
             for (int c = w.c0; c < w.c1; ++c) {
                 for (int k = 0; k < p.n_chunks; ++k) {
                     ptx::mbar_wait(bar_stage_full + 8 * st, ph);
@@ -515,13 +624,49 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                                                   : cs_base + p.stage_cs_bytes;
                     const uint32_t a_tm = tmem_base + lane_bits + a_col0 + (uint32_t)ab * (uint32_t)p.a_cols;
                     const int chunk_y = tile_y0 + k * p.chunk_rows;  // global row of chunk row 0 (block row 0)
+                    if (p.dbg_flags & 2) {
+                        uint32_t v[32];
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] = 0u;
+#pragma unroll
+                        for (int j = 0; j < 2; ++j)
+                            if (wg + 2 * j < n_groups) ptx::tmem_st_32x32b_x32(a_tm + g_acol[j], v);
+                    } else if (p.key_regs) {
+                        // <= 2 row groups per warpgroup (planner guarantee); key words in kreg[j]
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) {
+                            if (wg + 2 * j < n_groups) {
+                                const bool half2 = (g_meta[j] >> 16) & 1u;
+                                const int rows_in = p.H - (chunk_y + g_r0[j]);
+                                uint32_t v[32];
+                                if (rows_in >= kRowsPerSt) {
+#pragma unroll
+                                    for (int rr = 0; rr < kRowsPerSt; ++rr)
+                                        RowConvK<B>::run(cs_base + g_off[j] + (uint32_t)(rr * p.W),
+                                                         &kreg[j][rr * (B / 4)], v + rr * kWords, half2);
+                                } else {
+#pragma unroll
+                                    for (int rr = 0; rr < kRowsPerSt; ++rr) {
+                                        if (rr < rows_in) {
+                                            RowConvK<B>::run(cs_base + g_off[j] + (uint32_t)(rr * p.W),
+                                                             &kreg[j][rr * (B / 4)], v + rr * kWords, half2);
+                                        } else {
+#pragma unroll
+                                            for (int i = 0; i < kWords; ++i) v[rr * kWords + i] = 0u;
+                                        }
+                                    }
+                                }
+                                ptx::tmem_st_32x32b_x32(a_tm + g_acol[j], v);
+                            }
+                        }
+                    }
                     // row groups g = f*groups + gi, round-robin over the two warpgroups
-                    int f = 0, gi = wg;
+                    int f = 0, gi = p.key_regs ? n_groups : wg;
                     while (gi >= groups && f < p.F) {
                         gi -= groups;
                         ++f;
                     }
-                    for (int g = wg; g < n_groups; g += 2) {
+                    for (int g = p.key_regs ? n_groups : wg; g < n_groups; g += 2) {
                         const int r0 = gi * kRowsPerSt;
                         uint32_t off, meta;
                         asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
@@ -646,10 +791,11 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                             continue;
                         }
                         float* dst_row0 = out_cs + (long long)row0 * p.M;
+                        const bool skip = (p.dbg_flags & 8) != 0;
                         if (cw == 32)
-                            stage_store<32>(v, stage_tile, lane, dst_row0, p.M, j0, rows_valid);
+                            stage_store<32>(v, stage_tile, lane, dst_row0, p.M, j0, rows_valid, skip);
                         else
-                            stage_store<16>(v, stage_tile, lane, dst_row0, p.M, j0, rows_valid);
+                            stage_store<16>(v, stage_tile, lane, dst_row0, p.M, j0, rows_valid, skip);
                     }
                 }
                 ptx::tc_fence_before();

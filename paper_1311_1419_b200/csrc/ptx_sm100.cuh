@@ -49,6 +49,19 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// Same, letting the hardware suspend the thread (up to hint_ns) until the phase completes
+// instead of returning immediately: waiting warps stop re-probing the barrier.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t bar, uint32_t parity, uint32_t hint_ns) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"(hint_ns)
+        : "memory");
+    return ok != 0;
+}
 // Wait for the phase with the given parity to complete.  A watchdog traps after ~20 s so a
 // protocol bug surfaces as a launch error instead of a hung GPU.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
@@ -203,14 +216,42 @@ __device__ __forceinline__ uint32_t hsub2(uint32_t a, uint32_t b) {
     asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
     return d;
 }
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t c) {  // (a & b) | c
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+// Converter variant (compile-time; measured in DESIGN.md sec.7):
+//   0: four PRMT per four pixels (default)
+//   1: four fused LOP3 + two SHF (ALU pipe only)
+//   2: two fused LOP3 (bytes 0,2) + two PRMT (bytes 1,3)
+// Measured on B200 (C4 sweep / C5): all three within run-to-run noise -- the converter's
+// instruction mix is not the limiter (tools/sweep6.sh).
+#ifndef CSENC_CONV
+#define CSENC_CONV 0
+#endif
+
 // Four u8 pixels of the CS frame (c) and of the key (k) -> two fp16x2 words holding the exact
-// residuals c_i - k_i.  0x64XX is fp16(1024 + XX) for a byte XX, so (1024+c) - (1024+k) is exact
-// (every integer below 2048 is an fp16; the difference is an integer in [-255, 255]).
-// Element order: word0 = {px0 (low half), px1}, word1 = {px2, px3}.
+// residuals c_i - k_i.  A byte XX placed in the low half of a 16-bit lane under 0x64 is
+// fp16(1024 + XX), so (1024+c) - (1024+k) is exact (every integer below 2048 is an fp16; the
+// difference is an integer in [-255, 255]).  Element order: word0 = {px0 (low half), px2},
+// word1 = {px1, px3}: within every group of four pixels the K index order is (0, 2, 1, 3); the
+// host stores Phi with its columns in the same order, so the contraction is unchanged.
 __device__ __forceinline__ void residual4(uint32_t c, uint32_t k, uint32_t& w0, uint32_t& w1) {
-    const uint32_t magic = 0x64646464u;
-    w0 = hsub2(prmt(c, magic, 0x4140u), prmt(k, magic, 0x4140u));
-    w1 = hsub2(prmt(c, magic, 0x4342u), prmt(k, magic, 0x4342u));
+#if CSENC_CONV == 0
+    const uint32_t m8 = 0x64646464u;
+    w0 = hsub2(prmt(c, m8, 0x4240u), prmt(k, m8, 0x4240u));
+    w1 = hsub2(prmt(c, m8, 0x4341u), prmt(k, m8, 0x4341u));
+#elif CSENC_CONV == 1
+    const uint32_t mask = 0x00FF00FFu, magic = 0x64006400u;
+    w0 = hsub2(lop3_and_or(c, mask, magic), lop3_and_or(k, mask, magic));
+    w1 = hsub2(lop3_and_or(c >> 8, mask, magic), lop3_and_or(k >> 8, mask, magic));
+#else
+    const uint32_t mask = 0x00FF00FFu, magic = 0x64006400u, m8 = 0x64646464u;
+    w0 = hsub2(lop3_and_or(c, mask, magic), lop3_and_or(k, mask, magic));
+    w1 = hsub2(prmt(c, m8, 0x4341u), prmt(k, m8, 0x4341u));
+#endif
 }
 
 // ------------------------------------------------------------------ UMMA descriptors
