@@ -153,6 +153,9 @@ def run_ours(args, cfg, Ms):
         encs.append(e)
         outs.append(torch.empty(e.out_shape(n_seq, cfg.T), dtype=torch.float32, device=dev))
     stream = torch.cuda.current_stream(dev)
+    if not args.no_autotune:  # pick the fastest of the planner's top plans (outputs are bit-identical)
+        for i, e in enumerate(encs):
+            e.autotune(frames, outs[i], max_candidates=args.tune_candidates, reps=2, stream=stream)
 
     def step(ev=None):
         for i, e in enumerate(encs):
@@ -345,6 +348,8 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-autotune", action="store_true")
+    ap.add_argument("--tune-candidates", type=int, default=6)
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         ap.error("--warmup must be >= 3")

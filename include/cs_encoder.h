@@ -95,6 +95,19 @@ int cs_encoder_create(int W, int H, int gop, int B, int M, const uint16_t* phi_f
  * synchronised every stream that used it. */
 int cs_encoder_destroy(cs_encoder* enc);
 
+/* Autotune: time the planner's best `max_candidates` plans (ranked by its cost model) on the
+ * caller's buffers -- `reps` timed cs_encode_batch calls each on `stream`, after one warm-up --
+ * and keep the fastest for all later encodes.  Every plan produces bit-identical measurements
+ * (the per-block K order of the MMA chain does not depend on the plan), so tuning is invisible
+ * in the output.  Synchronises `stream`.  Not safe concurrently with other encodes of `enc`. */
+int cs_encoder_autotune(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, int T, float* meas_dev,
+                        int max_candidates, int reps, cs_stream_t stream);
+
+/* Number of feasible plans the planner ranked (-1 for NULL), and explicit selection of one
+ * (tests / tools).  Host only; not safe concurrently with encodes of `enc`. */
+int cs_encoder_num_candidates(const cs_encoder* enc);
+int cs_encoder_set_candidate(cs_encoder* enc, int index);
+
 /* Fill *info with the tiling plan.  Host only. */
 int cs_encoder_plan(const cs_encoder* enc, cs_plan_info* info);
 

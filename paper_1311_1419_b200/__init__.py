@@ -56,6 +56,9 @@ def lib() -> ctypes.CDLL:
             "cs_encoder_destroy": (c_int, [vp]),
             "cs_encoder_plan": (c_int, [vp, ctypes.POINTER(PlanInfo)]),
             "cs_encoder_set_trace": (c_int, [vp, vp, c_int]),
+            "cs_encoder_autotune": (c_int, [vp, vp, c_int, c_int, vp, c_int, c_int, vp]),
+            "cs_encoder_num_candidates": (c_int, [vp]),
+            "cs_encoder_set_candidate": (c_int, [vp, c_int]),
             "cs_encode_gop": (c_int, [vp, vp, c_int, vp, vp]),
             "cs_encode_batch": (c_int, [vp, vp, c_int, c_int, vp, vp]),
             "cs_encode_batch_gops": (c_int, [vp, vp, c_int, c_int, c_int, c_int, vp, vp]),
@@ -193,6 +196,24 @@ class Encoder:
         assert out.numel() >= self.measurement_count(n_seq, T)
         _check(lib().cs_encode_batch(self._h, _ptr(frames), n_seq, T, _ptr(out), _stream_handle(stream)))
         return out
+
+    def autotune(self, frames, out=None, max_candidates: int = 6, reps: int = 3, stream=None) -> dict:
+        """Time the planner's top plans on these buffers and keep the fastest (outputs are bitwise
+        identical across plans).  Returns the chosen plan."""
+        import torch
+        n_seq, T = frames.shape[:2]
+        if out is None:
+            out = torch.empty(self.out_shape(n_seq, T), dtype=torch.float32, device=frames.device)
+        _check(lib().cs_encoder_autotune(self._h, _ptr(frames), n_seq, T, _ptr(out), max_candidates, reps,
+                                         _stream_handle(stream)))
+        return self.plan()
+
+    def num_candidates(self) -> int:
+        return lib().cs_encoder_num_candidates(self._h)
+
+    def set_candidate(self, index: int) -> dict:
+        _check(lib().cs_encoder_set_candidate(self._h, index))
+        return self.plan()
 
     def encode_batch_gops(self, frames, gop_begin: int, gop_end: int, out, stream=None):
         n_seq, T = frames.shape[:2]

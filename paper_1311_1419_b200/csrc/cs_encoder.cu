@@ -128,7 +128,7 @@ bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem
     if (p.key_regs) {
         // each converter warpgroup holds <= 2 row groups (16 u8 words each) of the key
         const int groups_per_fold = chunk_rows / rows_per_st;
-        if (p.n_chunks != 1 || p.F * groups_per_fold > 4) return false;
+        if (g.B == 32 || p.n_chunks != 1 || p.F * groups_per_fold > 4) return false;
     }
     p.key_bytes = key_res ? (uint32_t)p.n_chunks * p.stage_cs_bytes : 0;
     p.stage_bytes = (key_res || p.key_regs) ? p.stage_cs_bytes : 2 * p.stage_cs_bytes;
@@ -144,17 +144,28 @@ bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem
     p.smem_bytes = p.off_stage + (uint32_t)p.n_stages * p.stage_bytes + 1024;
     // L2 prefetch of future strips: measured no benefit once the SMEM ring holds >= ~100 KB
     // (tools/sweep.sh); kept as a knob (CSENC_PREFETCH), off by default.
-    p.prefetch_items = 0;
-    // Score (measured on B200, tools/sweep.sh): every item (ring slot) costs a fixed ~1k cycles
-    // of pipeline handoffs, so larger strips win until ~30 KB; >= 3 slots are enough once the
-    // producer is warp-uniform; a resident key beats re-streaming it by ~25%.
-    const double util = (double)tile_blocks / (p.F * 128.0);
-    double s = util * ((key_res || p.key_regs) ? 1.0 : 0.75);
-    if (p.key_regs) s *= 1.02;  // no key LDS per item, no key SMEM
-    s *= std::pow(std::min(1.0, p.stage_cs_bytes / 30720.0), 0.7);
-    if (p.n_stages < 3) s *= 0.9;
-    const double inflight = (double)(p.n_stages - 1) * p.stage_cs_bytes;
-    s *= std::min(1.0, inflight / 61440.0);
+    p.prefetch_items = 0;  // (knob removed from the kernel; kept in the plan info as 0)
+    // Score = modelled pixels per cycle of one SM, calibrated on B200 measurements
+    // (tools/trace_timeline.py, tools/sweep*.sh): an item costs a fixed ~700
+    // cycles of pipeline handoffs plus ~150 per bulk copy, overlapped with the slowest of
+    //   converters ~350 cycles per row group per warpgroup, loads at ~32 B/cycle,
+    //   MMA issue ~48 cycles per tcgen05.mma.
+    const int groups_per_fold = chunk_rows / rows_per_st;
+    const int groups_per_wg = (p.F * groups_per_fold + 1) / 2;
+    const double px = (double)tile_blocks * p.chunk_k;
+    const double item_bytes = (double)p.stage_bytes;
+    const int copies = p.pieces * ((key_res || p.key_regs) ? 1 : 2);
+    const double conv = 350.0 * groups_per_wg;
+    const double load = item_bytes / 32.0;
+    const double mma = (double)(p.chunk_k / 16) * p.F * std::max(48.0, g.Mpad / 2.0);
+    const double cycles = 700.0 + 150.0 * copies + std::max({conv, load, mma});
+    double s = px / cycles;
+    // Measured (tools/sweep10.sh): with >= 3 ring slots the double-buffered SMEM key is ~5% faster
+    // than the register key (whose load sits in the ring at every unit start); the register key
+    // wins when a resident key would leave < 3 slots (C5).
+    // B = 8 rows are 8-byte loads, so dropping the per-item key loads matters more there.
+    if (p.key_regs) s *= (g.B == 8) ? 1.05 : 0.9;
+    if (p.n_stages < 3) s *= 0.85;
     if (p.n_dbuf < 2) s *= 0.8;
     s *= 0.85 + 0.15 * ring_q;
     p.score = s;
@@ -166,7 +177,41 @@ int env_int(const char* name, int dflt) {
     return v ? std::atoi(v) : dflt;
 }
 
+// All feasible plans, best model score first (the autotuner times the first few).
+std::vector<Plan> plan_candidates(const Geometry& g, int smem_limit) {
+    std::vector<Plan> all;
+    // experiment knobs (tools/sweep.sh): force a tile-row count / chunk size / key residency
+    const int f_tr = env_int("CSENC_TILE_ROWS", 0), f_cr = env_int("CSENC_CHUNK_ROWS", 0);
+    const int f_kr = env_int("CSENC_KEY_RESIDENT", -1), f_st = env_int("CSENC_STAGES", 0);
+    for (int T_r = 1; T_r <= g.nby; ++T_r) {
+        if (T_r * g.nbx > 128 * csenc::kMaxFolds) break;
+        if (f_tr && T_r != f_tr) continue;
+        for (int cr = g.B; cr >= 1; --cr) {
+            if (f_cr && cr != f_cr) continue;
+            for (int kr = 2; kr >= 0; --kr) {
+                if (f_kr >= 0 && kr != f_kr) continue;
+                Plan p;
+                if (!try_plan(g, T_r, cr, kr, smem_limit, p)) continue;
+                if (f_st > 0 && f_st < p.n_stages) {
+                    p.smem_bytes -= (uint32_t)(p.n_stages - f_st) * p.stage_bytes;
+                    p.n_stages = f_st;
+                }
+                all.push_back(p);
+            }
+        }
+    }
+    std::stable_sort(all.begin(), all.end(), [](const Plan& a, const Plan& b) { return a.score > b.score; });
+    return all;
+}
+
 bool make_plan(const Geometry& g, int smem_limit, Plan& best) {
+    std::vector<Plan> all = plan_candidates(g, smem_limit);
+    if (all.empty()) return false;
+    best = all[0];
+    return true;
+}
+
+[[maybe_unused]] bool make_plan_scan(const Geometry& g, int smem_limit, Plan& best) {
     best = Plan();
     // experiment knobs (tools/sweep.sh): force a tile-row count / chunk size / key residency
     const int f_tr = env_int("CSENC_TILE_ROWS", 0), f_cr = env_int("CSENC_CHUNK_ROWS", 0);
@@ -288,7 +333,10 @@ struct cs_encoder {
     float* ws_out = nullptr;
     size_t ws_frames_bytes = 0, ws_out_bytes = 0;
     cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
-    int prefetch_override = -1;  // tuning knob (CSENC_PREFETCH env at create), -1 = planner's
+    std::vector<Plan> candidates;  // planner's ranked plans (autotune)
+    int tuned = -1;                // index of the autotuned plan, -1 = model choice
+    void* zeros_dev = nullptr;   // piece_rows * W zero bytes: source for frame rows beyond H
+    size_t zeros_bytes = 0;
     unsigned long long* trace = nullptr;  // device buffer (debug timeline), caller-owned
     int trace_cap = 0;
     std::vector<cudaEvent_t> hev;
@@ -304,6 +352,7 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     KParams kp;
     std::memset(&kp, 0, sizeof(kp));
     kp.frames = frames;
+    kp.zeros = (const uint8_t*)e->zeros_dev;
     kp.out = out;
     kp.W = g.W;
     kp.H = g.H;
@@ -326,12 +375,11 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.piece_rows = pl.piece_rows;
     kp.single_piece = pl.single_piece;
     kp.piece_bytes = pl.piece_bytes;
-    kp.prefetch_items = e->prefetch_override >= 0 ? e->prefetch_override : pl.prefetch_items;
+    kp.set_bytes = (uint32_t)pl.pieces * (uint32_t)pl.piece_rows * (uint32_t)g.W;
     kp.stage_cs_bytes = pl.stage_cs_bytes;
     kp.stage_bytes = pl.stage_bytes;
     kp.key_bytes = pl.key_bytes;
-    kp.key_resident = pl.key_resident;
-    kp.key_regs = pl.key_regs;
+
     kp.n_stages = pl.n_stages;
     kp.off_phi = pl.off_phi;
     kp.off_key = pl.off_key;
@@ -360,25 +408,36 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.trace_cap = e->trace_cap;
     const int grid = std::max(1, std::min(e->sms, kp.n_units));
     cudaError_t err;
-    switch (g.B) {
-        case 8:
-            csenc::cs_measure_kernel<8><<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(kp);
-            break;
-        case 16:
-            csenc::cs_measure_kernel<16><<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(kp);
-            break;
-        default:
-            csenc::cs_measure_kernel<32><<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(kp);
-            break;
+    const int km = pl.key_regs ? csenc::KEY_REGS : (pl.key_resident ? csenc::KEY_RESIDENT : csenc::KEY_STREAMED);
+    auto go = [&](auto kern) { kern<<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(kp); };
+    switch (g.B * 4 + km) {
+        case 8 * 4 + csenc::KEY_STREAMED: go(csenc::cs_measure_kernel<8, csenc::KEY_STREAMED>); break;
+        case 8 * 4 + csenc::KEY_RESIDENT: go(csenc::cs_measure_kernel<8, csenc::KEY_RESIDENT>); break;
+        case 8 * 4 + csenc::KEY_REGS: go(csenc::cs_measure_kernel<8, csenc::KEY_REGS>); break;
+        case 16 * 4 + csenc::KEY_STREAMED: go(csenc::cs_measure_kernel<16, csenc::KEY_STREAMED>); break;
+        case 16 * 4 + csenc::KEY_RESIDENT: go(csenc::cs_measure_kernel<16, csenc::KEY_RESIDENT>); break;
+        case 16 * 4 + csenc::KEY_REGS: go(csenc::cs_measure_kernel<16, csenc::KEY_REGS>); break;
+        case 32 * 4 + csenc::KEY_STREAMED: go(csenc::cs_measure_kernel<32, csenc::KEY_STREAMED>); break;
+        case 32 * 4 + csenc::KEY_RESIDENT: go(csenc::cs_measure_kernel<32, csenc::KEY_RESIDENT>); break;
+        default: return fail(CS_ERR_UNSUPPORTED, "no kernel instantiation for this plan");
     }
     err = cudaGetLastError();
     if (err != cudaSuccess) return cuda_fail(err, "kernel launch");
+    (void)err;
     return CS_OK;
 }
 
-template <int B>
-cudaError_t set_smem_attr(int bytes) {
-    return cudaFuncSetAttribute(csenc::cs_measure_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+cudaError_t set_smem_attr_all(int bytes) {
+    cudaError_t e = cudaSuccess, r;
+#define CSENC_ATTR(B_, K_)                                                                                   \
+    r = cudaFuncSetAttribute(csenc::cs_measure_kernel<B_, K_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             bytes);                                                                          \
+    if (r != cudaSuccess) e = r;
+    CSENC_ATTR(8, csenc::KEY_STREAMED) CSENC_ATTR(8, csenc::KEY_RESIDENT) CSENC_ATTR(8, csenc::KEY_REGS)
+    CSENC_ATTR(16, csenc::KEY_STREAMED) CSENC_ATTR(16, csenc::KEY_RESIDENT) CSENC_ATTR(16, csenc::KEY_REGS)
+    CSENC_ATTR(32, csenc::KEY_STREAMED) CSENC_ATTR(32, csenc::KEY_RESIDENT)
+#undef CSENC_ATTR
+    return e;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -434,18 +493,14 @@ int cs_encoder_create(int W, int H, int gop, int B, int M, const uint16_t* phi_f
     }
     cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, e->device);
     cudaDeviceGetAttribute(&e->smem_limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device);
-    if (const char* pf = std::getenv("CSENC_PREFETCH")) e->prefetch_override = std::atoi(pf);
+    e->candidates = plan_candidates(e->geo, e->smem_limit);
     if (!make_plan(e->geo, e->smem_limit, e->plan)) {
         delete e;
         return fail(CS_ERR_UNSUPPORTED, "no tiling fits shared memory / TMEM for this configuration");
     }
     // The attribute is per kernel (not per encoder): set the device maximum so encoders with
     // different plans can coexist.
-    switch (B) {
-        case 8: err = set_smem_attr<8>(e->smem_limit); break;
-        case 16: err = set_smem_attr<16>(e->smem_limit); break;
-        default: err = set_smem_attr<32>(e->smem_limit); break;
-    }
+    err = set_smem_attr_all(e->smem_limit);
     if (err != cudaSuccess) {
         delete e;
         return cuda_fail(err, "cudaFuncSetAttribute");
@@ -481,6 +536,14 @@ int cs_encoder_create(int W, int H, int gop, int B, int M, const uint16_t* phi_f
         delete e;
         return cuda_fail(err, "cudaMemcpy(Phi)");
     }
+    e->zeros_bytes = (size_t)e->smem_limit;  // >= any plan's strip (strips live in SMEM)
+    if ((err = cudaMalloc(&e->zeros_dev, e->zeros_bytes)) != cudaSuccess ||
+        (err = cudaMemset(e->zeros_dev, 0, e->zeros_bytes)) != cudaSuccess) {
+        cudaFree(e->phi_dev);
+        if (e->zeros_dev) cudaFree(e->zeros_dev);
+        delete e;
+        return fail(CS_ERR_OOM, std::string("zero buffer: ") + cudaGetErrorString(err));
+    }
     *out = e;
     return CS_OK;
 }
@@ -488,6 +551,7 @@ int cs_encoder_create(int W, int H, int gop, int B, int M, const uint16_t* phi_f
 int cs_encoder_destroy(cs_encoder* e) {
     if (!e) return CS_OK;
     if (e->phi_dev) cudaFree(e->phi_dev);
+    if (e->zeros_dev) cudaFree(e->zeros_dev);
     if (e->ws_frames) cudaFree(e->ws_frames);
     if (e->ws_out) cudaFree(e->ws_out);
     for (auto& s : e->hs)
@@ -530,6 +594,62 @@ int cs_encoder_set_trace(cs_encoder* e, unsigned long long* trace_dev, int cap) 
     if (!e || cap < 0 || (cap > 0 && !trace_dev)) return fail(CS_ERR_ARG, "bad trace buffer");
     e->trace = cap > 0 ? trace_dev : nullptr;
     e->trace_cap = cap;
+    return CS_OK;
+}
+
+int cs_encoder_autotune(cs_encoder* e, const uint8_t* frames, int n_seq, int T, float* out, int max_candidates,
+                        int reps, cs_stream_t stream) {
+    if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
+    if (max_candidates < 1 || reps < 1) return fail(CS_ERR_ARG, "max_candidates and reps must be >= 1");
+    if (cs_frames_per_stream(T, e->geo.G) * n_seq == 0) return CS_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaEvent_t e0, e1;
+    cudaError_t err;
+    if ((err = cudaEventCreate(&e0)) != cudaSuccess) return cuda_fail(err, "cudaEventCreate");
+    if ((err = cudaEventCreate(&e1)) != cudaSuccess) {
+        cudaEventDestroy(e0);
+        return cuda_fail(err, "cudaEventCreate");
+    }
+    const Plan keep = e->plan;
+    int best = -1;
+    float best_ms = 1e30f;
+    const int n = std::min<int>(max_candidates, (int)e->candidates.size());
+    int rc = CS_OK;
+    for (int i = 0; i < n && rc == CS_OK; ++i) {
+        e->plan = e->candidates[i];
+        rc = cs_encode_batch(e, frames, n_seq, T, out, stream);  // warm-up
+        if (rc != CS_OK) break;
+        cudaEventRecord(e0, s);
+        for (int r = 0; r < reps && rc == CS_OK; ++r) rc = cs_encode_batch(e, frames, n_seq, T, out, stream);
+        cudaEventRecord(e1, s);
+        if ((err = cudaEventSynchronize(e1)) != cudaSuccess) {
+            rc = cuda_fail(err, "autotune");
+            break;
+        }
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best_ms) {
+            best_ms = ms;
+            best = i;
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (rc != CS_OK || best < 0) {
+        e->plan = keep;
+        return rc;
+    }
+    e->plan = e->candidates[best];
+    e->tuned = best;
+    return CS_OK;
+}
+
+int cs_encoder_num_candidates(const cs_encoder* e) { return e ? (int)e->candidates.size() : -1; }
+
+int cs_encoder_set_candidate(cs_encoder* e, int index) {
+    if (!e || index < 0 || index >= (int)e->candidates.size()) return fail(CS_ERR_ARG, "candidate index out of range");
+    e->plan = e->candidates[index];
+    e->tuned = index;
     return CS_OK;
 }
 

@@ -1,21 +1,20 @@
 // cs_measure_kernel.cuh -- K1: fused GOP residual formation + block CS measurement on sm_100a.
 //
-// One persistent, warp-specialised kernel per encode call (DESIGN.md "K1").  Work unit =
+// One persistent, warp-specialised kernel per encode call (DESIGN.md sec.6).  Work unit =
 // (stream s, GOP g, tile t of full-width block rows, range of CS frames of the GOP).  Item =
 // one K-chunk (chunk_rows pixel rows of every block) of one CS frame of the unit's tile.
 //
 //   warp 12       TMA producer: Phi -> SMEM once (bulk copy).  Per item the tile strip of the
 //                 CS frame -- contiguous in HBM, rows [y0, y0+rows) x all W columns -- arrives
-//                 in ONE cp.async.bulk per piece into a ring slot; the key strip of the unit is
-//                 kept in a double-buffered SMEM region (or streamed with every item when it does
-//                 not fit).  Strips `prefetch_items` ahead are pulled into L2 with
-//                 cp.async.bulk.prefetch.L2, so HBM latency is covered by L2, not by SMEM depth.
+//                 in ONE cp.async.bulk per piece into a ring slot; rows beyond H are filled from
+//                 a zero buffer (partial blocks, reading R10), so every slot holds whole blocks.
+//                 The unit's key strip: KM=2 once per unit through a ring slot into converter
+//                 registers; KM=1 into a double-buffered SMEM region; KM=0 with every item.
 //   warps 0..7    converters (a2 im2col + a3 residual), two warpgroups splitting each item's row
 //                 groups; thread = TMEM lane = block of the tile.  Reads its block's row segments
-//                 of the CS and key strips from SMEM, forms r = F - F_key exactly in fp16 (magic
-//                 number 0x64XX = 1024 + XX), zero for rows >= H / columns >= W (reading R10), and
-//                 writes it with tcgen05.st as the MMA A operand in TMEM (row = block, K = the
-//                 row-major pixel index j = yy*B + xx, two fp16 per 32-bit column).
+//                 of the CS strip (and key) from SMEM, forms r = F - F_key exactly in fp16 (magic
+//                 number 0x64XX = 1024 + XX), and writes it with tcgen05.st as the MMA A operand
+//                 in TMEM (row = block, two fp16 per 32-bit column, K order of ptx::residual4).
 //   warp 13       MMA issuer (a4) + TMEM allocator: D[tmem, fp32] += A[tmem, fp16] x
 //                 Phi^T[smem, fp16], one tcgen05.mma.kind::f16 (M=128 lanes, N=Mpad, K=16) per
 //                 16 pixels; commit -> mbarriers.  Warp-uniform loop, one elected issuing lane.
@@ -23,16 +22,21 @@
 //                 row-contiguous vector stores of y[s][g][c][by][bx][0..M) (block-major).
 //
 // The warp scheduler arbitrates highest-warp-id first, so the single-thread roles (MMA issue,
-// TMA issue) have the highest ids and are never starved by the converter warps.
+// TMA issue) have the highest ids and are never starved by the converter warps.  The kernel is
+// templated on the block size B and the key mode KM so that each instantiation carries only the
+// code its plan runs (instruction-cache footprint matters: 14 warps run 4 different loops).
 //
-// Pipelines (mbarrier phase/parity rings): stage_full/empty (TMA <-> converters), key_full/
-// empty (double-buffered key tile), a_full/empty (converters <-> MMA, 2 TMEM A buffers),
-// d_full/empty (MMA <-> epilogue, 1-2 TMEM accumulators).  Paper passages: Eq.(1) P:83-85,
-// P:87 and Eq.(2)-(3) P:89-91 (see include/cs_encoder.h).
+// Pipelines (mbarrier parity rings): stage_full/empty (TMA <-> converters), key_full/empty
+// (KM=1), a_full/empty (converters <-> MMA, TMEM A buffers), d_full/empty (MMA <-> epilogue,
+// TMEM accumulators).  Paper passages: Eq.(1) P:83-85, P:87 and Eq.(2)-(3) P:89-91.
 #pragma once
 #include <cstdint>
 
 #include "ptx_sm100.cuh"
+
+#ifndef CSENC_DEBUG
+#define CSENC_DEBUG 0  // 1: compile the ablation switches (KParams::dbg_*) into the kernel
+#endif
 
 namespace csenc {
 
@@ -46,8 +50,11 @@ constexpr int kMaxStages = 8;
 constexpr int kMaxTmemBufs = 4;                  // TMEM A buffers / accumulators (ring depth)
 constexpr uint32_t kTmemCols = 512;
 
+enum KeyMode : int { KEY_STREAMED = 0, KEY_RESIDENT = 1, KEY_REGS = 2 };
+
 struct KParams {
     const uint8_t* frames;    // device [n_seq][T][H][W]
+    const uint8_t* zeros;     // device, >= piece_rows * W zero bytes (rows beyond H)
     float* out;
     const uint16_t* phi;      // device, canonical UMMA layout, phi_bytes
     uint32_t phi_bytes;
@@ -60,8 +67,8 @@ struct KParams {
     int piece_rows;           // rows per strip
     int single_piece;
     uint32_t piece_bytes, stage_cs_bytes, stage_bytes, key_bytes;
-    int key_resident, n_stages, prefetch_items;
-    int key_regs;             // 1: the unit's key strip arrives in a ring slot and lives in converter registers
+    uint32_t set_bytes;       // bytes one load_strips() call delivers: pieces * piece_rows * W
+    int n_stages;
     uint32_t off_tab, off_epi, off_phi, off_key, off_stage;
     // work
     int G, T, gop_begin, n_gops_sel, cs_per_stream_sel, n_splits, cs_per_unit, n_units;
@@ -73,8 +80,8 @@ struct KParams {
     // occurrence of the event; nullptr disables (the default)
     unsigned long long* trace;
     int trace_cap;
-    int dbg_load_only;        // debug: converters release stages without converting; no MMA/epilogue
-    int dbg_flags;            // debug ablations: 2 = converters skip SMEM reads/ALU (A = 0), 4 = early slot release
+    int dbg_load_only;        // CSENC_DEBUG only: converters release stages, no MMA/epilogue
+    int dbg_flags;            // CSENC_DEBUG only: 2 = converters write zeros, 8 = no output stores
 };
 
 // trace events
@@ -116,71 +123,21 @@ __device__ __forceinline__ bool decode_unit(const KParams& p, int u, Unit& w) {
     return w.c1 > w.c0;
 }
 
-// Iterator over this CTA's items (unit, CS frame, K-chunk) in schedule order.
-struct ItemIter {
-    int u, c, k;
-    Unit w;
-    bool ok;
-    __device__ __forceinline__ void skip_empty(const KParams& p) {
-        while (u < p.n_units && !decode_unit(p, u, w)) u += gridDim.x;
-        ok = u < p.n_units;
-        if (ok) {
-            c = w.c0;
-            k = 0;
-        }
-    }
-    __device__ __forceinline__ void first(const KParams& p) {
-        u = blockIdx.x;
-        skip_empty(p);
-    }
-    __device__ __forceinline__ void next(const KParams& p) {
-        if (++k < p.n_chunks) return;
-        k = 0;
-        if (++c < w.c1) return;
-        u += gridDim.x;
-        skip_empty(p);
-    }
-};
-
 __device__ __forceinline__ int key_frame(const KParams& p, const Unit& w) { return w.s * p.T + w.g * p.G; }
 
-// First global row and row count of strip `pc` of K-chunk k of tile t (rows >= H are not copied).
-template <int B>
-__device__ __forceinline__ void strip_rows(const KParams& p, int t, int k, int pc, int& y0, int& rows) {
-    y0 = p.single_piece ? t * p.T_r * B : (t * p.T_r + pc) * B + k * p.chunk_rows;
-    rows = max(0, min(p.piece_rows, p.H - y0));
-}
-
-// Bytes a (tile, chunk) strip set delivers (the mbarrier transaction count).
-template <int B>
-__device__ __forceinline__ uint32_t strip_bytes(const KParams& p, int t, int k) {
-    uint32_t b = 0;
-    for (int pc = 0; pc < p.pieces; ++pc) {
-        int y0, rows;
-        strip_rows<B>(p, t, k, pc, y0, rows);
-        b += (uint32_t)rows * (uint32_t)p.W;
-    }
-    return b;
-}
-
+// Copy the strips of K-chunk k of tile t of `frame` into dst ([piece][piece_rows][W]); rows at or
+// beyond H come from the zero buffer.  Always delivers pieces * piece_rows * W bytes, so the
+// mbarrier transaction count of a slot is a constant.
 template <int B>
 __device__ __forceinline__ void load_strips(const KParams& p, uint32_t dst, const uint8_t* frame, int t, int k,
                                             uint32_t bar, uint64_t policy) {
     for (int pc = 0; pc < p.pieces; ++pc) {
-        int y0, rows;
-        strip_rows<B>(p, t, k, pc, y0, rows);
-        if (rows > 0)
-            ptx::bulk_load_hint(dst + (uint32_t)pc * p.piece_bytes, frame + (size_t)y0 * p.W, (uint32_t)rows * p.W,
-                                bar, policy);
-    }
-}
-
-template <int B>
-__device__ __forceinline__ void prefetch_strips(const KParams& p, const uint8_t* frame, int t, int k) {
-    for (int pc = 0; pc < p.pieces; ++pc) {
-        int y0, rows;
-        strip_rows<B>(p, t, k, pc, y0, rows);
-        if (rows > 0) ptx::prefetch_l2(frame + (size_t)y0 * p.W, (uint32_t)rows * p.W);
+        const int y0 = p.single_piece ? t * p.T_r * B : (t * p.T_r + pc) * B + k * p.chunk_rows;
+        const int rows = max(0, min(p.piece_rows, p.H - y0));
+        const uint32_t d = dst + (uint32_t)pc * p.piece_bytes;
+        if (rows > 0) ptx::bulk_load_hint(d, frame + (size_t)y0 * p.W, (uint32_t)rows * p.W, bar, policy);
+        if (rows < p.piece_rows)
+            ptx::bulk_load(d + (uint32_t)rows * p.W, p.zeros, (uint32_t)(p.piece_rows - rows) * p.W, bar);
     }
 }
 
@@ -188,7 +145,6 @@ __device__ __forceinline__ void prefetch_strips(const KParams& p, const uint8_t*
 // is false when the block's right 16 columns lie beyond W (they are then zero in both frames).
 template <int B>
 struct RowConv;
-
 template <>
 struct RowConv<8> {
     static constexpr int kWords = 4;
@@ -298,7 +254,7 @@ __device__ __forceinline__ void issue_chunk(uint32_t d, uint32_t a, uint64_t bde
 // v = this lane's CW values (its row); rows r < rows_valid are stored at dst_row0 + r*M + col.
 template <int CW>
 __device__ __forceinline__ void stage_store(const uint32_t* v, uint32_t tile, uint32_t lane, float* dst_row0, int M,
-                                            int j0, int rows_valid, bool skip = false) {
+                                            int j0, int rows_valid, bool skip) {
     constexpr int CPR = CW / 4;           // 16-byte chunks per row
     constexpr uint32_t PITCH = CW * 4;    // staged row pitch
     constexpr int RPI = 32 / CPR;         // rows per store instruction
@@ -321,12 +277,17 @@ __device__ __forceinline__ void stage_store(const uint32_t* v, uint32_t tile, ui
     __syncwarp();
 }
 
-template <int B>
+template <int B, int KM>
 __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_constant__ KParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t sbase = (ptx::smem_addr(smem_raw) + 1023u) & ~1023u;
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31u;
+#if CSENC_DEBUG
+    const int dbg_load_only = p.dbg_load_only, dbg_flags = p.dbg_flags;
+#else
+    constexpr int dbg_load_only = 0, dbg_flags = 0;
+#endif
 
     // barrier block at sbase: [stage_full x8][stage_empty x8][key_full x2][key_empty x2]
     //                         [a_full x4][a_empty x4][d_full x4][d_empty x4][phi_full][tmem slot]
@@ -406,21 +367,6 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
             ptx::bulk_load(s_phi, p.phi, p.phi_bytes, bar_phi);
         }
         __syncwarp();
-        // optional L2 prefetch `prefetch_items` items ahead of the SMEM loads
-        ItemIter ahead;
-        ahead.first(p);
-        auto prefetch_one = [&]() {
-            if (!ahead.ok) return;
-            const uint8_t* kf = p.frames + (size_t)key_frame(p, ahead.w) * frame_bytes;
-            if (elect_one()) {
-                if (ahead.c == ahead.w.c0 && ahead.k == 0)  // entering a unit: its key strips
-                    for (int k = 0; k < p.n_chunks; ++k) prefetch_strips<B>(p, kf, ahead.w.t, k);
-                prefetch_strips<B>(p, kf + (size_t)(1 + ahead.c) * frame_bytes, ahead.w.t, ahead.k);
-            }
-            __syncwarp();
-            ahead.next(p);
-        };
-        for (int i = 0; i < p.prefetch_items; ++i) prefetch_one();
         int st = 0;
         uint32_t ph = 0;
         int kb = 0;
@@ -430,11 +376,10 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
             Unit w;
             if (!decode_unit(p, u, w)) continue;
             const uint8_t* key_f = p.frames + (size_t)key_frame(p, w) * frame_bytes;
-            if (p.key_regs) {  // the key strip is the unit's first ring item
-                const uint32_t kbytes = strip_bytes<B>(p, w.t, 0);
+            if constexpr (KM == KEY_REGS) {  // the key strip is the unit's first ring item
                 ptx::mbar_wait(bar_stage_empty + 8 * st, ph ^ 1u);
                 if (elect_one()) {
-                    ptx::mbar_arrive_expect_tx(bar_stage_full + 8 * st, kbytes);
+                    ptx::mbar_arrive_expect_tx(bar_stage_full + 8 * st, p.set_bytes);
                     load_strips<B>(p, s_stage + (uint32_t)st * p.stage_bytes, key_f, w.t, 0, bar_stage_full + 8 * st,
                                    pol_key);
                 }
@@ -443,12 +388,10 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                     st = 0;
                     ph ^= 1u;
                 }
-            } else if (p.key_resident) {
+            } else if constexpr (KM == KEY_RESIDENT) {
                 ptx::mbar_wait(bar_key_empty + 8 * kb, kph ^ 1u);
-                uint32_t kbytes = 0;
-                for (int k = 0; k < p.n_chunks; ++k) kbytes += strip_bytes<B>(p, w.t, k);
                 if (elect_one()) {
-                    ptx::mbar_arrive_expect_tx(bar_key_full + 8 * kb, kbytes);
+                    ptx::mbar_arrive_expect_tx(bar_key_full + 8 * kb, (uint32_t)p.n_chunks * p.set_bytes);
                     for (int k = 0; k < p.n_chunks; ++k)
                         load_strips<B>(p, s_key + (uint32_t)kb * p.key_bytes + (uint32_t)k * p.stage_cs_bytes, key_f,
                                        w.t, k, bar_key_full + 8 * kb, pol_key);
@@ -460,15 +403,14 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
             for (int c = w.c0; c < w.c1; ++c) {
                 const uint8_t* cs_f = key_f + (size_t)(1 + c) * frame_bytes;
                 for (int k = 0; k < p.n_chunks; ++k) {
-                    if (p.prefetch_items > 0) prefetch_one();
-                    const uint32_t sb = strip_bytes<B>(p, w.t, k);
                     ptx::mbar_wait(bar_stage_empty + 8 * st, ph ^ 1u);
                     if (lane == 0) trace_ev(p, EV_P_EMPTY, n_items);
                     const uint32_t dst = s_stage + (uint32_t)st * p.stage_bytes;
                     if (elect_one()) {
-                        ptx::mbar_arrive_expect_tx(bar_stage_full + 8 * st, (p.key_resident || p.key_regs) ? sb : 2u * sb);
+                        ptx::mbar_arrive_expect_tx(bar_stage_full + 8 * st,
+                                                   (KM == KEY_STREAMED ? 2u : 1u) * p.set_bytes);
                         load_strips<B>(p, dst, cs_f, w.t, k, bar_stage_full + 8 * st, pol_stream);
-                        if (!p.key_resident && !p.key_regs)
+                        if constexpr (KM == KEY_STREAMED)
                             load_strips<B>(p, dst + p.stage_cs_bytes, key_f, w.t, k, bar_stage_full + 8 * st, pol_key);
                     }
                     __syncwarp();
@@ -481,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                 }
             }
         }
-    } else if (warp == kMmaWarp && !p.dbg_load_only) {
+    } else if (warp == kMmaWarp && !dbg_load_only) {
         // ================================================================ MMA issuer
         // The whole warp walks the schedule (warp-uniform control flow keeps every operand in
         // uniform registers); one elected lane issues the tcgen05 instructions.
@@ -552,28 +494,28 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
         constexpr int kRowsPerSt = 32 / kWords;         // rows per 32-column TMEM store
         const int groups = p.chunk_rows / kRowsPerSt;   // row groups per fold per chunk
         const int n_groups = p.F * groups;
-        const int Bi = B;
         int st = 0, ab = 0, kb = 0;
         uint32_t ph = 0, aph = 0, kph = 0;
         int n_items = 0;
         const bool tr = (warp == 0 && lane == 0);
         const uint32_t tab_lane = sbase + p.off_tab + (uint32_t)lane_idx * 8u;
-        // key_regs mode: this thread's key rows for its (<= 2) row groups, u8 words; the groups'
+        // KEY_REGS: this thread's key rows for its (<= 2) row groups, u8 words; the groups'
         // geometry is constant for the whole kernel
         uint32_t kreg[2][16];
-        uint32_t g_off[2] = {0, 0}, g_meta[2] = {0, 0}, g_acol[2] = {0, 0};
-        int g_r0[2] = {0, 0};
-        if (p.key_regs) {
+        uint32_t g_off[2] = {0, 0}, g_acol[2] = {0, 0};
+        bool g_half2[2] = {true, true};
+        if constexpr (KM == KEY_REGS) {
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const int g = wg + 2 * j;
                 if (g < n_groups) {
                     const int f = g / groups, r0 = (g - f * groups) * kRowsPerSt;
+                    uint32_t meta;
                     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
-                                 : "=r"(g_off[j]), "=r"(g_meta[j])
+                                 : "=r"(g_off[j]), "=r"(meta)
                                  : "r"(tab_lane + (uint32_t)(f * 1024)));
                     g_off[j] += (uint32_t)(r0 * p.W);
-                    g_r0[j] = r0 + (int)(g_meta[j] & 0xFFFFu);
+                    g_half2[j] = (meta >> 16) & 1u;
                     g_acol[j] = (uint32_t)(f * (p.chunk_k / 2) + r0 * kWords);
                 }
             }
@@ -581,9 +523,8 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             Unit w;
             if (!decode_unit(p, u, w)) continue;
-            if (p.key_resident) ptx::mbar_wait(bar_key_full + 8 * kb, kph);
-            const int tile_y0 = w.t * p.T_r * Bi;
-            if (p.key_regs) {
+            if constexpr (KM == KEY_RESIDENT) ptx::mbar_wait(bar_key_full + 8 * kb, kph);
+            if constexpr (KM == KEY_REGS) {
                 ptx::mbar_wait(bar_stage_full + 8 * st, ph);
                 const uint32_t kbase = s_stage + (uint32_t)st * p.stage_bytes;
 #pragma unroll
@@ -605,7 +546,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                 for (int k = 0; k < p.n_chunks; ++k) {
                     ptx::mbar_wait(bar_stage_full + 8 * st, ph);
                     if (tr) trace_ev(p, EV_C_FULL, n_items);
-                    if (p.dbg_load_only) {
+                    if (dbg_load_only) {
                         __syncwarp();
                         if (lane == 0) ptx::mbar_arrive(bar_stage_empty + 8 * st);
                         if (++st == p.n_stages) {
@@ -619,87 +560,58 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                     ptx::tc_fence_after();
                     if (tr) trace_ev(p, EV_C_AEMPTY, n_items);
                     const uint32_t cs_base = s_stage + (uint32_t)st * p.stage_bytes;
-                    const uint32_t key_base = p.key_resident
-                                                  ? s_key + (uint32_t)kb * p.key_bytes + (uint32_t)k * p.stage_cs_bytes
-                                                  : cs_base + p.stage_cs_bytes;
                     const uint32_t a_tm = tmem_base + lane_bits + a_col0 + (uint32_t)ab * (uint32_t)p.a_cols;
-                    const int chunk_y = tile_y0 + k * p.chunk_rows;  // global row of chunk row 0 (block row 0)
-                    if (p.dbg_flags & 2) {
+                    if (dbg_flags & 2) {
                         uint32_t v[32];
 #pragma unroll
                         for (int i = 0; i < 32; ++i) v[i] = 0u;
-#pragma unroll
-                        for (int j = 0; j < 2; ++j)
-                            if (wg + 2 * j < n_groups) ptx::tmem_st_32x32b_x32(a_tm + g_acol[j], v);
-                    } else if (p.key_regs) {
+                        for (int g = wg; g < n_groups; g += 2)
+                            ptx::tmem_st_32x32b_x32(a_tm + (uint32_t)((g / groups) * (p.chunk_k / 2) +
+                                                                       (g % groups) * kRowsPerSt * kWords),
+                                                    v);
+                    } else if constexpr (KM == KEY_REGS) {
                         // <= 2 row groups per warpgroup (planner guarantee); key words in kreg[j]
 #pragma unroll
                         for (int j = 0; j < 2; ++j) {
                             if (wg + 2 * j < n_groups) {
-                                const bool half2 = (g_meta[j] >> 16) & 1u;
-                                const int rows_in = p.H - (chunk_y + g_r0[j]);
                                 uint32_t v[32];
-                                if (rows_in >= kRowsPerSt) {
 #pragma unroll
-                                    for (int rr = 0; rr < kRowsPerSt; ++rr)
-                                        RowConvK<B>::run(cs_base + g_off[j] + (uint32_t)(rr * p.W),
-                                                         &kreg[j][rr * (B / 4)], v + rr * kWords, half2);
-                                } else {
-#pragma unroll
-                                    for (int rr = 0; rr < kRowsPerSt; ++rr) {
-                                        if (rr < rows_in) {
-                                            RowConvK<B>::run(cs_base + g_off[j] + (uint32_t)(rr * p.W),
-                                                             &kreg[j][rr * (B / 4)], v + rr * kWords, half2);
-                                        } else {
-#pragma unroll
-                                            for (int i = 0; i < kWords; ++i) v[rr * kWords + i] = 0u;
-                                        }
-                                    }
-                                }
+                                for (int rr = 0; rr < kRowsPerSt; ++rr)
+                                    RowConvK<B>::run(cs_base + g_off[j] + (uint32_t)(rr * p.W), &kreg[j][rr * (B / 4)],
+                                                     v + rr * kWords, g_half2[j]);
                                 ptx::tmem_st_32x32b_x32(a_tm + g_acol[j], v);
                             }
                         }
-                    }
-                    // row groups g = f*groups + gi, round-robin over the two warpgroups
-                    int f = 0, gi = p.key_regs ? n_groups : wg;
-                    while (gi >= groups && f < p.F) {
-                        gi -= groups;
-                        ++f;
-                    }
-                    for (int g = p.key_regs ? n_groups : wg; g < n_groups; g += 2) {
-                        const int r0 = gi * kRowsPerSt;
-                        uint32_t off, meta;
-                        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
-                                     : "=r"(off), "=r"(meta)
-                                     : "r"(tab_lane + (uint32_t)(f * 1024)));
-                        off += (uint32_t)(r0 * p.W);
-                        const bool half2 = (meta >> 16) & 1u;
-                        // rows of this group that lie inside the frame (the rest are zero)
-                        const int rows_in = p.H - (chunk_y + (int)(meta & 0xFFFFu) + r0);
-                        uint32_t v[32];
-                        if (rows_in >= kRowsPerSt) {
+                    } else {
+                        const uint32_t key_base = (KM == KEY_RESIDENT)
+                                                      ? s_key + (uint32_t)kb * p.key_bytes + (uint32_t)k * p.stage_cs_bytes
+                                                      : cs_base + p.stage_cs_bytes;
+                        // row groups g = f*groups + gi, round-robin over the two warpgroups
+                        int f = 0, gi = wg;
+                        while (gi >= groups && f < p.F) {
+                            gi -= groups;
+                            ++f;
+                        }
+                        for (int g = wg; g < n_groups; g += 2) {
+                            const int r0 = gi * kRowsPerSt;
+                            uint32_t off, meta;
+                            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                                         : "=r"(off), "=r"(meta)
+                                         : "r"(tab_lane + (uint32_t)(f * 1024)));
+                            off += (uint32_t)(r0 * p.W);
+                            const bool half2 = (meta >> 16) & 1u;
+                            uint32_t v[32];
 #pragma unroll
                             for (int rr = 0; rr < kRowsPerSt; ++rr) {
                                 const uint32_t ro = off + (uint32_t)(rr * p.W);
                                 RowConv<B>::run(cs_base + ro, key_base + ro, v + rr * kWords, half2);
                             }
-                        } else {
-#pragma unroll
-                            for (int rr = 0; rr < kRowsPerSt; ++rr) {
-                                if (rr < rows_in) {
-                                    const uint32_t ro = off + (uint32_t)(rr * p.W);
-                                    RowConv<B>::run(cs_base + ro, key_base + ro, v + rr * kWords, half2);
-                                } else {
-#pragma unroll
-                                    for (int i = 0; i < kWords; ++i) v[rr * kWords + i] = 0u;
-                                }
+                            ptx::tmem_st_32x32b_x32(a_tm + (uint32_t)(f * (p.chunk_k / 2) + r0 * kWords), v);
+                            gi += 2;
+                            while (gi >= groups) {
+                                gi -= groups;
+                                ++f;
                             }
-                        }
-                        ptx::tmem_st_32x32b_x32(a_tm + (uint32_t)(f * (p.chunk_k / 2) + r0 * kWords), v);
-                        gi += 2;
-                        while (gi >= groups) {
-                            gi -= groups;
-                            ++f;
                         }
                     }
                     if (tr) trace_ev(p, EV_C_CONV, n_items);
@@ -722,14 +634,14 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                     }
                 }
             }
-            if (p.key_resident) {
+            if constexpr (KM == KEY_RESIDENT) {
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(bar_key_empty + 8 * kb);
                 kb ^= 1;
                 if (kb == 0) kph ^= 1u;
             }
         }
-    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4 && !p.dbg_load_only) {
+    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4 && !dbg_load_only) {
         // ================================================================ epilogue (a6)
         // Output rows (blocks) are M*4 bytes apart.  For M == 4 a thread's row is one 16-byte
         // vector and the warp's 32 rows are contiguous: store straight from registers.  For other
@@ -741,6 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
         const uint32_t lane_bits = (uint32_t)(ew * 32) << 16;
         const uint32_t stage_tile = sbase + p.off_epi + (uint32_t)ew * 4096u;
         const int mode = (p.M == 4) ? 0 : ((p.M & 3) == 0 ? 1 : 2);
+        const bool skip = (dbg_flags & 8) != 0;
         int db = 0;
         uint32_t dph = 0;
         int n_items = 0;
@@ -768,7 +681,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                         uint32_t v[16];
                         ptx::tmem_ld_32x32b_x16(d_tm + (uint32_t)(f * p.Mpad), v);
                         ptx::tc_wait_ld();
-                        if (valid) ptx::stg128(out_cs + (long long)b * 4, v[0], v[1], v[2], v[3]);
+                        if (valid && !skip) ptx::stg128(out_cs + (long long)b * 4, v[0], v[1], v[2], v[3]);
                         continue;
                     }
                     for (int j0 = 0; j0 < p.Mpad; j0 += 32) {
@@ -791,7 +704,6 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                             continue;
                         }
                         float* dst_row0 = out_cs + (long long)row0 * p.M;
-                        const bool skip = (p.dbg_flags & 8) != 0;
                         if (cw == 32)
                             stage_store<32>(v, stage_tile, lane, dst_row0, p.M, j0, rows_valid, skip);
                         else

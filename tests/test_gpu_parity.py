@@ -277,3 +277,34 @@ def test_encoders_with_different_plans_coexist():
         torch.cuda.synchronize()
         phi = synth.phi_from_seed(synth.phi_seed(), M, 256)
         assert_parity(out.cpu().numpy(), frames, phi, cfg.G, cfg.B)
+
+
+def test_all_candidate_plans_bitwise_identical():
+    """Every feasible plan (tile rows, folds, K-chunk, key mode, ring depths) computes the same
+    per-block MMA chain, so outputs are bit-identical -- the autotuner can pick any of them."""
+    for name, M in (("C4", 64), ("C5", 4), ("C3", 64)):
+        base = synth.CONFIGS[name]
+        cfg = base.with_(T=min(base.T, 9 if name != "C3" else 17), S=1)
+        frames = synth.gen_video(cfg)
+        fd = torch.from_numpy(frames).cuda()
+        phi = synth.phi_from_seed(synth.phi_seed(), M, cfg.B ** 2)
+        enc = P.Encoder(cfg.W, cfg.H, cfg.G, cfg.B, M, phi)
+        n = min(enc.num_candidates(), 8)
+        assert n >= 2
+        ref = None
+        seen = set()
+        for i in range(n):
+            plan = enc.set_candidate(i)
+            seen.add((plan["tile_block_rows"], plan["chunk_rows"], plan["key_resident"]))
+            out = enc.encode_batch(fd)
+            torch.cuda.synchronize()
+            if ref is None:
+                ref = out.clone()
+                assert_parity(out.cpu().numpy(), frames, phi, cfg.G, cfg.B)
+            else:
+                assert torch.equal(out, ref), (name, plan)
+        assert len(seen) >= 2
+        chosen = enc.autotune(fd, max_candidates=3, reps=1)
+        out = enc.encode_batch(fd)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref) and chosen["smem_bytes"] > 0
