@@ -107,6 +107,7 @@ int cs_encoder_autotune(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, i
  * (tests / tools).  Host only; not safe concurrently with encodes of `enc`. */
 int cs_encoder_num_candidates(const cs_encoder* enc);
 int cs_encoder_set_candidate(cs_encoder* enc, int index);
+int cs_encoder_candidate_index(const cs_encoder* enc);  /* plan in use (0 = model's best) */
 
 /* Fill *info with the tiling plan.  Host only. */
 int cs_encoder_plan(const cs_encoder* enc, cs_plan_info* info);

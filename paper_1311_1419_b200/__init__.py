@@ -59,6 +59,7 @@ def lib() -> ctypes.CDLL:
             "cs_encoder_autotune": (c_int, [vp, vp, c_int, c_int, vp, c_int, c_int, vp]),
             "cs_encoder_num_candidates": (c_int, [vp]),
             "cs_encoder_set_candidate": (c_int, [vp, c_int]),
+            "cs_encoder_candidate_index": (c_int, [vp]),
             "cs_encode_gop": (c_int, [vp, vp, c_int, vp, vp]),
             "cs_encode_batch": (c_int, [vp, vp, c_int, c_int, vp, vp]),
             "cs_encode_batch_gops": (c_int, [vp, vp, c_int, c_int, c_int, c_int, vp, vp]),
@@ -210,6 +211,9 @@ class Encoder:
 
     def num_candidates(self) -> int:
         return lib().cs_encoder_num_candidates(self._h)
+
+    def tuned_index(self) -> int:
+        return lib().cs_encoder_candidate_index(self._h)
 
     def set_candidate(self, index: int) -> dict:
         _check(lib().cs_encoder_set_candidate(self._h, index))

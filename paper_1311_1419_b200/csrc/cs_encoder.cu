@@ -646,6 +646,8 @@ int cs_encoder_autotune(cs_encoder* e, const uint8_t* frames, int n_seq, int T, 
 
 int cs_encoder_num_candidates(const cs_encoder* e) { return e ? (int)e->candidates.size() : -1; }
 
+int cs_encoder_candidate_index(const cs_encoder* e) { return e ? (e->tuned < 0 ? 0 : e->tuned) : -1; }
+
 int cs_encoder_set_candidate(cs_encoder* e, int index) {
     if (!e || index < 0 || index >= (int)e->candidates.size()) return fail(CS_ERR_ARG, "candidate index out of range");
     e->plan = e->candidates[index];
