@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -376,6 +377,9 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.single_piece = pl.single_piece;
     kp.piece_bytes = pl.piece_bytes;
     kp.set_bytes = (uint32_t)pl.pieces * (uint32_t)pl.piece_rows * (uint32_t)g.W;
+    kp.smem_bytes = pl.smem_bytes - 1024;
+    kp.out_floats = (long long)n_seq * cs_frames_in_gops(T, g.G, g0, g1) * g.nblk * g.M;
+    kp.frames_bytes = (long long)n_seq * T * g.W * g.H;
     kp.stage_cs_bytes = pl.stage_cs_bytes;
     kp.stage_bytes = pl.stage_bytes;
     kp.key_bytes = pl.key_bytes;

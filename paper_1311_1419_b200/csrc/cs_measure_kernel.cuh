@@ -37,6 +37,21 @@
 #ifndef CSENC_DEBUG
 #define CSENC_DEBUG 0  // 1: compile the ablation switches (KParams::dbg_*) into the kernel
 #endif
+#ifndef CSENC_CHECKS
+#define CSENC_CHECKS 0  // 1: device-side bounds checks (SMEM, TMEM, global output); trap on violation
+#endif
+#if CSENC_CHECKS
+#define CS_CHECK(cond)                                                                            \
+    do {                                                                                          \
+        if (!(cond)) {                                                                            \
+            printf("CSENC_CHECK failed: %s (block %d thread %d, line %d)\n", #cond, blockIdx.x,    \
+                   threadIdx.x, __LINE__);                                                        \
+            __trap();                                                                             \
+        }                                                                                         \
+    } while (0)
+#else
+#define CS_CHECK(cond) ((void)0)
+#endif
 
 namespace csenc {
 
@@ -82,6 +97,10 @@ struct KParams {
     int trace_cap;
     int dbg_load_only;        // CSENC_DEBUG only: converters release stages, no MMA/epilogue
     int dbg_flags;            // CSENC_DEBUG only: 2 = converters write zeros, 8 = no output stores
+    // CSENC_CHECKS only: bounds
+    uint32_t smem_bytes;      // dynamic SMEM size (from the aligned base)
+    long long out_floats;     // output buffer size in floats
+    long long frames_bytes;   // input buffer size in bytes
 };
 
 // trace events
@@ -135,6 +154,8 @@ __device__ __forceinline__ void load_strips(const KParams& p, uint32_t dst, cons
         const int y0 = p.single_piece ? t * p.T_r * B : (t * p.T_r + pc) * B + k * p.chunk_rows;
         const int rows = max(0, min(p.piece_rows, p.H - y0));
         const uint32_t d = dst + (uint32_t)pc * p.piece_bytes;
+        CS_CHECK(rows == 0 || (long long)(frame - p.frames) + (long long)y0 * p.W + (long long)rows * p.W <= p.frames_bytes);
+        CS_CHECK(rows >= p.piece_rows || (uint32_t)(p.piece_rows - rows) * p.W <= p.smem_bytes);
         if (rows > 0) ptx::bulk_load_hint(d, frame + (size_t)y0 * p.W, (uint32_t)rows * p.W, bar, policy);
         if (rows < p.piece_rows)
             ptx::bulk_load(d + (uint32_t)rows * p.W, p.zeros, (uint32_t)(p.piece_rows - rows) * p.W, bar);
@@ -304,6 +325,10 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
     const uint32_t s_phi = sbase + p.off_phi;
     const uint32_t s_key = sbase + p.off_key;
     const uint32_t s_stage = sbase + p.off_stage;
+    CS_CHECK(p.off_stage + (uint32_t)p.n_stages * p.stage_bytes <= p.smem_bytes);
+    CS_CHECK(p.set_bytes * (KM == KEY_STREAMED ? 2u : 1u) <= p.stage_bytes);
+    CS_CHECK(KM != KEY_RESIDENT || p.off_key + 2u * p.key_bytes <= p.off_stage);
+    CS_CHECK(p.n_abuf * p.a_cols + p.n_dbuf * p.d_cols <= (int)kTmemCols);
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < p.n_stages; ++i) {
@@ -574,6 +599,8 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
 #pragma unroll
                         for (int j = 0; j < 2; ++j) {
                             if (wg + 2 * j < n_groups) {
+                                CS_CHECK(g_off[j] + (uint32_t)((kRowsPerSt - 1) * p.W + B) <= p.set_bytes);
+                                CS_CHECK(g_acol[j] + 32u <= (uint32_t)p.a_cols);
                                 uint32_t v[32];
 #pragma unroll
                                 for (int rr = 0; rr < kRowsPerSt; ++rr)
@@ -600,6 +627,8 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                                          : "r"(tab_lane + (uint32_t)(f * 1024)));
                             off += (uint32_t)(r0 * p.W);
                             const bool half2 = (meta >> 16) & 1u;
+                            CS_CHECK(off + (uint32_t)((kRowsPerSt - 1) * p.W + B) <= p.set_bytes + 128u);
+                            CS_CHECK((uint32_t)(f * (p.chunk_k / 2) + r0 * kWords + 32) <= (uint32_t)p.a_cols);
                             uint32_t v[32];
 #pragma unroll
                             for (int rr = 0; rr < kRowsPerSt; ++rr) {
@@ -672,6 +701,8 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                                             (long long)(w.g - p.gop_begin) * (p.G - 1) + c;
                 float* const out_cs = p.out + (cs_global * p.nblk + blk0) * (long long)p.M;
                 const uint32_t d_tm = tmem_base + lane_bits + d_col0 + (uint32_t)db * (uint32_t)p.d_cols;
+                CS_CHECK(d_col0 + (uint32_t)(db + 1) * (uint32_t)p.d_cols <= kTmemCols);
+                CS_CHECK((cs_global + 1) * p.nblk * (long long)p.M <= p.out_floats);
                 for (int f = 0; f < p.F; ++f) {
                     const int row0 = f * p.L + ew * 32;            // tile block of this warp's lane 0
                     const int b = row0 + (int)lane;
