@@ -36,7 +36,7 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = [
-    "gop_partition", "cs_frame_count", "block_grid", "frame_blocks", "residual", "measure",
+    "quantize", "dequantize", "quantize_frames", "measure_entries", "gop_partition", "cs_frame_count", "block_grid", "frame_blocks", "residual", "measure",
     "tolerance_scale", "encode", "encode_stream", "phi_values", "compression_ratio", "total_cr",
     "check_tolerance",
 ]
@@ -164,6 +164,49 @@ def measure_entries(frames: np.ndarray, phi_bits: np.ndarray, G: int, B: int, cs
         ys.append(measure(r, phi)[0])
         Ss.append(tolerance_scale(r, phi)[0])
     return np.asarray(ys), np.asarray(Ss)
+
+
+# -- f1: 16-bit measurement quantisation ---------------------------------------------------------
+def quantize(y, bits: int = 16):
+    """SPEC.md:154-162 quantize: scale = max|y_i| / 32767 (scale = 1 if y is all zero),
+    codes = round(y_i / scale), dequantize = codes * scale.  The container stores the scale as f32
+    (SPEC.md:410), so scale is rounded to fp32; round = round half to even (SPEC leaves the tie rule
+    open -- DESIGN.md reading R17).  The rounding decision is taken in fp32 arithmetic on the
+    fp32-rounded y, the precision the kernel decides in (R18).
+    Returns (int16 codes, float32 scale)."""
+    if bits != 16:
+        raise ValueError("16-bit quantisation only")
+    y = np.asarray(y, dtype=np.float64)
+    if not np.all(np.isfinite(y)):
+        raise ValueError("non-finite measurement")
+    qmax = (1 << (bits - 1)) - 1
+    amax = float(np.max(np.abs(y))) if y.size else 0.0
+    scale = np.float32(amax / qmax) if amax > 0 else np.float32(1.0)
+    q = np.rint(y.astype(np.float32) / scale)  # fp32 IEEE division, round half to even
+    codes = np.clip(q, -qmax, qmax).astype(np.int16)
+    return codes, scale
+
+
+def dequantize(codes, scale):
+    return np.asarray(codes, dtype=np.float64) * float(scale)
+
+
+def quantize_frames(y, group_blocks=None):
+    """Quantise every CS frame of y [n_cs][nblk][M]: one scale per frame (SPEC), or -- with
+    group_blocks = list of (b0, b1) block ranges -- one scale per (frame, range) (per-tile
+    variant).  Returns (codes int16 like y, scales float32 [n_cs] or [n_cs][n_groups])."""
+    y = np.asarray(y, dtype=np.float64)
+    codes = np.empty(y.shape, dtype=np.int16)
+    if group_blocks is None:
+        scales = np.empty(y.shape[0], dtype=np.float32)
+        for i in range(y.shape[0]):
+            codes[i], scales[i] = quantize(y[i])
+    else:
+        scales = np.empty((y.shape[0], len(group_blocks)), dtype=np.float32)
+        for i in range(y.shape[0]):
+            for gi, (b0, b1) in enumerate(group_blocks):
+                codes[i, b0:b1], scales[i, gi] = quantize(y[i, b0:b1])
+    return codes, scales
 
 
 # -- a7 ------------------------------------------------------------------------------------------

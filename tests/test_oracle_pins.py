@@ -291,3 +291,49 @@ def test_check_tolerance_semantics():
     assert not ok
     ok, _ = oracle.check_tolerance(np.array([1.0 + 2e-5, 0.0, -2.0]), y, S)
     assert not ok
+
+
+# ---------------------------------------------------------------- f1: 16-bit quantisation
+def test_quantize_zero_vector():
+    """y = 0 -> codes all zero, scale 1, round-trip exact."""
+    codes, scale = oracle.quantize(np.zeros(37))
+    assert scale == np.float32(1.0) and np.all(codes == 0)
+    assert np.all(oracle.dequantize(codes, scale) == 0)
+
+
+def test_quantize_bounds_and_extremes():
+    """max|y| = 32767*s -> round-trip error <= s/2; the max element maps to
+    +-32767; antisymmetry; exhaustive check on random vectors."""
+    rng = np.random.default_rng(21)
+    for trial in range(200):
+        y = rng.normal(size=rng.integers(1, 400)) * 10.0 ** rng.uniform(-6, 6)
+        codes, scale = oracle.quantize(y)
+        err = np.abs(oracle.dequantize(codes, scale) - y)
+        # s/2 (SPEC.md:161) plus the fp32 decision (R18): rounding y and the scale to fp32 each
+        # moves code*s by at most 32767 * 2^-24 * s
+        assert np.all(err <= scale * (0.5 + 2 * 32767 * 2.0 ** -24)), (trial, err.max() / scale)
+        if trial < 50:  # in exact arithmetic (fp64 decision) the SPEC bound holds as printed
+            q = np.clip(np.rint(y / float(scale)), -32767, 32767)
+            assert np.all(np.abs(q * float(scale) - y) <= float(scale) * 0.5 * (1 + 1e-12))
+        k = np.argmax(np.abs(y))
+        assert abs(int(codes[k])) == 32767
+        assert np.all(np.abs(codes.astype(int)) <= 32767)
+        c2, s2 = oracle.quantize(-y)
+        assert s2 == scale and np.array_equal(c2, -codes)
+    s = np.float32(0.25)
+    y = np.array([32767 * 0.25, -0.125, 0.375, 1.0])      # ties: -0.5 -> -0 (even), 1.5 -> 2 (even)
+    codes, scale = oracle.quantize(y)
+    assert scale == s and codes.tolist() == [32767, 0, 2, 4]
+
+
+def test_quantize_frames_per_group():
+    rng = np.random.default_rng(22)
+    y = rng.normal(size=(3, 10, 4))
+    c, s = oracle.quantize_frames(y)
+    assert s.shape == (3,) and c.shape == y.shape
+    for i in range(3):
+        ci, si = oracle.quantize(y[i])
+        assert si == s[i] and np.array_equal(ci, c[i])
+    c2, s2 = oracle.quantize_frames(y, [(0, 4), (4, 10)])
+    assert s2.shape == (3, 2)
+    assert np.array_equal(c2[1, 4:], oracle.quantize(y[1, 4:])[0])
