@@ -144,6 +144,32 @@ int cs_encode_batch(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, int T
 int cs_encode_batch_gops(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, int T, int gop_begin,
                          int gop_end, float* meas_dev, cs_stream_t stream);
 
+/* ---- 16-bit measurement quantisation ---------------------------- */
+
+/* SPEC.md:154-162 quantize: scale = max|y_i| / 32767 (1 if all y_i == 0), codes = round(y_i /
+ * scale) (IEEE fp32 division, round half to even, clamped to +-32767); dequantize = codes *
+ * scale.  Container payload per CS frame: f32 scale + M*nblk int16 codes.
+ *   CS_Q16_FRAME: one scale per CS frame, exactly as SPEC states.  The frame maximum is a
+ *     grid-wide dependency, so this runs the measurement twice: an absmax pass (no stores, one
+ *     atomicMax per warp and frame) and a codes pass, plus a tiny finalize kernel
+ *     (memset + 3 launches on `stream`).
+ *   CS_Q16_ROW: one scale per (CS frame, block row of B pixel rows): a single fused pass (the
+ *     maximum is reduced on chip).  A documented deviation (R19), available when the
+ *     plan's tile has <= 40 block rows (CS_ERR_UNSUPPORTED otherwise). */
+#define CS_Q16_FRAME 0
+#define CS_Q16_ROW 1
+
+/* Number of fp32 scales cs_encode_batch_q16 writes: n_cs (FRAME) or n_cs * nby (ROW), where
+ * n_cs = n_seq * CS frames per stream; -1 on bad arguments. */
+int64_t cs_q16_scale_count(const cs_encoder* enc, int n_seq, int T, int granularity);
+
+/* frames_dev as cs_encode_batch; codes_dev = DEVICE int16 [n_cs][nby][nbx][M] (the measurement
+ * layout), 16-byte aligned; scales_dev = DEVICE fp32, cs_q16_scale_count entries, 4-byte
+ * aligned, [n_cs] or [n_cs][nby].  Asynchronous on `stream`; no allocation.  Errors: CS_ERR_ARG
+ * (NULL / misaligned / bad granularity), CS_ERR_UNSUPPORTED (see CS_Q16_ROW), CS_ERR_CUDA. */
+int cs_encode_batch_q16(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, int T, int granularity,
+                        int16_t* codes_dev, float* scales_dev, cs_stream_t stream);
+
 /* ---- encode (HOST buffers; synchronous) ------------------------------------------------- */
 
 /* End-to-end call: frames_host = HOST [n_seq][T][H][W] uint8, meas_host = HOST fp32 output

@@ -64,6 +64,8 @@ def lib() -> ctypes.CDLL:
             "cs_encode_batch": (c_int, [vp, vp, c_int, c_int, vp, vp]),
             "cs_encode_batch_gops": (c_int, [vp, vp, c_int, c_int, c_int, c_int, vp, vp]),
             "cs_encode_batch_host": (c_int, [vp, vp, c_int, c_int, vp]),
+            "cs_encode_batch_q16": (c_int, [vp, vp, c_int, c_int, c_int, vp, vp, vp]),
+            "cs_q16_scale_count": (c_i64, [vp, c_int, c_int, c_int]),
             "cs_measurement_count": (c_i64, [vp, c_int, c_int]),
             "cs_compression_ratio": (c_dbl, [vp, c_int, c_dbl, c_int]),
             "cs_compression_ratio_cfg": (c_dbl, [c_int, c_int, c_int, c_int, c_int, c_int, c_dbl, c_int]),
@@ -233,6 +235,33 @@ class Encoder:
             out = torch.empty((max(n - 1, 0), self.nblk, self.M), dtype=torch.float32, device=frames.device)
         _check(lib().cs_encode_gop(self._h, _ptr(frames), n, _ptr(out), _stream_handle(stream)))
         return out
+
+    # -- 16-bit quantisation (f1)
+    Q16_FRAME, Q16_ROW = 0, 1
+
+    def q16_scale_shape(self, n_seq: int, T: int, granularity: int = 0):
+        n_cs = self.out_shape(n_seq, T)[0]
+        return (n_cs,) if granularity == self.Q16_FRAME else (n_cs, self.nby)
+
+    def encode_batch_q16(self, frames, granularity: int = 0, codes=None, scales=None, stream=None):
+        """frames: CUDA uint8 [n_seq][T][H][W]; returns (codes int16 [n_cs][nblk][M], scales fp32
+        [n_cs] (Q16_FRAME, SPEC's per-frame scale) or [n_cs][nby] (Q16_ROW, per block row))."""
+        import torch
+        assert frames.is_cuda and frames.dtype == torch.uint8 and frames.is_contiguous()
+        n_seq, T, H, W = frames.shape
+        assert (H, W) == (self.H, self.W)
+        if codes is None:
+            codes = torch.empty(self.out_shape(n_seq, T), dtype=torch.int16, device=frames.device)
+        if scales is None:
+            scales = torch.empty(self.q16_scale_shape(n_seq, T, granularity), dtype=torch.float32,
+                                 device=frames.device)
+        assert codes.is_cuda and codes.dtype == torch.int16 and codes.is_contiguous()
+        assert scales.is_cuda and scales.dtype == torch.float32 and scales.is_contiguous()
+        assert codes.numel() >= self.measurement_count(n_seq, T)
+        assert scales.numel() >= lib().cs_q16_scale_count(self._h, n_seq, T, granularity)
+        _check(lib().cs_encode_batch_q16(self._h, _ptr(frames), n_seq, T, granularity, _ptr(codes), _ptr(scales),
+                                         _stream_handle(stream)))
+        return codes, scales
 
     # -- encode (host buffers)
     def encode_batch_host(self, frames, out=None):

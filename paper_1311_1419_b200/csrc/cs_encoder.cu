@@ -345,7 +345,16 @@ struct cs_encoder {
 
 namespace {
 
-int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g1, float* out, cudaStream_t stream) {
+// f1 epilogue arguments (qmode 0 = fp32 output)
+struct QArgs {
+    int qmode = 0;
+    int16_t* codes = nullptr;
+    uint32_t* amax = nullptr;
+    float* scales = nullptr;
+};
+
+int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g1, float* out, cudaStream_t stream,
+           const QArgs& q = QArgs()) {
     const Geometry& g = e->geo;
     const Plan& pl = e->plan;
     if (g1 <= g0 || g.G == 1) return CS_OK;
@@ -410,21 +419,25 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.dbg_flags = env_int("CSENC_DBG_FLAGS", 0);
     kp.trace = e->trace;
     kp.trace_cap = e->trace_cap;
+    kp.qmode = q.qmode;
+    kp.codes = q.codes;
+    kp.amax = q.amax;
+    kp.scales = q.scales;
     const int grid = std::max(1, std::min(e->sms, kp.n_units));
     cudaError_t err;
     const int km = pl.key_regs ? csenc::KEY_REGS : (pl.key_resident ? csenc::KEY_RESIDENT : csenc::KEY_STREAMED);
     auto go = [&](auto kern) { kern<<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(kp); };
-    switch (g.B * 4 + km) {
-        case 8 * 4 + csenc::KEY_STREAMED: go(csenc::cs_measure_kernel<8, csenc::KEY_STREAMED>); break;
-        case 8 * 4 + csenc::KEY_RESIDENT: go(csenc::cs_measure_kernel<8, csenc::KEY_RESIDENT>); break;
-        case 8 * 4 + csenc::KEY_REGS: go(csenc::cs_measure_kernel<8, csenc::KEY_REGS>); break;
-        case 16 * 4 + csenc::KEY_STREAMED: go(csenc::cs_measure_kernel<16, csenc::KEY_STREAMED>); break;
-        case 16 * 4 + csenc::KEY_RESIDENT: go(csenc::cs_measure_kernel<16, csenc::KEY_RESIDENT>); break;
-        case 16 * 4 + csenc::KEY_REGS: go(csenc::cs_measure_kernel<16, csenc::KEY_REGS>); break;
-        case 32 * 4 + csenc::KEY_STREAMED: go(csenc::cs_measure_kernel<32, csenc::KEY_STREAMED>); break;
-        case 32 * 4 + csenc::KEY_RESIDENT: go(csenc::cs_measure_kernel<32, csenc::KEY_RESIDENT>); break;
+    const int epi = q.qmode ? csenc::EPI_Q16 : csenc::EPI_F32;
+#define CSENC_CASE(B_, K_)                                                                              \
+    case (B_ * 4 + K_) * 2 + csenc::EPI_F32: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_F32>); break; \
+    case (B_ * 4 + K_) * 2 + csenc::EPI_Q16: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16>); break;
+    switch ((g.B * 4 + km) * 2 + epi) {
+        CSENC_CASE(8, csenc::KEY_STREAMED) CSENC_CASE(8, csenc::KEY_RESIDENT) CSENC_CASE(8, csenc::KEY_REGS)
+        CSENC_CASE(16, csenc::KEY_STREAMED) CSENC_CASE(16, csenc::KEY_RESIDENT) CSENC_CASE(16, csenc::KEY_REGS)
+        CSENC_CASE(32, csenc::KEY_STREAMED) CSENC_CASE(32, csenc::KEY_RESIDENT)
         default: return fail(CS_ERR_UNSUPPORTED, "no kernel instantiation for this plan");
     }
+#undef CSENC_CASE
     err = cudaGetLastError();
     if (err != cudaSuccess) return cuda_fail(err, "kernel launch");
     (void)err;
@@ -433,9 +446,12 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
 
 cudaError_t set_smem_attr_all(int bytes) {
     cudaError_t e = cudaSuccess, r;
-#define CSENC_ATTR(B_, K_)                                                                                   \
-    r = cudaFuncSetAttribute(csenc::cs_measure_kernel<B_, K_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                             bytes);                                                                          \
+#define CSENC_ATTR(B_, K_)                                                                               \
+    r = cudaFuncSetAttribute(csenc::cs_measure_kernel<B_, K_, csenc::EPI_F32>,                           \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);                         \
+    if (r != cudaSuccess) e = r;                                                                          \
+    r = cudaFuncSetAttribute(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16>,                           \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);                         \
     if (r != cudaSuccess) e = r;
     CSENC_ATTR(8, csenc::KEY_STREAMED) CSENC_ATTR(8, csenc::KEY_RESIDENT) CSENC_ATTR(8, csenc::KEY_REGS)
     CSENC_ATTR(16, csenc::KEY_STREAMED) CSENC_ATTR(16, csenc::KEY_RESIDENT) CSENC_ATTR(16, csenc::KEY_REGS)
@@ -445,6 +461,12 @@ cudaError_t set_smem_attr_all(int bytes) {
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// f1, per-frame scale: amax bits (pass 1) -> fp32 scales in place, after pass 2 has read them.
+__global__ void q16_finalize_kernel(uint32_t* amax, long long n) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) amax[i] = __float_as_uint(csenc::q16_scale(amax[i]));
+}
 
 }  // namespace
 
@@ -698,6 +720,52 @@ int cs_encode_gop(cs_encoder* e, const uint8_t* frames, int n_frames, float* out
     if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
     if (n_frames < 1 || n_frames > e->geo.G) return fail(CS_ERR_ARG, "n_frames must be in [1, gop]");
     return cs_encode_batch_gops(e, frames, 1, n_frames, 0, 1, out, stream);
+}
+
+int64_t cs_q16_scale_count(const cs_encoder* e, int n_seq, int T, int granularity) {
+    if (!e || n_seq < 0 || T < 0) return -1;
+    const long long n_cs = (long long)n_seq * cs_frames_per_stream(T, e->geo.G);
+    if (granularity == CS_Q16_FRAME) return n_cs;
+    if (granularity == CS_Q16_ROW) return n_cs * e->geo.nby;
+    return -1;
+}
+
+int cs_encode_batch_q16(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int granularity, int16_t* codes,
+                        float* scales, cs_stream_t stream) {
+    if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
+    if (n_seq < 0 || T < 0) return fail(CS_ERR_ARG, "n_seq and T must be >= 0");
+    if (granularity != CS_Q16_FRAME && granularity != CS_Q16_ROW) return fail(CS_ERR_ARG, "bad granularity");
+    const Geometry& g = e->geo;
+    const long long n_cs = (long long)n_seq * cs_frames_per_stream(T, g.G);
+    if (n_cs == 0) return CS_OK;
+    if (!frames || !codes || !scales) return fail(CS_ERR_ARG, "NULL buffer");
+    if (!aligned16(frames) || !aligned16(codes) || (reinterpret_cast<uintptr_t>(scales) & 3u))
+        return fail(CS_ERR_ARG, "frames/codes must be 16-byte aligned, scales 4-byte aligned");
+    if ((long long)n_seq * T > 0x7FFFFFFFLL) return fail(CS_ERR_UNSUPPORTED, "too many frames");
+    const int n_gops = cdiv(T, g.G);
+    const cudaStream_t st = (cudaStream_t)stream;
+    QArgs q;
+    q.codes = codes;
+    if (granularity == CS_Q16_ROW) {
+        if (e->plan.T_r > csenc::kRowSlots)
+            return fail(CS_ERR_UNSUPPORTED, "row-scale quantisation needs a plan with <= 40 block rows per tile");
+        q.qmode = csenc::Q_ROW;
+        q.scales = scales;
+        return launch(e, frames, n_seq, T, 0, n_gops, nullptr, st, q);
+    }
+    // per-frame scale: zero the |y| maxima, absmax pass, codes pass, finalize
+    q.amax = reinterpret_cast<uint32_t*>(scales);
+    cudaError_t err = cudaMemsetAsync(scales, 0, (size_t)n_cs * sizeof(float), st);
+    if (err != cudaSuccess) return cuda_fail(err, "cudaMemsetAsync");
+    q.qmode = csenc::Q_ABSMAX;
+    int rc = launch(e, frames, n_seq, T, 0, n_gops, nullptr, st, q);
+    if (rc != CS_OK) return rc;
+    q.qmode = csenc::Q_FRAME;
+    rc = launch(e, frames, n_seq, T, 0, n_gops, nullptr, st, q);
+    if (rc != CS_OK) return rc;
+    q16_finalize_kernel<<<(unsigned)((n_cs + 255) / 256), 256, 0, st>>>(q.amax, n_cs);
+    err = cudaGetLastError();
+    return err == cudaSuccess ? CS_OK : cuda_fail(err, "finalize launch");
 }
 
 int cs_encode_batch_host(cs_encoder* e, const uint8_t* frames_host, int n_seq, int T, float* out_host) {

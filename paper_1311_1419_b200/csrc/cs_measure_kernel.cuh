@@ -66,6 +66,18 @@ constexpr int kMaxTmemBufs = 4;                  // TMEM A buffers / accumulator
 constexpr uint32_t kTmemCols = 512;
 
 enum KeyMode : int { KEY_STREAMED = 0, KEY_RESIDENT = 1, KEY_REGS = 2 };
+// epilogue variants (template EPI): fp32 measurements (a6), or 16-bit codes (f1)
+enum Epilogue : int { EPI_F32 = 0, EPI_Q16 = 1 };
+// EPI_Q16 sub-modes (KParams::qmode)
+enum QMode : int {
+    Q_ABSMAX = 1,     // pass 1 of the per-frame scale: atomicMax of |y| bits into amax[cs], no stores
+    Q_FRAME = 2,      // pass 2: codes with scale = amax[cs] / 32767 (1 if 0)
+    Q_ROW = 3,        // single pass: one scale per (CS frame, block row), reduced in SMEM
+};
+constexpr int kRowSlots = 40;                    // Q_ROW: max block rows per tile (3 x 40 u32 slots)
+constexpr uint32_t kRowSlotOff = 512;            // Q_ROW slots live in the barrier page (bytes 512..991)
+static_assert(16 * kMaxStages + 32 + 32 * kMaxTmemBufs + 16 <= (int)kRowSlotOff, "barrier block overlaps row slots");
+static_assert(kRowSlotOff + 3 * kRowSlots * 4 <= 1024, "row slots overflow the barrier page");
 
 struct KParams {
     const uint8_t* frames;    // device [n_seq][T][H][W]
@@ -101,6 +113,11 @@ struct KParams {
     uint32_t smem_bytes;      // dynamic SMEM size (from the aligned base)
     long long out_floats;     // output buffer size in floats
     long long frames_bytes;   // input buffer size in bytes
+    // EPI_Q16 (f1)
+    int qmode;                // QMode
+    int16_t* codes;           // [n_cs][nblk][M] int16, same layout as out
+    uint32_t* amax;           // Q_ABSMAX / Q_FRAME: [n_cs] fp32 |y| max bits (zeroed before pass 1)
+    float* scales;            // Q_ROW: [n_cs][nby] fp32 scales
 };
 
 // trace events
@@ -298,7 +315,47 @@ __device__ __forceinline__ void stage_store(const uint32_t* v, uint32_t tile, ui
     __syncwarp();
 }
 
-template <int B, int KM>
+// f1 epilogue helper: a warp's 32 rows x (4*CPR) 32-bit words of packed int16 codes -> global through
+// the same 4 KB swizzled SMEM tile (CPR 16-byte chunks per row, CPR = 2 or 4).  dst_row0 points at
+// row 0's word col0w; rows are row_words apart; chunk cc is stored if col0w + 4*cc < valid_words.
+template <int CPR>
+__device__ __forceinline__ void stage_store_codes(const uint32_t* w, uint32_t tile, uint32_t lane, uint32_t* dst_row0,
+                                                  int row_words, int col0w, int valid_words, int rows_valid) {
+    constexpr uint32_t PITCH = CPR * 16;
+    constexpr int RPI = 32 / CPR;
+#pragma unroll
+    for (int q = 0; q < CPR; ++q) {
+        const int slot = (CPR == 4) ? (q ^ (int)((lane >> 1) & 3u)) : (q ^ (int)((lane >> 2) & 1u));
+        ptx::sts128(tile + lane * PITCH + (uint32_t)slot * 16u, w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+    }
+    __syncwarp();
+    const int cc = (int)(lane % CPR);
+    const int rsub = (int)(lane / CPR);
+    const bool col_ok = col0w + 4 * cc < valid_words;
+#pragma unroll
+    for (int it = 0; it < CPR; ++it) {
+        const int r = it * RPI + rsub;
+        const int slot = (CPR == 4) ? (cc ^ ((r >> 1) & 3)) : (cc ^ ((r >> 2) & 1));
+        uint4 t = ptx::lds128(tile + (uint32_t)r * PITCH + (uint32_t)slot * 16u);
+        if (r < rows_valid && col_ok) ptx::stg128(dst_row0 + (long long)r * row_words + 4 * cc, t.x, t.y, t.z, t.w);
+    }
+    __syncwarp();
+}
+
+// y -> 16-bit code: round(y / scale) (IEEE fp32 division, round half to even),
+// clamped to +-32767 (only reachable through fp32 rounding of the scale).
+__device__ __forceinline__ int q16_code(uint32_t ybits, float scale) {
+    const int c = __float2int_rn(__fdiv_rn(__uint_as_float(ybits), scale));
+    return max(-32767, min(32767, c));
+}
+__device__ __forceinline__ uint32_t q16_pack(uint32_t y0, uint32_t y1, float scale) {
+    return ((uint32_t)q16_code(y0, scale) & 0xFFFFu) | ((uint32_t)q16_code(y1, scale) << 16);
+}
+__device__ __forceinline__ float q16_scale(uint32_t amax_bits) {
+    return amax_bits == 0 ? 1.0f : __fdiv_rn(__uint_as_float(amax_bits), 32767.0f);
+}
+
+template <int B, int KM, int EPI>
 __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_constant__ KParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t sbase = (ptx::smem_addr(smem_raw) + 1023u) & ~1023u;
@@ -371,6 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
             asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(e), "r"(off), "r"(meta));
         }
     }
+    if (EPI == EPI_Q16 && threadIdx.x < 3 * kRowSlots) ptx::sts32(sbase + kRowSlotOff + threadIdx.x * 4u, 0u);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -670,7 +728,148 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                 if (kb == 0) kph ^= 1u;
             }
         }
-    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4 && !dbg_load_only) {
+    } else if (EPI == EPI_Q16 && warp >= kEpiWarp0 && warp < kEpiWarp0 + 4 && !dbg_load_only) {
+        // ================================================================ epilogue, 16-bit codes (f1)
+        // Per item: (Q_ABSMAX) warp max of |y| -> one atomicMax per warp into amax[cs];
+        // (Q_FRAME) codes with the frame's scale; (Q_ROW) pass A: per-block-row max reduced across
+        // the 4 epilogue warps in SMEM slots (triple-buffered, one named barrier per item), pass B:
+        // re-read the accumulators from TMEM and store codes with the row's scale.
+        const int ew = warp - kEpiWarp0;
+        const int lane_idx = ew * 32 + (int)lane;
+        const uint32_t lane_bits = (uint32_t)(ew * 32) << 16;
+        const uint32_t stage_tile = sbase + p.off_epi + (uint32_t)ew * 4096u;
+        const int qmode = p.qmode;
+        const int smode = (p.M == 4) ? 0 : ((p.M & 7) == 0 ? 1 : 2);   // store mode
+        int db = 0;
+        uint32_t dph = 0;
+        int n_items = 0;
+        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+            Unit w;
+            if (!decode_unit(p, u, w)) continue;
+            const int rows_here = min(p.T_r, p.nby - w.t * p.T_r);
+            const int blocks_here = rows_here * p.nbx;
+            const int blk0 = w.t * p.T_r * p.nbx;
+            for (int c = w.c0; c < w.c1; ++c) {
+                ptx::mbar_wait(bar_d_full + 8 * db, dph);
+                ptx::tc_fence_after();
+                const long long cs_global = (long long)w.s * p.cs_per_stream_sel +
+                                            (long long)(w.g - p.gop_begin) * (p.G - 1) + c;
+                const uint32_t d_tm = tmem_base + lane_bits + d_col0 + (uint32_t)db * (uint32_t)p.d_cols;
+                CS_CHECK((cs_global + 1) * p.nblk * (long long)p.M <= p.out_floats);
+                if (qmode == Q_ABSMAX || qmode == Q_ROW) {
+                    const uint32_t slots = sbase + kRowSlotOff + (uint32_t)(n_items % 3) * (kRowSlots * 4);
+                    if (qmode == Q_ROW && lane_idx < kRowSlots)   // next item's slots: last read 2 items ago
+                        ptx::sts32(sbase + kRowSlotOff + (uint32_t)((n_items + 1) % 3) * (kRowSlots * 4) +
+                                       (uint32_t)lane_idx * 4u, 0u);
+                    uint32_t mx = 0;
+                    for (int f = 0; f < p.F; ++f) {
+                        const int b = f * p.L + lane_idx;
+                        const bool valid = lane_idx < p.L && b < blocks_here;
+                        uint32_t mf = 0;
+                        for (int j0 = 0; j0 < p.Mpad; j0 += 32) {
+                            uint32_t v[32];
+                            if (p.Mpad - j0 >= 32) {
+                                ptx::tmem_ld_32x32b_x32(d_tm + (uint32_t)(f * p.Mpad + j0), v);
+                            } else {
+                                ptx::tmem_ld_32x32b_x16(d_tm + (uint32_t)(f * p.Mpad + j0),
+                                                        *reinterpret_cast<uint32_t(*)[16]>(v));
+#pragma unroll
+                                for (int q = 16; q < 32; ++q) v[q] = 0;
+                            }
+                            ptx::tc_wait_ld();
+#pragma unroll
+                            for (int q = 0; q < 32; ++q) mf = max(mf, v[q] & 0x7FFFFFFFu);
+                        }
+                        if (!valid) mf = 0;
+                        if (qmode == Q_ABSMAX) {
+                            mx = max(mx, mf);
+                        } else {
+                            // segmented warp max over the (few) block rows this warp's 32 blocks touch
+                            const int r = valid ? b / p.nbx : 0x7FFFFFFF;
+                            const int rlo = (int)__reduce_min_sync(0xFFFFFFFFu, (unsigned)r);
+                            const int rhi = (int)__reduce_max_sync(0xFFFFFFFFu, valid ? (unsigned)r : 0u);
+                            for (int rr = rlo; rr <= rhi; ++rr) {
+                                const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, r == rr ? mf : 0u);
+                                if (lane == 0 && m != 0) ptx::atom_smem_max(slots + (uint32_t)rr * 4u, m);
+                            }
+                        }
+                    }
+                    if (qmode == Q_ABSMAX) {
+                        mx = __reduce_max_sync(0xFFFFFFFFu, mx);
+                        if (lane == 0 && mx != 0) atomicMax(p.amax + cs_global, mx);
+                    } else {
+                        ptx::named_bar(1, 128);
+                    }
+                }
+                if (qmode == Q_FRAME || qmode == Q_ROW) {
+                    const uint32_t slots = sbase + kRowSlotOff + (uint32_t)(n_items % 3) * (kRowSlots * 4);
+                    float frame_scale = 1.0f;
+                    if (qmode == Q_FRAME) {
+                        frame_scale = q16_scale(__ldcg(p.amax + cs_global));
+                    } else if (lane_idx < rows_here) {
+                        p.scales[cs_global * p.nby + w.t * p.T_r + lane_idx] =
+                            q16_scale(ptx::lds32(slots + (uint32_t)lane_idx * 4u));
+                    }
+                    int16_t* const codes_cs = p.codes + (cs_global * p.nblk + blk0) * (long long)p.M;
+                    for (int f = 0; f < p.F; ++f) {
+                        const int row0 = f * p.L + ew * 32;
+                        const int b = row0 + (int)lane;
+                        const bool valid = lane_idx < p.L && b < blocks_here;
+                        const int rows_valid = min(32, min(p.L - ew * 32, blocks_here - row0));
+                        const float scale =
+                            qmode == Q_FRAME ? frame_scale
+                                             : q16_scale(valid ? ptx::lds32(slots + (uint32_t)(b / p.nbx) * 4u) : 0u);
+                        if (smode == 0) {
+                            uint32_t v[16];
+                            ptx::tmem_ld_32x32b_x16(d_tm + (uint32_t)(f * p.Mpad), v);
+                            ptx::tc_wait_ld();
+                            if (valid) ptx::stg64(codes_cs + (long long)b * 4, q16_pack(v[0], v[1], scale),
+                                                  q16_pack(v[2], v[3], scale));
+                            continue;
+                        }
+                        for (int j0 = 0; j0 < p.Mpad; j0 += 32) {
+                            const int cw = min(32, p.Mpad - j0);
+                            uint32_t v[32];
+                            if (cw == 32) {
+                                ptx::tmem_ld_32x32b_x32(d_tm + (uint32_t)(f * p.Mpad + j0), v);
+                            } else {
+                                ptx::tmem_ld_32x32b_x16(d_tm + (uint32_t)(f * p.Mpad + j0),
+                                                        *reinterpret_cast<uint32_t(*)[16]>(v));
+                            }
+                            ptx::tc_wait_ld();
+                            if (smode == 2) {
+                                if (valid) {
+                                    int16_t* dst = codes_cs + (long long)b * p.M + j0;
+#pragma unroll
+                                    for (int q = 0; q < 32; ++q)
+                                        if (q < cw && j0 + q < p.M) dst[q] = (int16_t)q16_code(v[q], scale);
+                                }
+                                continue;
+                            }
+                            uint32_t wd[16];
+#pragma unroll
+                            for (int q = 0; q < 16; ++q) wd[q] = q16_pack(v[2 * q], v[2 * q + 1], scale);
+                            uint32_t* dst_row0 = reinterpret_cast<uint32_t*>(codes_cs + (long long)row0 * p.M + j0);
+                            if (cw == 32)
+                                stage_store_codes<4>(wd, stage_tile, lane, dst_row0, p.M / 2, j0 / 2, p.M / 2,
+                                                     rows_valid);
+                            else
+                                stage_store_codes<2>(wd, stage_tile, lane, dst_row0, p.M / 2, j0 / 2, p.M / 2,
+                                                     rows_valid);
+                        }
+                    }
+                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(bar_d_empty + 8 * db);
+                ++n_items;
+                if (++db == p.n_dbuf) {
+                    db = 0;
+                    dph ^= 1u;
+                }
+            }
+        }
+    } else if (EPI == EPI_F32 && warp >= kEpiWarp0 && warp < kEpiWarp0 + 4 && !dbg_load_only) {
         // ================================================================ epilogue (a6)
         // Output rows (blocks) are M*4 bytes apart.  For M == 4 a thread's row is one 16-byte
         // vector and the warp's 32 rows are contiguous: store straight from registers.  For other
