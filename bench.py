@@ -36,12 +36,19 @@ import synth  # noqa: E402
 L2_BYTES = 126 * 1024 * 1024
 
 
-def alg_bytes(cfg, M, n_seq):
-    """Algorithmic HBM bytes of one launch: every frame read once + every fp32 measurement
-    written once."""
-    nblk = -(-cfg.W // cfg.B) * -(-cfg.H // cfg.B)
+OUTPUTS = {"f32": None, "q16frame": 0, "q16row": 1}   # --output -> cs_encode_batch_q16 granularity
+
+
+def alg_bytes(cfg, M, n_seq, output="f32"):
+    """Algorithmic HBM bytes of one step for one M: every frame read once + every measurement
+    written once: fp32 (4 B), or int16 codes (2 B) + fp32 scales
+    (one per CS frame, or per CS frame and block row) for the f1 outputs."""
+    nbx, nby = -(-cfg.W // cfg.B), -(-cfg.H // cfg.B)
     n_cs = cfg.T - -(-cfg.T // cfg.G)
-    return n_seq * (cfg.T * cfg.W * cfg.H + n_cs * nblk * M * 4)
+    if output == "f32":
+        return n_seq * (cfg.T * cfg.W * cfg.H + n_cs * nbx * nby * M * 4)
+    n_scales = n_cs * (nby if output == "q16row" else 1)
+    return n_seq * (cfg.T * cfg.W * cfg.H + n_cs * nbx * nby * M * 2 + 4 * n_scales)
 
 
 def cs_pixels(cfg, n_seq):
@@ -146,12 +153,19 @@ def run_ours(args, cfg, Ms):
     # rank r encodes its own independent streams (weak scaling)
     frames_h = synth.gen_video(cfg, streams=range(rank * n_seq, (rank + 1) * n_seq))
     frames = torch.from_numpy(frames_h).to(dev)
-    encs, outs = [], []
+    encs, outs, qouts = [], [], []
+    gran = OUTPUTS[args.output]
     for M in Ms:
         phi = synth.phi_from_seed(synth.phi_seed(), M, cfg.B ** 2)
         e = P.Encoder(cfg.W, cfg.H, cfg.G, cfg.B, M, phi)
         encs.append(e)
         outs.append(torch.empty(e.out_shape(n_seq, cfg.T), dtype=torch.float32, device=dev))
+        if gran is not None:
+            qouts.append((torch.empty(e.out_shape(n_seq, cfg.T), dtype=torch.int16, device=dev),
+                          torch.empty(e.q16_scale_shape(n_seq, cfg.T, gran), dtype=torch.float32, device=dev)))
+    if gran is not None:
+        outs = [None] * len(Ms)   # the q16 step does not touch the fp32 buffers; free them
+        torch.cuda.empty_cache()
     stream = torch.cuda.current_stream(dev)
     # plan choice: the fastest of the planner's top plans (outputs are bit-identical across plans);
     # --tune-file reuses earlier choices (e.g. under ncu, so no tuning launches are profiled)
@@ -165,6 +179,7 @@ def run_ours(args, cfg, Ms):
             e.set_candidate(int(tuned[key]))
         elif not args.no_autotune:
             e.autotune(frames, outs[i], max_candidates=args.tune_candidates, reps=2, stream=stream)
+            # (q16 outputs: the plan is tuned on the fp32 epilogue; the load side dominates both)
             tuned[key] = e.tuned_index()
     if args.tune_file and rank == 0:
         with open(args.tune_file, "w") as f:
@@ -174,7 +189,10 @@ def run_ours(args, cfg, Ms):
         for i, e in enumerate(encs):
             if ev is not None:
                 ev[i][0].record(stream)
-            e.encode_batch(frames, outs[i], stream)
+            if gran is None:
+                e.encode_batch(frames, outs[i], stream)
+            else:
+                e.encode_batch_q16(frames, gran, qouts[i][0], qouts[i][1], stream)
             if ev is not None:
                 ev[i][1].record(stream)
 
@@ -206,7 +224,10 @@ def run_ours(args, cfg, Ms):
 
     # ---- end to end through the public host-buffer C-ABI call (copies inside the timed region)
     e2e = None
-    if not args.no_e2e:
+    if gran is not None:
+        e2e = {"value": None, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+               "how": "not measured: the host-buffer C-ABI call (cs_encode_batch_host) returns fp32 only"}
+    elif not args.no_e2e:
         pin_in = torch.from_numpy(frames_h).pin_memory()
         pin_out = [torch.empty(o.shape, dtype=torch.float32).pin_memory() for o in outs]
         for i, e in enumerate(encs):  # warm-up (workspace allocation)
@@ -241,7 +262,7 @@ def run_ours(args, cfg, Ms):
     for i, M in enumerate(Ms):
         med = statistics.median(launch_ms[i])
         avg = sum(launch_ms[i]) / K
-        b = alg_bytes(cfg, M, n_seq)
+        b = alg_bytes(cfg, M, n_seq, args.output)
         per_m[str(M)] = {"ms_median": med, "ms_mean": avg,
                          "gpix_s": cs_pixels(cfg, n_seq) / (avg * 1e-3) / 1e9,
                          "alg_gbs": b / (avg * 1e-3) / 1e9, "frac_of_peak": b / (avg * 1e-3) / 1e9 / peak,
@@ -259,20 +280,22 @@ def run_ours(args, cfg, Ms):
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u8 in, fp16 x fp16 -> fp32 (tensor core kind::f16)", "data": "synthetic (seeded surveillance-like video, synth/)",
         "config": {"workload": args.workload, "W": cfg.W, "H": cfg.H, "T": cfg.T, "streams_per_gpu": n_seq,
-                   "G": cfg.G, "B": cfg.B, "M": list(Ms),
+                   "G": cfg.G, "B": cfg.B, "M": list(Ms), "output": args.output,
                    "l2": f"inputs larger than L2 ({in_mb:.0f} MiB read per launch vs 126 MiB L2); no flush",
                    "parallelism": f"dp{world} (independent sequences per GPU, no collective)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "cs_measure_kernel (all launches of the step; alg bytes = frames read once + fp32 "
-                               "measurements written once)"},
+                     "kernel": "cs_measure_kernel (all launches of the step; alg bytes = frames read once + "
+                               + ("fp32 measurements written once)" if gran is None else
+                                  "int16 codes + fp32 scales written once; q16frame runs two passes, so it reads "
+                                  "the frames twice against this one-read algorithmic count)")},
         "per_M": per_m,
-        "gpu_launches": K * len(Ms),
+        "gpu_launches": K * len(Ms) * (3 if args.output == "q16frame" else 1),
         "clocks": clk.summary(),
         "e2e": e2e,
     }
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg, Ms, budget_s=args.cpu_budget)
+        line["cpu_baseline"] = cpu_baseline(cfg, Ms, budget_s=args.cpu_budget, output=args.output)
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
@@ -291,30 +314,35 @@ def cpu_threads():
     return os.cpu_count() or 1
 
 
-def oracle_sample(cfg, Ms, n_gops=1, seed_stream=0):
-    """Encode the first n_gops GOPs of one stream with the oracle for every M; returns
-    (seconds, CS pixels)."""
+def oracle_sample(cfg, Ms, n_gops=1, seed_stream=0, output="f32"):
+    """Encode the first n_gops GOPs of one stream with the oracle for every M (and quantise, for
+    the f1 outputs); returns (seconds, CS pixels)."""
     import oracle
     T = min(cfg.T, n_gops * cfg.G)
     frames = synth.gen_stream(cfg, seed_stream, T=T)
     phis = [synth.phi_from_seed(synth.phi_seed(), M, cfg.B ** 2) for M in Ms]
     t0 = time.perf_counter()
+    nbx = -(-cfg.W // cfg.B)
     for phi in phis:
-        oracle.encode_stream(frames, phi, cfg.G, cfg.B, with_scale=False)
+        y, _ = oracle.encode_stream(frames, phi, cfg.G, cfg.B, with_scale=False)
+        if output == "q16frame":
+            oracle.quantize_frames(y)
+        elif output == "q16row":
+            oracle.quantize_frames(y, [(b, min(b + nbx, y.shape[1])) for b in range(0, y.shape[1], nbx)])
     dt = time.perf_counter() - t0
     px = len(Ms) * (T - -(-T // cfg.G)) * cfg.W * cfg.H
     return dt, px
 
 
-def cpu_baseline(cfg, Ms, budget_s=15.0):
+def cpu_baseline(cfg, Ms, budget_s=15.0, output="f32"):
     n_gops, dt, px = 1, 0.0, 0
     while True:
-        dt, px = oracle_sample(cfg, Ms, n_gops)
+        dt, px = oracle_sample(cfg, Ms, n_gops, output=output)
         if dt * 2 > budget_s or n_gops * cfg.G >= cfg.T:
             break
         n_gops = min(-(-cfg.T // cfg.G), max(n_gops + 1, int(n_gops * budget_s / max(dt, 1e-3) / 2)))
     return {"value": px / dt / 1e9, "unit": "Gpixel/s", "cores": cpu_threads(), "kind": "oracle",
-            "sample": f"fp64 numpy oracle (y only), first {n_gops} GOP(s) = {px // (cfg.W * cfg.H) // len(Ms)} CS "
+            "sample": f"fp64 numpy oracle ({'y only' if output == 'f32' else 'y + ' + output}), first {n_gops} GOP(s) = {px // (cfg.W * cfg.H) // len(Ms)} CS "
                       f"frames of one {cfg.W}x{cfg.H} stream x M in {list(Ms)}, {dt:.2f} s"}
 
 
@@ -323,10 +351,10 @@ def run_reference(args, cfg, Ms):
     if rank != 0:
         return None
     if args.warmup > 0:  # one untimed pass (page-in, BLAS thread start-up)
-        oracle_sample(cfg, Ms, 1)
+        oracle_sample(cfg, Ms, 1, output=args.output)
     times, pxs = [], []
     for _ in range(args.steps):
-        dt, px = oracle_sample(cfg, Ms, 1)
+        dt, px = oracle_sample(cfg, Ms, 1, output=args.output)
         times.append(dt)
         pxs.append(px)
     ms = 1e3 * sum(times) / len(times)
@@ -339,7 +367,7 @@ def run_reference(args, cfg, Ms):
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded surveillance-like video, synth/)",
         "config": {"workload": args.workload, "W": cfg.W, "H": cfg.H, "T": cfg.T, "G": cfg.G, "B": cfg.B,
-                   "M": list(Ms), "sample_per_step": "first GOP of one stream, every M"},
+                   "M": list(Ms), "output": args.output, "sample_per_step": "first GOP of one stream, every M"},
         "cpu_baseline": {"value": value, "unit": "Gpixel/s", "cores": cores, "kind": "oracle",
                          "sample": "fp64 numpy oracle (y only) on the first GOP of one stream for every M, per step"},
         "e2e": {"value": value, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -363,6 +391,8 @@ def main(argv=None):
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-autotune", action="store_true")
     ap.add_argument("--tune-candidates", type=int, default=6)
+    ap.add_argument("--output", choices=list(OUTPUTS), default="f32",
+                    help="f32 measurements (headline) or 16-bit codes (f1): per-frame or per-row scales")
     ap.add_argument("--tune-file", default=None, help="json of chosen plan indices (read if present, else written)")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":

@@ -171,9 +171,10 @@ def quantize(y, bits: int = 16):
     """SPEC.md:154-162 quantize: scale = max|y_i| / 32767 (scale = 1 if y is all zero),
     codes = round(y_i / scale), dequantize = codes * scale.  The container stores the scale as f32
     (SPEC.md:410), so scale is rounded to fp32; round = round half to even (SPEC leaves the tie rule
-    open -- DESIGN.md reading R17).  The rounding decision is taken in fp32 arithmetic on the
-    fp32-rounded y, the precision the kernel decides in (R18).
-    Returns (int16 codes, float32 scale)."""
+    open -- DESIGN.md reading R17).  The rounding decision is taken in the kernel's precision
+    (R18): y rounded to fp32, divided by the scale as a multiplication with the fp32
+    reciprocal inv = fl32(1 / scale), the exact product rounded half-to-even (an fp32 x fp32 product
+    is exact in fp64, so np.rint of it is that rounding).  Returns (int16 codes, float32 scale)."""
     if bits != 16:
         raise ValueError("16-bit quantisation only")
     y = np.asarray(y, dtype=np.float64)
@@ -182,7 +183,8 @@ def quantize(y, bits: int = 16):
     qmax = (1 << (bits - 1)) - 1
     amax = float(np.max(np.abs(y))) if y.size else 0.0
     scale = np.float32(amax / qmax) if amax > 0 else np.float32(1.0)
-    q = np.rint(y.astype(np.float32) / scale)  # fp32 IEEE division, round half to even
+    inv = np.float32(1.0) / scale                       # fp32 IEEE division
+    q = np.rint(y.astype(np.float32).astype(np.float64) * float(inv))
     codes = np.clip(q, -qmax, qmax).astype(np.int16)
     return codes, scale
 

@@ -342,18 +342,21 @@ __device__ __forceinline__ void stage_store_codes(const uint32_t* w, uint32_t ti
     __syncwarp();
 }
 
-// y -> 16-bit code: round(y / scale) (IEEE fp32 division, round half to even),
-// clamped to +-32767 (only reachable through fp32 rounding of the scale).
-__device__ __forceinline__ int q16_code(uint32_t ybits, float scale) {
-    const int c = __float2int_rn(__fdiv_rn(__uint_as_float(ybits), scale));
-    return max(-32767, min(32767, c));
+// y -> 16-bit code, SPEC.md:154-162 round(y / scale), evaluated as round-half-even of the exact
+// product y * inv with inv = fl32(1 / scale) (R18): one FFMA against 1.5 * 2^23 puts
+// the rounded integer in the low mantissa bits (|y * inv| <= 32767 * (1 + 2^-22) << 2^22), whose
+// low 16 bits are the int16 two's-complement code.  No clamp is reachable: |y| <= amax, so
+// |y * inv| < 32767.5.
+__device__ __forceinline__ uint32_t q16_bits(uint32_t ybits, float inv) {
+    return __float_as_uint(__fmaf_rn(__uint_as_float(ybits), inv, 12582912.0f));
 }
-__device__ __forceinline__ uint32_t q16_pack(uint32_t y0, uint32_t y1, float scale) {
-    return ((uint32_t)q16_code(y0, scale) & 0xFFFFu) | ((uint32_t)q16_code(y1, scale) << 16);
+__device__ __forceinline__ uint32_t q16_pack(uint32_t y0, uint32_t y1, float inv) {
+    return ptx::prmt(q16_bits(y0, inv), q16_bits(y1, inv), 0x5410u);
 }
 __device__ __forceinline__ float q16_scale(uint32_t amax_bits) {
     return amax_bits == 0 ? 1.0f : __fdiv_rn(__uint_as_float(amax_bits), 32767.0f);
 }
+__device__ __forceinline__ float q16_inv(float scale) { return __frcp_rn(scale); }
 
 template <int B, int KM, int EPI>
 __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_constant__ KParams p) {
@@ -740,9 +743,25 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
         const uint32_t stage_tile = sbase + p.off_epi + (uint32_t)ew * 4096u;
         const int qmode = p.qmode;
         const int smode = (p.M == 4) ? 0 : ((p.M & 7) == 0 ? 1 : 2);   // store mode
+        // Q_ROW: block row (within the tile) of this lane's block in fold f, and the warp's lowest /
+        // highest row in fold f, 6 bits per fold (rows < kRowSlots <= 63; fixed for the kernel)
+        uint64_t rowpack = 0, lopack = 0, hipack = 0;
+        if (qmode == Q_ROW) {
+            for (int f = 0; f < p.F; ++f) {
+                const int b = f * p.L + lane_idx;
+                const bool ok = lane_idx < p.L && b < p.T_r * p.nbx;
+                const uint32_t r = ok ? (uint32_t)(b / p.nbx) : 63u;
+                const uint32_t lo = __reduce_min_sync(0xFFFFFFFFu, r);
+                const uint32_t hi = __reduce_max_sync(0xFFFFFFFFu, ok ? r : 0u);
+                rowpack |= (uint64_t)r << (6 * f);
+                lopack |= (uint64_t)lo << (6 * f);
+                hipack |= (uint64_t)hi << (6 * f);
+            }
+        }
         int db = 0;
         uint32_t dph = 0;
         int n_items = 0;
+        const bool tr = (warp == kEpiWarp0 && lane == 0);
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             Unit w;
             if (!decode_unit(p, u, w)) continue;
@@ -752,10 +771,12 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
             for (int c = w.c0; c < w.c1; ++c) {
                 ptx::mbar_wait(bar_d_full + 8 * db, dph);
                 ptx::tc_fence_after();
+                if (tr) trace_ev(p, EV_E_DFULL, n_items);
                 const long long cs_global = (long long)w.s * p.cs_per_stream_sel +
                                             (long long)(w.g - p.gop_begin) * (p.G - 1) + c;
                 const uint32_t d_tm = tmem_base + lane_bits + d_col0 + (uint32_t)db * (uint32_t)p.d_cols;
                 CS_CHECK((cs_global + 1) * p.nblk * (long long)p.M <= p.out_floats);
+                CS_CHECK(qmode != Q_ROW || p.T_r <= kRowSlots);
                 if (qmode == Q_ABSMAX || qmode == Q_ROW) {
                     const uint32_t slots = sbase + kRowSlotOff + (uint32_t)(n_items % 3) * (kRowSlots * 4);
                     if (qmode == Q_ROW && lane_idx < kRowSlots)   // next item's slots: last read 2 items ago
@@ -765,7 +786,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                     for (int f = 0; f < p.F; ++f) {
                         const int b = f * p.L + lane_idx;
                         const bool valid = lane_idx < p.L && b < blocks_here;
-                        uint32_t mf = 0;
+                        float mff = 0.0f;
                         for (int j0 = 0; j0 < p.Mpad; j0 += 32) {
                             uint32_t v[32];
                             if (p.Mpad - j0 >= 32) {
@@ -778,16 +799,16 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                             }
                             ptx::tc_wait_ld();
 #pragma unroll
-                            for (int q = 0; q < 32; ++q) mf = max(mf, v[q] & 0x7FFFFFFFu);
+                            for (int q = 0; q < 32; ++q) mff = fmaxf(mff, fabsf(__uint_as_float(v[q])));
                         }
-                        if (!valid) mf = 0;
+                        const uint32_t mf = valid ? __float_as_uint(mff) : 0u;
                         if (qmode == Q_ABSMAX) {
                             mx = max(mx, mf);
                         } else {
                             // segmented warp max over the (few) block rows this warp's 32 blocks touch
-                            const int r = valid ? b / p.nbx : 0x7FFFFFFF;
-                            const int rlo = (int)__reduce_min_sync(0xFFFFFFFFu, (unsigned)r);
-                            const int rhi = (int)__reduce_max_sync(0xFFFFFFFFu, valid ? (unsigned)r : 0u);
+                            const int r = (int)((rowpack >> (6 * f)) & 63u);
+                            const int rlo = (int)((lopack >> (6 * f)) & 63u);
+                            const int rhi = (int)((hipack >> (6 * f)) & 63u);
                             for (int rr = rlo; rr <= rhi; ++rr) {
                                 const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, r == rr ? mf : 0u);
                                 if (lane == 0 && m != 0) ptx::atom_smem_max(slots + (uint32_t)rr * 4u, m);
@@ -803,9 +824,10 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                 }
                 if (qmode == Q_FRAME || qmode == Q_ROW) {
                     const uint32_t slots = sbase + kRowSlotOff + (uint32_t)(n_items % 3) * (kRowSlots * 4);
-                    float frame_scale = 1.0f;
+                    float inv = 1.0f;
+                    int inv_row = -1;
                     if (qmode == Q_FRAME) {
-                        frame_scale = q16_scale(__ldcg(p.amax + cs_global));
+                        inv = q16_inv(q16_scale(__ldcg(p.amax + cs_global)));
                     } else if (lane_idx < rows_here) {
                         p.scales[cs_global * p.nby + w.t * p.T_r + lane_idx] =
                             q16_scale(ptx::lds32(slots + (uint32_t)lane_idx * 4u));
@@ -816,15 +838,19 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                         const int b = row0 + (int)lane;
                         const bool valid = lane_idx < p.L && b < blocks_here;
                         const int rows_valid = min(32, min(p.L - ew * 32, blocks_here - row0));
-                        const float scale =
-                            qmode == Q_FRAME ? frame_scale
-                                             : q16_scale(valid ? ptx::lds32(slots + (uint32_t)(b / p.nbx) * 4u) : 0u);
+                        if (qmode == Q_ROW) {
+                            const int r = (int)((rowpack >> (6 * f)) & 63u);
+                            if (r != inv_row) {   // rows only grow with f: at most rows-per-tile updates
+                                inv_row = r;
+                                inv = q16_inv(q16_scale(valid ? ptx::lds32(slots + (uint32_t)r * 4u) : 0u));
+                            }
+                        }
                         if (smode == 0) {
                             uint32_t v[16];
                             ptx::tmem_ld_32x32b_x16(d_tm + (uint32_t)(f * p.Mpad), v);
                             ptx::tc_wait_ld();
-                            if (valid) ptx::stg64(codes_cs + (long long)b * 4, q16_pack(v[0], v[1], scale),
-                                                  q16_pack(v[2], v[3], scale));
+                            if (valid) ptx::stg64(codes_cs + (long long)b * 4, q16_pack(v[0], v[1], inv),
+                                                  q16_pack(v[2], v[3], inv));
                             continue;
                         }
                         for (int j0 = 0; j0 < p.Mpad; j0 += 32) {
@@ -842,13 +868,13 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                                     int16_t* dst = codes_cs + (long long)b * p.M + j0;
 #pragma unroll
                                     for (int q = 0; q < 32; ++q)
-                                        if (q < cw && j0 + q < p.M) dst[q] = (int16_t)q16_code(v[q], scale);
+                                        if (q < cw && j0 + q < p.M) dst[q] = (int16_t)(q16_bits(v[q], inv) & 0xFFFFu);
                                 }
                                 continue;
                             }
                             uint32_t wd[16];
 #pragma unroll
-                            for (int q = 0; q < 16; ++q) wd[q] = q16_pack(v[2 * q], v[2 * q + 1], scale);
+                            for (int q = 0; q < 16; ++q) wd[q] = q16_pack(v[2 * q], v[2 * q + 1], inv);
                             uint32_t* dst_row0 = reinterpret_cast<uint32_t*>(codes_cs + (long long)row0 * p.M + j0);
                             if (cw == 32)
                                 stage_store_codes<4>(wd, stage_tile, lane, dst_row0, p.M / 2, j0 / 2, p.M / 2,
@@ -862,6 +888,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(bar_d_empty + 8 * db);
+                if (tr) trace_ev(p, EV_E_DONE, n_items);
                 ++n_items;
                 if (++db == p.n_dbuf) {
                     db = 0;

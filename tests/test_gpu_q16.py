@@ -4,12 +4,13 @@ The kernel quantises ITS fp32 measurements y_gpu (|y_gpu - y| <= 1e-5 * S, BASEL
 with an fp32 scale and an fp32 rounding decision (R17-R19).  Against the exact y of the
 fp64 oracle this fixes, per scale group with exact maximum a and tolerance scale Smax:
   * scale:  |scale - a/32767| <= 1e-5 * Smax / 32767 + 2^-22 * scale;  all-zero group -> 1.0
-  * codes:  with t = y / scale (exact y, the kernel's scale) and d = 1e-5 * S / scale + |t| 2^-22,
+  * codes:  with t = y * inv (exact y, inv = fl32(1/scale) of the kernel's scale; the decision
+            rule of DESIGN.md R18) and d = 1e-5 * S * inv + |t| 2^-22,
             |code - t| <= 0.5 + d, and code == round(t) wherever t is farther than d from a tie
             (entries with S == 0 are exactly 0);  |code| <= 32767.
 Both sides decide in fp32 on their own y, so codes may differ from the oracle's only at ties
 within the tolerance band.  Two further bitwise checks tie q16 to the fp32 path: the codes equal
-round(y_gpu / scale) computed with torch from the fp32 output of the same kernel, and the
+round(y_gpu * inv) computed on the host from the fp32 output of the same kernel, and the
 per-frame scale equals the maximum of the per-row scales.
 """
 import numpy as np
@@ -40,8 +41,9 @@ def check_group(codes, scale, y, S):
         return
     smax = float(np.max(S))
     assert abs(scale - a / QMAX) <= REL * smax / QMAX + 2.0 ** -22 * scale, (scale, a / QMAX)
-    t = y / scale
-    d = REL * S / scale + np.abs(t) * 2.0 ** -22
+    inv = float(np.float32(1.0) / np.float32(scale))
+    t = y * inv
+    d = REL * S * inv + np.abs(t) * 2.0 ** -22
     assert np.all(np.abs(codes) <= QMAX)
     assert np.all(np.abs(codes - t) <= 0.5 + d + 1e-12), float(np.max(np.abs(codes - t) - d))
     away = np.abs(np.abs(t - np.floor(t)) - 0.5) > d + 1e-9
@@ -72,16 +74,17 @@ def run_q16(enc, fd, granularity):
 
 
 def fp32_consistency(enc, fd, codes_f, scales_f, codes_r, scales_r):
-    """Bitwise: q16 codes == round(y_gpu / scale) from the fp32 output of the same kernel, and the
-    frame scale == max of the row scales."""
+    """Bitwise: q16 codes == round-half-even(y_gpu * fl32(1/scale)) from the fp32 output of the same
+    kernel (exact fp64 product), and the frame scale == max of the row scales."""
     y32 = enc.encode_batch(fd)
     torch.cuda.synchronize()
-    q = torch.round(y32 / scales_f.view(-1, 1, 1)).clamp(-QMAX, QMAX).to(torch.int16)
-    assert torch.equal(q, codes_f)
-    rs = scales_r.view(scales_r.shape[0], enc.nby, 1).repeat(1, 1, enc.nbx).view(scales_r.shape[0], -1, 1)
-    qr = torch.round(y32 / rs).clamp(-QMAX, QMAX).to(torch.int16)
-    assert torch.equal(qr, codes_r)
-    assert torch.equal(scales_f, scales_r.max(dim=1).values)
+    y32 = y32.cpu().numpy().astype(np.float64)
+    sf, sr = scales_f.cpu().numpy(), scales_r.cpu().numpy()
+    inv_f = (np.float32(1.0) / sf).astype(np.float64)
+    assert np.array_equal(np.rint(y32 * inv_f[:, None, None]).astype(np.int16), codes_f.cpu().numpy())
+    inv_r = np.repeat((np.float32(1.0) / sr).astype(np.float64), enc.nbx, axis=1)[:, :, None]
+    assert np.array_equal(np.rint(y32 * inv_r).astype(np.int16), codes_r.cpu().numpy())
+    assert np.array_equal(sf, sr.max(axis=1))
 
 
 CASES = [

@@ -7,19 +7,26 @@ import torch
 import synth
 import paper_1311_1419_b200 as P
 
-def main(workload="C4", M=None, cap=256, T=None):
+def main(workload="C4", M=None, cap=256, T=None, q16=None):
     cfg = synth.CONFIGS[workload]
     M = M or cfg.M
     if T:
         cfg = cfg.with_(T=T)
     frames = torch.from_numpy(synth.gen_video(cfg)).cuda()
     enc = P.Encoder(cfg.W, cfg.H, cfg.G, cfg.B, M, synth.phi_from_seed(synth.phi_seed(), M, cfg.B ** 2))
+    tf = os.environ.get("TUNE_FILE")
+    if tf and os.path.exists(tf):
+        k = json.load(open(tf)).get(f"{workload}:{M}")
+        if k is not None:
+            enc.set_candidate(int(k))
+    run = (lambda: enc.encode_batch(frames, out)) if q16 is None else (lambda: enc.encode_batch_q16(frames, q16))
     out = enc.encode_batch(frames)
+    run()
     ev = enc.TRACE_EVENTS
     buf = torch.zeros(len(ev) * cap, dtype=torch.int64, device="cuda")
     enc.set_trace(buf, cap)
     torch.cuda.synchronize()
-    enc.encode_batch(frames, out)
+    run()
     torch.cuda.synchronize()
     enc.set_trace(None, 0)
     t = buf.view(len(ev), cap).cpu().numpy().astype(np.int64)
@@ -72,5 +79,6 @@ def main(workload="C4", M=None, cap=256, T=None):
 if __name__ == "__main__":
     w = sys.argv[1] if len(sys.argv) > 1 else "C4"
     Ms = [int(m) for m in sys.argv[2].split(",")] if len(sys.argv) > 2 else [None]
+    q16 = None if len(sys.argv) <= 3 or sys.argv[3] == "f32" else {"q16frame": 0, "q16row": 1}[sys.argv[3]]
     for M in Ms:
-        main(w, M)
+        main(w, M, q16=q16)
