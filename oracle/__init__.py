@@ -30,13 +30,18 @@ Paper passages followed (PAPER.md line numbers, section):
   a6 output layout   -- y[s][g][c][by][bx][m], block-major (BASELINE.json:5 item 4)
   a7 CR accounting   -- "original bits / (key bits + measurement bits)"
                         (BASELINE.json:5); Table I closed form P:113-126
+  f1 quantisation    -- SPEC.md:154-162 (scale = max|y|/32767, codes = round(y/scale)),
+                        f32 scale SPEC.md:410; decision precision DESIGN.md R17-R18
+  f3 adjoint         -- SPEC.md:145-153 (A^T v), TVAL3 start point x = A^T y SPEC.md:235;
+                        per block x_b = Phi^T y_b reassembled into the frame (inverse of a2)
 """
 from __future__ import annotations
 
 import numpy as np
 
 __all__ = [
-    "quantize", "dequantize", "quantize_frames", "measure_entries", "gop_partition", "cs_frame_count", "block_grid", "frame_blocks", "residual", "measure",
+    "quantize", "dequantize", "quantize_frames", "frame_unblocks", "adjoint_blocks", "adjoint",
+    "adjoint_tolerance_scale", "measure_entries", "gop_partition", "cs_frame_count", "block_grid", "frame_blocks", "residual", "measure",
     "tolerance_scale", "encode", "encode_stream", "phi_values", "compression_ratio", "total_cr",
     "check_tolerance",
 ]
@@ -209,6 +214,39 @@ def quantize_frames(y, group_blocks=None):
             for gi, (b0, b1) in enumerate(group_blocks):
                 codes[i, b0:b1], scales[i, gi] = quantize(y[i, b0:b1])
     return codes, scales
+
+
+# -- f3: adjoint / back-projection ---------------------------------------------------------------
+def frame_unblocks(X: np.ndarray, W: int, H: int, B: int) -> np.ndarray:
+    """Inverse of frame_blocks: [nby*nbx][B*B] (block raster order, row-major inside the block)
+    -> [H][W], dropping the zero padding outside the frame."""
+    nby, nbx = block_grid(W, H, B)
+    X = np.asarray(X)
+    full = X.reshape(nby, nbx, B, B).transpose(0, 2, 1, 3).reshape(nby * B, nbx * B)
+    return full[:H, :W]
+
+
+def adjoint_blocks(v: np.ndarray, phi: np.ndarray) -> np.ndarray:
+    """SPEC.md:145-153 adjoint: A^T v for every block row v_b of v [nblk][M] -> [nblk][N],
+    x_b = Phi^T v_b (fp64)."""
+    return np.asarray(v, dtype=np.float64) @ np.asarray(phi, dtype=np.float64)
+
+
+def adjoint(meas: np.ndarray, phi_bits: np.ndarray, W: int, H: int, B: int) -> np.ndarray:
+    """Back-projection x0 = Phi^T y of every block of every frame (the TVAL3
+    initial point x = A^T y), reassembled into frames: meas [n][nblk][M] (the
+    measurement layout, a6) -> fp64 [n][H][W]."""
+    phi = phi_values(phi_bits)
+    meas = np.asarray(meas, dtype=np.float64)
+    return np.stack([frame_unblocks(adjoint_blocks(meas[i], phi), W, H, B) for i in range(meas.shape[0])]) \
+        if meas.shape[0] else np.zeros((0, H, W))
+
+
+def adjoint_tolerance_scale(meas: np.ndarray, phi_bits: np.ndarray, W: int, H: int, B: int) -> np.ndarray:
+    """S[n][y][x] = sum_m |Phi_mj| |v_m| for the pixel's block and in-block index j (the per-entry
+    scale of the acceptance bound, in the form BASELINE.json:5 states for y)."""
+    return adjoint(np.abs(np.asarray(meas, dtype=np.float64)),
+                   np.abs(phi_values(phi_bits)).astype(np.float16).view(np.uint16), W, H, B)
 
 
 # -- a7 ------------------------------------------------------------------------------------------

@@ -337,3 +337,78 @@ def test_quantize_frames_per_group():
     c2, s2 = oracle.quantize_frames(y, [(0, 4), (4, 10)])
     assert s2.shape == (3, 2)
     assert np.array_equal(c2[1, 4:], oracle.quantize(y[1, 4:])[0])
+
+
+# ---------------------------------------------------------------- f3: adjoint
+def test_frame_unblocks_inverts_frame_blocks():
+    rng = np.random.default_rng(31)
+    for (H, W, B) in [(16, 16, 8), (33, 48, 16), (40, 96, 32), (7, 5, 2)]:
+        F = rng.integers(0, 256, (H, W))
+        assert np.array_equal(oracle.frame_unblocks(oracle.frame_blocks(F, B), W, H, B), F)
+
+
+def test_adjoint_identity():
+    """SPEC.md:144/153/556: <Phi r, v> == <r, Phi^T v> (per frame, summed over blocks), 1e-9 relative,
+    on 100 random instances including ragged frames -- catches a transposed Phi, a wrong block
+    placement or in-block order in the reassembly, or a dropped/duplicated block."""
+    rng = np.random.default_rng(32)
+    for trial in range(100):
+        B = int(rng.choice([2, 4, 8]))
+        M = int(rng.integers(1, B * B + 1))
+        H, W = int(rng.integers(1, 3 * B + 2)), int(rng.integers(1, 3 * B + 2))
+        phi = synth.phi_from_seed(int(rng.integers(1 << 30)), M, B * B)
+        F = rng.integers(-255, 256, (H, W))
+        nby, nbx = oracle.block_grid(W, H, B)
+        v = rng.normal(size=(1, nby * nbx, M))
+        y = oracle.measure(oracle.frame_blocks(F, B), oracle.phi_values(phi))
+        x = oracle.adjoint(v, phi, W, H, B)[0]
+        lhs, rhs = float(np.sum(y * v[0])), float(np.sum(F * x))
+        assert abs(lhs - rhs) <= 1e-9 * max(1.0, np.sum(np.abs(y * v[0]))), (trial, lhs, rhs)
+
+
+def test_adjoint_special_cases():
+    """v = 0 -> 0; v = e_(b,i) -> row i of Phi laid into block b (cropped at the frame edge);
+    Phi = I (M = N) -> the unblocked v; orthonormal rows (a row subset of a permutation) ->
+    Phi Phi^T v = v."""
+    B, M = 4, 5
+    H, W = 6, 10                                    # nby = 2, nbx = 3, ragged both ways
+    phi = synth.phi_from_seed(4, M, B * B)
+    phiv = oracle.phi_values(phi)
+    assert np.all(oracle.adjoint(np.zeros((2, 6, M)), phi, W, H, B) == 0)
+    for b in range(6):
+        for i in range(M):
+            v = np.zeros((1, 6, M))
+            v[0, b, i] = 1.0
+            x = oracle.adjoint(v, phi, W, H, B)[0]
+            want = np.zeros((2 * B, 3 * B))
+            by, bx = divmod(b, 3)
+            want[by * B:(by + 1) * B, bx * B:(bx + 1) * B] = phiv[i].reshape(B, B)
+            assert np.array_equal(x, want[:H, :W]), (b, i)
+    eye = np.eye(B * B).astype(np.float16).view(np.uint16)
+    v = np.random.default_rng(5).normal(size=(2, 6, B * B))
+    x = oracle.adjoint(v, eye, W, H, B)
+    for k in range(2):
+        assert np.array_equal(x[k], oracle.frame_unblocks(v[k], W, H, B))
+    perm = np.random.default_rng(6).permutation(B * B)[:M]
+    P = np.zeros((M, B * B))
+    P[np.arange(M), perm] = 1.0
+    v = np.random.default_rng(7).integers(-100, 100, size=(1, 6, M)).astype(np.float64)  # frame_blocks is integer
+    Wf, Hf = 3 * B, 2 * B                           # no cropping: Phi (Phi^T v) == v exactly
+    xb = oracle.frame_blocks(oracle.adjoint(v, P.astype(np.float16).view(np.uint16), Wf, Hf, B)[0], B)
+    assert np.array_equal(oracle.measure(xb, P), v[0])
+
+
+def test_adjoint_brute_force():
+    """Exact rational loops over the definition x[Y][X] = sum_m Phi[m][j] v[b][m] on a tiny case."""
+    B, M, H, W = 2, 3, 3, 5
+    phi = synth.phi_from_seed(9, M, B * B)
+    phiv = oracle.phi_values(phi)
+    rng = np.random.default_rng(8)
+    v = rng.integers(-50, 50, size=(1, 6, M)) / 8.0
+    x = oracle.adjoint(v, phi, W, H, B)[0]
+    for Y in range(H):
+        for X in range(W):
+            b = (Y // B) * 3 + X // B
+            j = (Y % B) * B + X % B
+            want = sum(Fraction(float(phiv[m, j])) * Fraction(float(v[0, b, m])) for m in range(M))
+            assert Fraction(float(x[Y, X])) == want
