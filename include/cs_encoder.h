@@ -170,6 +170,20 @@ int64_t cs_q16_scale_count(const cs_encoder* enc, int n_seq, int T, int granular
 int cs_encode_batch_q16(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, int T, int granularity,
                         int16_t* codes_dev, float* scales_dev, cs_stream_t stream);
 
+/* ---- adjoint / back-projection ---------------------------------- */
+
+/* SPEC.md:145-153 adjoint(A, v) = A^T v, the decoder's start point x = A^T y, for the
+ * block-based Phi: every block b of every frame gets x_b = Phi^T y_b (B*B values from M), laid back
+ * into the frame (block (by, bx), in-block index j = yy*B + xx -> pixel (by*B + yy, bx*B + xx);
+ * pixels of padded blocks outside the frame are dropped).
+ *   meas_dev = DEVICE fp32 [n_frames][nby][nbx][M] (the layout cs_encode_batch writes; any fp32
+ *              values), 16-byte aligned;  x_dev = DEVICE fp32 [n_frames][H][W], 16-byte aligned.
+ * Tensor cores (kind::tf32) with y split into two tf32 terms: |error| <~ 1e-6 * sum_m |Phi_mj y_m|.
+ * One asynchronous launch on `stream`; no allocation.  Errors: CS_ERR_ARG (NULL / misaligned /
+ * n_frames < 0), CS_ERR_UNSUPPORTED (M % 4 != 0: measurement rows must be 16-byte multiples;
+ * more than 2^31 blocks in one call), CS_ERR_CUDA. */
+int cs_adjoint(cs_encoder* enc, const float* meas_dev, int64_t n_frames, float* x_dev, cs_stream_t stream);
+
 /* ---- encode (HOST buffers; synchronous) ------------------------------------------------- */
 
 /* End-to-end call: frames_host = HOST [n_seq][T][H][W] uint8, meas_host = HOST fp32 output

@@ -66,6 +66,7 @@ def lib() -> ctypes.CDLL:
             "cs_encode_batch_host": (c_int, [vp, vp, c_int, c_int, vp]),
             "cs_encode_batch_q16": (c_int, [vp, vp, c_int, c_int, c_int, vp, vp, vp]),
             "cs_q16_scale_count": (c_i64, [vp, c_int, c_int, c_int]),
+            "cs_adjoint": (c_int, [vp, vp, c_i64, vp, vp]),
             "cs_measurement_count": (c_i64, [vp, c_int, c_int]),
             "cs_compression_ratio": (c_dbl, [vp, c_int, c_dbl, c_int]),
             "cs_compression_ratio_cfg": (c_dbl, [c_int, c_int, c_int, c_int, c_int, c_int, c_dbl, c_int]),
@@ -262,6 +263,20 @@ class Encoder:
         _check(lib().cs_encode_batch_q16(self._h, _ptr(frames), n_seq, T, granularity, _ptr(codes), _ptr(scales),
                                          _stream_handle(stream)))
         return codes, scales
+
+    # -- adjoint / back-projection (f3)
+    def adjoint(self, meas, out=None, stream=None):
+        """meas: CUDA float32 [n][nblk][M] (contiguous); returns CUDA float32 [n][H][W] = Phi^T y per
+        block laid back into the frame."""
+        import torch
+        assert meas.is_cuda and meas.dtype == torch.float32 and meas.is_contiguous()
+        n = meas.numel() // (self.nblk * self.M)
+        assert meas.numel() == n * self.nblk * self.M
+        if out is None:
+            out = torch.empty((n, self.H, self.W), dtype=torch.float32, device=meas.device)
+        assert out.is_cuda and out.dtype == torch.float32 and out.is_contiguous() and out.numel() >= n * self.H * self.W
+        _check(lib().cs_adjoint(self._h, _ptr(meas), n, _ptr(out), _stream_handle(stream)))
+        return out
 
     # -- encode (host buffers)
     def encode_batch_host(self, frames, out=None):
