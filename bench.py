@@ -138,6 +138,49 @@ def load_traffic(workload):
 
 
 # ------------------------------------------------------------------------------------------ ours
+def timed_steps(args, launch, n_launch, stream, dev, world):
+    """W untimed warm-up steps, then K timed steps of n_launch launches each (CUDA events around
+    every launch and around the whole timed region, on the launching stream), barrier +
+    synchronize on both sides, clocks sampled during the timed region; the device time is the max
+    over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    def step(ev=None):
+        for i in range(n_launch):
+            if ev is not None:
+                ev[i][0].record(stream)
+            launch(i)
+            if ev is not None:
+                ev[i][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    K = args.steps
+    evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in range(n_launch)]
+           for _ in range(K)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index or 0) as clk:
+        t0.record(stream)
+        for k in range(K):
+            step(evs[k])
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms_total = t0.elapsed_time(t1)
+    launch_ms = [[evs[k][i][0].elapsed_time(evs[k][i][1]) for k in range(K)] for i in range(n_launch)]
+    if world > 1:
+        tt = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_total = float(tt.item())
+    return ms_total, launch_ms, clk
+
+
 def run_ours(args, cfg, Ms):
     import torch
     import torch.distributed as dist
@@ -185,42 +228,15 @@ def run_ours(args, cfg, Ms):
         with open(args.tune_file, "w") as f:
             json.dump(tuned, f)
 
-    def step(ev=None):
-        for i, e in enumerate(encs):
-            if ev is not None:
-                ev[i][0].record(stream)
-            if gran is None:
-                e.encode_batch(frames, outs[i], stream)
-            else:
-                e.encode_batch_q16(frames, gran, qouts[i][0], qouts[i][1], stream)
-            if ev is not None:
-                ev[i][1].record(stream)
+    def launch(i):
+        e = encs[i]
+        if gran is None:
+            e.encode_batch(frames, outs[i], stream)
+        else:
+            e.encode_batch_q16(frames, gran, qouts[i][0], qouts[i][1], stream)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize(dev)
-
+    ms_total, launch_ms, clk = timed_steps(args, launch, len(Ms), stream, dev, world)
     K = args.steps
-    evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in Ms]
-           for _ in range(K)]
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clk:
-        t0.record(stream)
-        for k in range(K):
-            step(evs[k])
-        t1.record(stream)
-        torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    ms_total = t0.elapsed_time(t1)
-    launch_ms = [[evs[k][i][0].elapsed_time(evs[k][i][1]) for k in range(K)] for i in range(len(Ms))]
-    if world > 1:
-        tt = torch.tensor([ms_total], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms_total = float(tt.item())
 
     # ---- end to end through the public host-buffer C-ABI call (copies inside the timed region)
     e2e = None
@@ -300,6 +316,104 @@ def run_ours(args, cfg, Ms):
     if world > 1:
         dist.destroy_process_group()
     return line
+
+
+# ------------------------------------------------------------------------------- f3 adjoint op
+def run_adjoint(args, cfg, Ms):
+    """--op adjoint: back-projection x0 = Phi^T y of every CS frame of the workload (the measurements
+    the encoder produced, resident in HBM), one cs_adjoint launch per M per step."""
+    import torch
+    import torch.distributed as dist
+    import paper_1311_1419_b200 as P
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    n_seq = cfg.S
+    frames = torch.from_numpy(synth.gen_video(cfg, streams=range(rank * n_seq, (rank + 1) * n_seq))).to(dev)
+    encs, ys, xs = [], [], []
+    for M in Ms:
+        phi = synth.phi_from_seed(synth.phi_seed(), M, cfg.B ** 2)
+        e = P.Encoder(cfg.W, cfg.H, cfg.G, cfg.B, M, phi)
+        y = e.encode_batch(frames)
+        encs.append(e)
+        ys.append(y)
+        xs.append(torch.empty((y.shape[0], cfg.H, cfg.W), dtype=torch.float32, device=dev))
+    del frames
+    torch.cuda.synchronize(dev)
+    torch.cuda.empty_cache()
+    stream = torch.cuda.current_stream(dev)
+
+    def launch(i):
+        encs[i].adjoint(ys[i], xs[i], stream)
+
+    ms_total, launch_ms, clk = timed_steps(args, launch, len(Ms), stream, dev, world)
+    K = args.steps
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return None
+    peak, peak_src = load_peaks()
+    n_cs = ys[0].shape[0]
+    px = n_cs * cfg.W * cfg.H
+    per_m, tot_b, tot_ms = {}, 0.0, 0.0
+    for i, M in enumerate(Ms):
+        avg = sum(launch_ms[i]) / K
+        b = ys[i].numel() * 4 + xs[i].numel() * 4          # y read once + x written once
+        per_m[str(M)] = {"ms_median": statistics.median(launch_ms[i]), "ms_mean": avg,
+                         "gpix_s": px / (avg * 1e-3) / 1e9, "alg_gbs": b / (avg * 1e-3) / 1e9,
+                         "frac_of_peak": b / (avg * 1e-3) / 1e9 / peak, "alg_bytes": b,
+                         "tflops_tf32": 2 * 2 * n_cs * encs[i].nblk * M * cfg.B ** 2 / (avg * 1e-3) / 1e12}
+        tot_b += b
+        tot_ms += avg
+    achieved = tot_b / (tot_ms * 1e-3) / 1e9
+    ms_step = ms_total / K
+    line = {
+        "metric": "CS-frame Gpixels/s back-projected (x0 = Phi^T y per block, frame layout)",
+        "value": world * len(Ms) * px / (ms_step * 1e-3) / 1e9, "unit": "Gpixel/s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 in, tf32 x2 (hi/lo split) -> f32 (tensor core kind::tf32)",
+        "data": "synthetic (measurements of the seeded video, synth/)",
+        "config": {"workload": args.workload, "op": "adjoint", "W": cfg.W, "H": cfg.H, "T": cfg.T,
+                   "streams_per_gpu": n_seq, "B": cfg.B, "M": list(Ms),
+                   "l2": "outputs larger than L2 (x is n_cs*H*W*4 bytes per launch); no flush",
+                   "parallelism": f"dp{world} (independent sequences per GPU, no collective)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "peak_source": peak_src,
+                     "kernel": "cs_adjoint_kernel (alg bytes = fp32 y read once + fp32 x written once)"},
+        "per_M": per_m,
+        "gpu_launches": K * len(Ms),
+        "clocks": clk.summary(),
+        "e2e": {"value": None, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                "how": "not measured: the adjoint has a device-buffer C-ABI call only"},
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = adjoint_cpu_baseline(cfg, Ms, args.cpu_budget)
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return line
+
+
+def adjoint_cpu_baseline(cfg, Ms, budget_s=15.0):
+    """The oracle's adjoint (fp64 numpy) on CS frames of the workload's shape; frames added until
+    about half the budget is spent."""
+    import oracle
+    rng = np.random.default_rng(0)
+    nblk = -(-cfg.W // cfg.B) * -(-cfg.H // cfg.B)
+    phis = [synth.phi_from_seed(synth.phi_seed(), M, cfg.B ** 2) for M in Ms]
+    n, dt = 0, 0.0
+    t0 = time.perf_counter()
+    while dt < budget_s / 2 and n < 64:
+        for M, phi in zip(Ms, phis):
+            oracle.adjoint(rng.normal(size=(1, nblk, M)), phi, cfg.W, cfg.H, cfg.B)
+        n += 1
+        dt = time.perf_counter() - t0
+    px = n * len(Ms) * cfg.W * cfg.H
+    return {"value": px / dt / 1e9, "unit": "Gpixel/s", "cores": cpu_threads(), "kind": "oracle",
+            "sample": f"fp64 numpy oracle adjoint, {n} frame(s) of {cfg.W}x{cfg.H} x M in {list(Ms)}, {dt:.2f} s"}
 
 
 # ------------------------------------------------------------------------------------ oracle arm
@@ -391,6 +505,8 @@ def main(argv=None):
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-autotune", action="store_true")
     ap.add_argument("--tune-candidates", type=int, default=6)
+    ap.add_argument("--op", choices=["encode", "adjoint"], default="encode",
+                    help="encode (the north-star hot path, default) or adjoint (f3 back-projection)")
     ap.add_argument("--output", choices=list(OUTPUTS), default="f32",
                     help="f32 measurements (headline) or 16-bit codes (f1): per-frame or per-row scales")
     ap.add_argument("--tune-file", default=None, help="json of chosen plan indices (read if present, else written)")
@@ -401,6 +517,8 @@ def main(argv=None):
     Ms = tuple(int(m) for m in args.M.split(",")) if args.M else cfg.Ms
     if args.impl == "reference":
         return run_reference(args, cfg, Ms)
+    if args.op == "adjoint":
+        return run_adjoint(args, cfg, Ms)
     return run_ours(args, cfg, Ms)
 
 
