@@ -34,6 +34,8 @@ Paper passages followed (PAPER.md line numbers, section):
                         f32 scale SPEC.md:410; decision precision DESIGN.md R17-R18
   f3 adjoint         -- SPEC.md:145-153 (A^T v), TVAL3 start point x = A^T y SPEC.md:235;
                         per block x_b = Phi^T y_b reassembled into the frame (inverse of a2)
+  f4 closed-loop key -- Eq.(2)-(3) P:87-91 with SPEC's 8x8 DCT intra codec as the
+                        stand-in for H.264 intra; fixed-point transform DESIGN.md R21
 """
 from __future__ import annotations
 
@@ -41,7 +43,8 @@ import numpy as np
 
 __all__ = [
     "quantize", "dequantize", "quantize_frames", "frame_unblocks", "adjoint_blocks", "adjoint",
-    "adjoint_tolerance_scale", "measure_entries", "gop_partition", "cs_frame_count", "block_grid", "frame_blocks", "residual", "measure",
+    "adjoint_tolerance_scale", "JPEG_LUMA", "dct_basis", "dct_basis_int", "key_qsteps", "pad8",
+    "intra_forward", "intra_inverse", "decode_key", "encode_stream_closed_loop", "measure_entries", "gop_partition", "cs_frame_count", "block_grid", "frame_blocks", "residual", "measure",
     "tolerance_scale", "encode", "encode_stream", "phi_values", "compression_ratio", "total_cr",
     "check_tolerance",
 ]
@@ -247,6 +250,103 @@ def adjoint_tolerance_scale(meas: np.ndarray, phi_bits: np.ndarray, W: int, H: i
     scale of the acceptance bound, in the form BASELINE.json:5 states for y)."""
     return adjoint(np.abs(np.asarray(meas, dtype=np.float64)),
                    np.abs(phi_values(phi_bits)).astype(np.float16).view(np.uint16), W, H, B)
+
+
+# -- f4: closed-loop key frame through the stand-in intra codec -----------------------------------
+# SPEC.md:282-308: 8x8 block DCT, uniform quantisation by quant_scale * the standard luminance
+# perceptual matrix, dequantise, inverse DCT, clamp to [0, 255]; edge-replication padding to
+# multiples of 8.  The transform is defined in fixed point (DESIGN.md R21) so that every integer
+# decision (coefficient rounding, pixel rounding) is exact and identical on every platform
+# (SPEC.md:299 "bit-exact deterministic").  Entropy coding and the CR-23 rate search (S:284, S:303)
+# are host-side and out of scope (SURVEY.md sec.2/8 f4).
+JPEG_LUMA = np.array([
+    [16, 11, 10, 16, 24, 40, 51, 61],
+    [12, 12, 14, 19, 26, 58, 60, 55],
+    [14, 13, 16, 24, 40, 57, 69, 56],
+    [14, 17, 22, 29, 51, 87, 80, 62],
+    [18, 22, 37, 56, 68, 109, 103, 77],
+    [24, 35, 55, 64, 81, 104, 113, 92],
+    [49, 64, 78, 87, 103, 121, 120, 101],
+    [72, 92, 95, 98, 112, 100, 103, 99]], dtype=np.int64)   # ITU-T T.81 Annex K, Table K.1
+DCT_BITS = 12
+
+
+def dct_basis() -> np.ndarray:
+    """Orthonormal 8-point DCT-II: C[u][x] = a(u) cos((2x+1) u pi / 16), a(0) = sqrt(1/8),
+    a(u>0) = sqrt(2/8); the 2-D transform of a block s is C s C^T."""
+    u = np.arange(8)[:, None]
+    x = np.arange(8)[None, :]
+    a = np.where(u == 0, np.sqrt(1.0 / 8.0), np.sqrt(2.0 / 8.0))
+    return a * np.cos((2 * x + 1) * u * np.pi / 16.0)
+
+
+def dct_basis_int() -> np.ndarray:
+    """C scaled by 2^12 and rounded to integers (the fixed-point basis of R21)."""
+    return np.rint(dct_basis() * (1 << DCT_BITS)).astype(np.int64)
+
+
+def key_qsteps(quant_scale: float) -> np.ndarray:
+    """Integer quantiser steps [v][u] = clip(round(quant_scale * JPEG_LUMA), 1, 4096) (R21)."""
+    return np.clip(np.rint(quant_scale * JPEG_LUMA), 1, 4096).astype(np.int64)
+
+
+def pad8(frame: np.ndarray) -> np.ndarray:
+    """Edge replication to multiples of 8."""
+    H, W = frame.shape
+    return np.pad(frame, ((0, (-H) % 8), (0, (-W) % 8)), mode="edge")
+
+
+def intra_forward(frame: np.ndarray, qsteps: np.ndarray) -> np.ndarray:
+    """Quantised DCT coefficients int16 [nby8][nbx8][8 (v)][8 (u)] of a uint8 frame.
+    Per 8x8 block s (level-shifted by -128): t1 = s Ci^T, t2 = Ci t1 (exact integers, scale 2^24);
+    q = round-half-away-from-zero(t2 / (qstep * 2^24)), clipped to int16."""
+    Ci = dct_basis_int()
+    P = pad8(np.asarray(frame)).astype(np.int64) - 128
+    nby, nbx = P.shape[0] // 8, P.shape[1] // 8
+    out = np.empty((nby, nbx, 8, 8), dtype=np.int16)
+    d = np.asarray(qsteps, dtype=np.int64) << (2 * DCT_BITS)
+    for by in range(nby):
+        for bx in range(nbx):
+            s = P[by * 8:(by + 1) * 8, bx * 8:(bx + 1) * 8]
+            t2 = Ci @ (s @ Ci.T)
+            q = np.sign(t2) * ((np.abs(t2) + d // 2) // d)
+            out[by, bx] = np.clip(q, -32768, 32767)
+    return out
+
+
+def intra_inverse(coef: np.ndarray, qsteps: np.ndarray, W: int, H: int) -> np.ndarray:
+    """Decoded uint8 frame [H][W] (Eq. 2's F-hat): dq = q * qstep; t1 = dq Ci (scale 2^12),
+    t1 = floor((t1 + 2^11) / 2^12); t2 = Ci^T t1; pixel = floor((t2 + 2^11) / 2^12) + 128, clamped to
+    [0, 255]; the padding is cropped."""
+    Ci = dct_basis_int()
+    coef = np.asarray(coef, dtype=np.int64)
+    nby, nbx = coef.shape[:2]
+    out = np.empty((nby * 8, nbx * 8), dtype=np.int64)
+    half = 1 << (DCT_BITS - 1)
+    for by in range(nby):
+        for bx in range(nbx):
+            dq = coef[by, bx] * np.asarray(qsteps, dtype=np.int64)
+            t1 = (dq @ Ci + half) >> DCT_BITS
+            t2 = Ci.T @ t1
+            out[by * 8:(by + 1) * 8, bx * 8:(bx + 1) * 8] = ((t2 + half) >> DCT_BITS) + 128
+    return np.clip(out, 0, 255)[:H, :W].astype(np.uint8)
+
+
+def decode_key(frame: np.ndarray, qsteps: np.ndarray) -> np.ndarray:
+    """F-hat_key = decode(encode(F_key)) (Eq. 2), computed at the encoder (closed loop)."""
+    H, W = frame.shape
+    return intra_inverse(intra_forward(frame, qsteps), qsteps, W, H)
+
+
+def encode_stream_closed_loop(frames: np.ndarray, phi_bits: np.ndarray, G: int, B: int, qsteps: np.ndarray,
+                              with_scale: bool = True):
+    """As encode_stream, with every CS frame's residual taken against its GOP's DECODED key frame
+    (Eq. 3: D = F_N - F-hat_key; "we reconstruct key frame, which is subtracted from CS
+    frames")."""
+    frames = np.array(frames, copy=True)
+    for key_t, _ in gop_partition(frames.shape[0], G):
+        frames[key_t] = decode_key(frames[key_t], qsteps)
+    return encode_stream(frames, phi_bits, G, B, with_scale)
 
 
 # -- a7 ------------------------------------------------------------------------------------------

@@ -113,6 +113,10 @@ struct KParams {
     uint32_t smem_bytes;      // dynamic SMEM size (from the aligned base)
     long long out_floats;     // output buffer size in floats
     long long frames_bytes;   // input buffer size in bytes
+    // f4 closed loop: decoded key frames [n_seq][n_gops_T][H][W] (nullptr = the raw key frames of
+    // `frames`, the north star's pass-through); n_gops_T = ceil(T / G)
+    const uint8_t* keys;
+    int n_gops_T;
     // EPI_Q16 (f1)
     int qmode;                // QMode
     int16_t* codes;           // [n_cs][nblk][M] int16, same layout as out
@@ -461,7 +465,9 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             Unit w;
             if (!decode_unit(p, u, w)) continue;
-            const uint8_t* key_f = p.frames + (size_t)key_frame(p, w) * frame_bytes;
+            const uint8_t* const raw_key = p.frames + (size_t)key_frame(p, w) * frame_bytes;
+            const uint8_t* const key_f =
+                p.keys ? p.keys + ((size_t)w.s * p.n_gops_T + (size_t)w.g) * frame_bytes : raw_key;
             if constexpr (KM == KEY_REGS) {  // the key strip is the unit's first ring item
                 ptx::mbar_wait(bar_stage_empty + 8 * st, ph ^ 1u);
                 if (elect_one()) {
@@ -487,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                 if (kb == 0) kph ^= 1u;
             }
             for (int c = w.c0; c < w.c1; ++c) {
-                const uint8_t* cs_f = key_f + (size_t)(1 + c) * frame_bytes;
+                const uint8_t* cs_f = raw_key + (size_t)(1 + c) * frame_bytes;
                 for (int k = 0; k < p.n_chunks; ++k) {
                     ptx::mbar_wait(bar_stage_empty + 8 * st, ph ^ 1u);
                     if (lane == 0) trace_ev(p, EV_P_EMPTY, n_items);

@@ -412,3 +412,95 @@ def test_adjoint_brute_force():
             j = (Y % B) * B + X % B
             want = sum(Fraction(float(phiv[m, j])) * Fraction(float(v[0, b, m])) for m in range(M))
             assert Fraction(float(x[Y, X])) == want
+
+
+# ---------------------------------------------------------------- f4: closed-loop key (Eq. 2-4)
+def _psnr(a, b):
+    mse = np.mean((a.astype(np.float64) - b.astype(np.float64)) ** 2)
+    return np.inf if mse == 0 else 10 * np.log10(255.0 ** 2 / mse)
+
+
+def test_dct_basis_is_the_textbook_dct():
+    """C is orthonormal, row 0 constant 1/sqrt(8), and C s C^T of a cosine image has one nonzero
+    coefficient at (v, u) -- catches a transposed basis or a wrong normalisation; the integer basis
+    is within 1/2 of 2^12 C and keeps the antisymmetry that makes flat blocks DC-only."""
+    C = oracle.dct_basis()
+    assert np.allclose(C @ C.T, np.eye(8), atol=1e-14)
+    assert np.allclose(C[0], np.sqrt(1 / 8))
+    x = np.arange(8)
+    img = np.outer(np.cos((2 * x + 1) * 2 * np.pi / 16), np.cos((2 * x + 1) * 5 * np.pi / 16))  # v=2, u=5
+    D = C @ img @ C.T
+    assert abs(D[2, 5]) > 1 and np.sum(np.abs(D) > 1e-12) == 1
+    Ci = oracle.dct_basis_int()
+    assert np.all(np.abs(Ci - C * 4096) <= 0.5)
+    assert np.all(Ci[1:].sum(axis=1) == 0)
+
+
+def test_key_codec_flat_frame_dc_only():
+    """SPEC.md:293 flat gray frame -> DC coefficients only; decoded within 1 grey level."""
+    for c in (0, 37, 128, 200, 255):
+        f = np.full((16, 24), c, np.uint8)
+        for qs in (0.01, 1.0, 4.0):
+            q = oracle.intra_forward(f, oracle.key_qsteps(qs))
+            assert np.all(q[:, :, 0, 1:] == 0) and np.all(q[:, :, 1:, :] == 0)
+    f = np.full((16, 24), 77, np.uint8)
+    assert np.all(np.abs(oracle.decode_key(f, oracle.key_qsteps(0.01)).astype(int) - 77) <= 1)
+
+
+def test_key_codec_near_lossless_and_monotone():
+    """SPEC.md:301 minimum scale -> PSNR >= 45 dB; S:318 PSNR non-increasing in quant_scale over a
+    ladder; S:295 decoded dimensions == original (ragged frame, edge-replication padding)."""
+    cfg = synth.CONFIGS["C1"]
+    f = synth.gen_video(cfg)[0, 0]
+    ps = [_psnr(oracle.decode_key(f, oracle.key_qsteps(s)), f) for s in (0.01, 0.25, 0.5, 1, 2, 4, 8)]
+    assert ps[0] >= 45, ps
+    assert all(ps[i] >= ps[i + 1] - 1e-9 for i in range(len(ps) - 1)), ps
+    rag = f[:13, :21]
+    d = oracle.decode_key(rag, oracle.key_qsteps(1.0))
+    assert d.shape == rag.shape and _psnr(d, rag) > 25
+
+
+def test_key_codec_against_real_dct():
+    """The fixed-point forward transform rounds to the same code as the exact real DCT except
+    within the basis-rounding band (|t - k - 1/2| small), never by more than 1; the inverse of a
+    single coefficient is the textbook basis image (horizontal frequency u along x)."""
+    rng = np.random.default_rng(41)
+    C = oracle.dct_basis()
+    qs = oracle.key_qsteps(1.0)
+    n_diff = 0
+    for _ in range(200):
+        blk = rng.integers(0, 256, (8, 8)).astype(np.uint8)
+        q = oracle.intra_forward(blk, qs)[0, 0].astype(np.int64)
+        t = (C @ (blk.astype(np.float64) - 128) @ C.T) / qs
+        assert np.all(np.abs(q - np.sign(t) * np.floor(np.abs(t) + 0.5)) <= 1)
+        n_diff += int(np.sum(q != np.sign(t) * np.floor(np.abs(t) + 0.5)))
+    assert n_diff <= 200 * 64 * 0.01
+    coef = np.zeros((1, 1, 8, 8), np.int16)
+    coef[0, 0, 0, 1] = 40                       # v = 0, u = 1: varies along x only
+    img = oracle.intra_inverse(coef, np.ones((8, 8), np.int64) * 4, 8, 8).astype(np.int64)
+    assert np.all(img == img[0:1, :])           # every row identical
+    want = 128 + 160 * C[1][None, :] * C[0][:, None]
+    assert np.all(np.abs(img - want) <= 1)
+    assert img[0, 0] > img[0, 7]                # cos decreasing along x
+
+
+@pytest.mark.parametrize("qs", [0.3, 1.0, 5.0])
+def test_closed_loop_cancellation_eq4(qs):
+    """Eq. 4 / SPEC.md:371, 554: with M = N (Phi = I) the measurement IS the residual
+    against the decoded key, so y + F-hat_key reproduces every CS frame exactly, whatever the key
+    codec's error; and the closed-loop residual differs from the open-loop one by exactly the key's
+    coding error (Eq. 3)."""
+    B = 8
+    cfg = synth.CONFIGS["C1"].with_(T=5, G=5)
+    frames = synth.gen_video(cfg)[0]
+    qst = oracle.key_qsteps(qs)
+    eye = np.eye(B * B).astype(np.float16).view(np.uint16)
+    y, _ = oracle.encode_stream_closed_loop(frames, eye, 5, B, qst)
+    key_hat = oracle.decode_key(frames[0], qst)
+    for i in range(4):
+        rec = oracle.frame_unblocks(y[i], cfg.W, cfg.H, B) + key_hat.astype(np.float64)
+        assert np.array_equal(rec, frames[1 + i].astype(np.float64))
+    y_open, _ = oracle.encode_stream(frames, eye, 5, B)
+    err = key_hat.astype(np.int64) - frames[0].astype(np.int64)          # e_coding + e_decoding
+    diff = oracle.frame_unblocks(y_open[0] - y[0], cfg.W, cfg.H, B)
+    assert np.array_equal(diff, err.astype(np.float64))
