@@ -184,6 +184,39 @@ int cs_encode_batch_q16(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, i
  * more than 2^31 blocks in one call), CS_ERR_CUDA. */
 int cs_adjoint(cs_encoder* enc, const float* meas_dev, int64_t n_frames, float* x_dev, cs_stream_t stream);
 
+/* ---- closed-loop key frame --------------------------------------- */
+
+/* Eq. (2)-(3): the CS frames subtract the reconstructed key F-hat = decode(encode(F_key)),
+ * which cancels the key codec's error at the decoder (Eq. 4).  The key codec is SPEC's stand-in for
+ * H.264 intra: per 8x8 block (frame padded to multiples of 8 by edge
+ * replication) s = pixel - 128; fixed-point DCT with Ci = rint(4096 * C) (C the orthonormal DCT-II):
+ *   forward  t2 = Ci s Ci^T (exact), q = sign(t2) * floor((|t2| + qstep * 2^23) / (qstep * 2^24))
+ *   inverse  t1 = floor((q*qstep Ci + 2^11) / 2^12), t2 = Ci^T t1,
+ *            pixel = clamp(floor((t2 + 2^11) / 2^12) + 128, 0, 255)
+ * (R21).  Entropy coding and the CR-23 rate search are not part of this library. */
+
+/* Quantiser steps [v][u] = clamp(round_half_even(quant_scale * T.81 Table K.1), 1, 4096).  Host. */
+int cs_key_qsteps(double quant_scale, int32_t qsteps_out[64]);
+
+/* The fixed-point DCT basis Ci[u][x] the kernels use (diagnostics / tests).  Host. */
+void cs_key_dct_basis(int32_t basis_out[64]);
+
+/* Number of int16 coefficients cs_key_codec writes: n_seq * ceil(T/gop) * ceil(H/8) * ceil(W/8) * 64. */
+int64_t cs_key_coef_count(const cs_encoder* enc, int n_seq, int T);
+
+/* Code and decode every GOP key frame (frame g*gop of every stream) of frames_dev [n_seq][T][H][W]:
+ *   qsteps_host : HOST int32 [64], each in [1, 4096] (else CS_ERR_ARG);
+ *   coef_dev    : DEVICE int16 [n_seq][ceil(T/gop)][ceil(H/8)][ceil(W/8)][8 v][8 u] or NULL;
+ *   keys_dev    : DEVICE uint8 [n_seq][ceil(T/gop)][H][W], the decoded key frames F-hat.
+ * 16-byte aligned device buffers.  One asynchronous launch on `stream`. */
+int cs_key_codec(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, int T, const int32_t* qsteps_host,
+                 int16_t* coef_dev, uint8_t* keys_dev, cs_stream_t stream);
+
+/* cs_encode_batch with every CS frame's residual taken against keys_dev[s][g] (e.g. the decoded keys
+ * from cs_key_codec) instead of the raw key frame; same output layout and accuracy contract. */
+int cs_encode_batch_keys(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, int T, const uint8_t* keys_dev,
+                         float* meas_dev, cs_stream_t stream);
+
 /* ---- encode (HOST buffers; synchronous) ------------------------------------------------- */
 
 /* End-to-end call: frames_host = HOST [n_seq][T][H][W] uint8, meas_host = HOST fp32 output

@@ -67,6 +67,11 @@ def lib() -> ctypes.CDLL:
             "cs_encode_batch_q16": (c_int, [vp, vp, c_int, c_int, c_int, vp, vp, vp]),
             "cs_q16_scale_count": (c_i64, [vp, c_int, c_int, c_int]),
             "cs_adjoint": (c_int, [vp, vp, c_i64, vp, vp]),
+            "cs_key_qsteps": (c_int, [c_dbl, vp]),
+            "cs_key_dct_basis": (None, [vp]),
+            "cs_key_coef_count": (c_i64, [vp, c_int, c_int]),
+            "cs_key_codec": (c_int, [vp, vp, c_int, c_int, vp, vp, vp, vp]),
+            "cs_encode_batch_keys": (c_int, [vp, vp, c_int, c_int, vp, vp, vp]),
             "cs_measurement_count": (c_i64, [vp, c_int, c_int]),
             "cs_compression_ratio": (c_dbl, [vp, c_int, c_dbl, c_int]),
             "cs_compression_ratio_cfg": (c_dbl, [c_int, c_int, c_int, c_int, c_int, c_int, c_dbl, c_int]),
@@ -117,6 +122,19 @@ def plan_cfg(W, H, gop, B, M, smem_limit=232448, sms=148) -> dict:
     info = PlanInfo()
     _check(lib().cs_plan_cfg(W, H, gop, B, M, smem_limit, sms, ctypes.byref(info)))
     return info.as_dict()
+
+
+def key_qsteps(quant_scale: float) -> np.ndarray:
+    """cs_key_qsteps: int32 [8][8] quantiser steps of the key codec for a quant_scale."""
+    out = np.zeros(64, dtype=np.int32)
+    _check(lib().cs_key_qsteps(float(quant_scale), out.ctypes.data))
+    return out.reshape(8, 8)
+
+
+def key_dct_basis() -> np.ndarray:
+    out = np.zeros(64, dtype=np.int32)
+    lib().cs_key_dct_basis(out.ctypes.data)
+    return out.reshape(8, 8)
 
 
 def _ptr(t) -> int:
@@ -263,6 +281,45 @@ class Encoder:
         _check(lib().cs_encode_batch_q16(self._h, _ptr(frames), n_seq, T, granularity, _ptr(codes), _ptr(scales),
                                          _stream_handle(stream)))
         return codes, scales
+
+    # -- closed-loop key frame (f4; Eq. 2-3)
+    def n_gops(self, T: int) -> int:
+        return -(-T // self.G)
+
+    def key_codec(self, frames, qsteps, keys=None, coef=None, want_coef=True, stream=None):
+        """frames: CUDA uint8 [n_seq][T][H][W]; qsteps: int [8][8] (see key_qsteps).  Returns
+        (decoded keys uint8 [n_seq][ceil(T/G)][H][W], coefficients int16 [...][nby8][nbx8][8][8] or None)."""
+        import torch
+        assert frames.is_cuda and frames.dtype == torch.uint8 and frames.is_contiguous()
+        n_seq, T = frames.shape[:2]
+        ng = self.n_gops(T)
+        if keys is None:
+            keys = torch.empty((n_seq, ng, self.H, self.W), dtype=torch.uint8, device=frames.device)
+        if coef is None and want_coef:
+            coef = torch.empty((n_seq, ng, -(-self.H // 8), -(-self.W // 8), 8, 8), dtype=torch.int16,
+                               device=frames.device)
+        q = np.ascontiguousarray(qsteps, dtype=np.int32).ravel()
+        assert q.size == 64
+        _check(lib().cs_key_codec(self._h, _ptr(frames), n_seq, T, q.ctypes.data,
+                                  _ptr(coef) if coef is not None else None, _ptr(keys), _stream_handle(stream)))
+        return keys, coef
+
+    def encode_batch_keys(self, frames, keys, out=None, stream=None):
+        """cs_encode_batch with residuals against keys [n_seq][ceil(T/G)][H][W] (decoded key frames)."""
+        import torch
+        n_seq, T = frames.shape[:2]
+        assert keys.is_cuda and keys.dtype == torch.uint8 and keys.is_contiguous()
+        assert keys.shape == (n_seq, self.n_gops(T), self.H, self.W)
+        if out is None:
+            out = torch.empty(self.out_shape(n_seq, T), dtype=torch.float32, device=frames.device)
+        _check(lib().cs_encode_batch_keys(self._h, _ptr(frames), n_seq, T, _ptr(keys), _ptr(out),
+                                          _stream_handle(stream)))
+        return out
+
+    def encode_batch_closed_loop(self, frames, qsteps, out=None, stream=None):
+        """Eq. 2-3 closed loop: key codec (decoded keys) then the measurement against them (2 launches)."""
+        keys, coef = self.key_codec(frames, qsteps, stream=stream)
+        return self.encode_batch_keys(frames, keys, out, stream), keys, coef
 
     # -- adjoint / back-projection (f3; SPEC.md:145-153)
     def adjoint(self, meas, out=None, stream=None):

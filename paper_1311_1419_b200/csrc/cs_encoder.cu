@@ -18,6 +18,7 @@
 #include "../../include/cs_encoder.h"
 #include "cs_measure_kernel.cuh"
 #include "cs_adjoint_kernel.cuh"
+#include "cs_key_codec_kernel.cuh"
 
 using csenc::KParams;
 
@@ -352,6 +353,7 @@ namespace {
 
 // f1 epilogue arguments (qmode 0 = fp32 output)
 struct QArgs {
+    const uint8_t* keys = nullptr;   // f4: decoded key frames [n_seq][ceil(T/G)][H][W]
     int qmode = 0;
     int16_t* codes = nullptr;
     uint32_t* amax = nullptr;
@@ -424,6 +426,8 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.dbg_flags = env_int("CSENC_DBG_FLAGS", 0);
     kp.trace = e->trace;
     kp.trace_cap = e->trace_cap;
+    kp.keys = q.keys;
+    kp.n_gops_T = cdiv(T, g.G);
     kp.qmode = q.qmode;
     kp.codes = q.codes;
     kp.amax = q.amax;
@@ -846,6 +850,72 @@ int cs_encode_gop(cs_encoder* e, const uint8_t* frames, int n_frames, float* out
     if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
     if (n_frames < 1 || n_frames > e->geo.G) return fail(CS_ERR_ARG, "n_frames must be in [1, gop]");
     return cs_encode_batch_gops(e, frames, 1, n_frames, 0, 1, out, stream);
+}
+
+void cs_key_dct_basis(int32_t out[64]) {
+    for (int i = 0; i < 64; ++i) out[i] = csenc::kc::kDctHost[i];
+}
+
+int cs_key_qsteps(double quant_scale, int32_t out[64]) {
+    if (!out) return fail(CS_ERR_ARG, "out is NULL");
+    if (!(quant_scale > 0.0) || !std::isfinite(quant_scale)) return fail(CS_ERR_ARG, "quant_scale must be > 0");
+    for (int i = 0; i < 64; ++i) {
+        const double v = std::nearbyint(quant_scale * csenc::kc::kJpegLuma[i]);  // round half to even
+        out[i] = (int32_t)std::min(4096.0, std::max(1.0, v));
+    }
+    return CS_OK;
+}
+
+int64_t cs_key_coef_count(const cs_encoder* e, int n_seq, int T) {
+    if (!e || n_seq < 0 || T < 0) return -1;
+    const Geometry& g = e->geo;
+    return (int64_t)n_seq * cdiv(T, g.G) * cdiv(g.H, 8) * cdiv(g.W, 8) * 64;
+}
+
+int cs_key_codec(cs_encoder* e, const uint8_t* frames, int n_seq, int T, const int32_t* qsteps, int16_t* coef,
+                 uint8_t* keys, cs_stream_t stream) {
+    if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
+    if (n_seq < 0 || T < 0) return fail(CS_ERR_ARG, "n_seq and T must be >= 0");
+    if (n_seq == 0 || T == 0) return CS_OK;
+    if (!frames || !keys || !qsteps) return fail(CS_ERR_ARG, "NULL buffer");
+    if (!aligned16(frames) || !aligned16(keys) || (coef && !aligned16(coef)))
+        return fail(CS_ERR_ARG, "buffers must be 16-byte aligned");
+    const Geometry& g = e->geo;
+    csenc::kc::KCParams kp;
+    std::memset(&kp, 0, sizeof(kp));
+    for (int i = 0; i < 64; ++i) {
+        if (qsteps[i] < 1 || qsteps[i] > 4096) return fail(CS_ERR_ARG, "quantiser steps must be in [1, 4096]");
+        kp.qsteps[i] = qsteps[i];
+    }
+    kp.frames = frames;
+    kp.coef = coef;
+    kp.keys = keys;
+    kp.W = g.W;
+    kp.H = g.H;
+    kp.T = T;
+    kp.G = g.G;
+    kp.n_gops_T = cdiv(T, g.G);
+    kp.nbx8 = cdiv(g.W, 8);
+    kp.nby8 = cdiv(g.H, 8);
+    kp.n_blocks = (long long)n_seq * kp.n_gops_T * kp.nby8 * kp.nbx8;
+    const long long warps = (kp.n_blocks + 3) / 4;
+    const int grid = (int)std::max(1LL, std::min((long long)e->sms * 8, (warps + 7) / 8));
+    csenc::kc::cs_key_codec_kernel<<<grid, csenc::kc::kThreads, 0, (cudaStream_t)stream>>>(kp);
+    const cudaError_t err = cudaGetLastError();
+    return err == cudaSuccess ? CS_OK : cuda_fail(err, "key codec launch");
+}
+
+int cs_encode_batch_keys(cs_encoder* e, const uint8_t* frames, int n_seq, int T, const uint8_t* keys, float* out,
+                         cs_stream_t stream) {
+    if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
+    if (n_seq < 0 || T < 0) return fail(CS_ERR_ARG, "n_seq and T must be >= 0");
+    if (n_seq == 0 || T == 0 || cs_frames_per_stream(T, e->geo.G) == 0) return CS_OK;
+    if (!frames || !keys || !out) return fail(CS_ERR_ARG, "NULL buffer");
+    if (!aligned16(frames) || !aligned16(keys) || !aligned16(out)) return fail(CS_ERR_ARG, "buffers must be 16-byte aligned");
+    if ((long long)n_seq * T > 0x7FFFFFFFLL) return fail(CS_ERR_UNSUPPORTED, "too many frames");
+    QArgs q;
+    q.keys = keys;
+    return launch(e, frames, n_seq, T, 0, cdiv(T, e->geo.G), out, (cudaStream_t)stream, q);
 }
 
 int cs_adjoint(cs_encoder* e, const float* meas, int64_t n_frames, float* x, cs_stream_t stream) {

@@ -99,3 +99,14 @@ def test_plans_fit_b200_limits():
                  (64, 64, 2, 32, 80), (16, 16, 2, 16, 256), (3840, 2160, 8, 8, 4)]:
         p = P.plan_cfg(*args)
         assert p["smem_bytes"] <= 232448 and p["tmem_cols"] <= 512
+
+
+def test_key_codec_tables_match_oracle():
+    """The library's fixed-point DCT basis and quantiser steps (independent copies) equal the
+    oracle's definitions (R21), including round-half-even ties of quant_scale * table."""
+    import oracle
+    assert np.array_equal(P.key_dct_basis(), oracle.dct_basis_int())
+    for qs in (0.01, 0.5, 1.0, 1.5, 2.25, 7.0, 100.0, 1000.0):
+        assert np.array_equal(P.key_qsteps(qs), oracle.key_qsteps(qs)), qs
+    with pytest.raises(P.CSError):
+        P.key_qsteps(0.0)
