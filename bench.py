@@ -228,21 +228,37 @@ def run_ours(args, cfg, Ms):
         with open(args.tune_file, "w") as f:
             json.dump(tuned, f)
 
+    closed = args.op == "closed_loop"
+    if closed:   # f4: key codec once per step (keys do not depend on M), then every M against them
+        qsteps = P.key_qsteps(args.key_scale)
+        keys, coef = encs[0].key_codec(frames, qsteps, stream=stream)
+
     def launch(i):
+        if closed:
+            if i == 0:
+                encs[0].key_codec(frames, qsteps, keys=keys, coef=coef, stream=stream)
+                return
+            i -= 1
         e = encs[i]
-        if gran is None:
+        if closed:
+            e.encode_batch_keys(frames, keys, outs[i], stream)
+        elif gran is None:
             e.encode_batch(frames, outs[i], stream)
         else:
             e.encode_batch_q16(frames, gran, qouts[i][0], qouts[i][1], stream)
 
-    ms_total, launch_ms, clk = timed_steps(args, launch, len(Ms), stream, dev, world)
+    ms_total, launch_ms, clk = timed_steps(args, launch, len(Ms) + (1 if closed else 0), stream, dev, world)
     K = args.steps
+    key_ms = None
+    if closed:
+        key_ms = sum(launch_ms[0]) / K
+        launch_ms = launch_ms[1:]
 
     # ---- end to end through the public host-buffer C-ABI call (copies inside the timed region)
     e2e = None
-    if gran is not None:
+    if gran is not None or closed:
         e2e = {"value": None, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-               "how": "not measured: the host-buffer C-ABI call (cs_encode_batch_host) returns fp32 only"}
+               "how": "not measured: the host-buffer C-ABI call (cs_encode_batch_host) is the open-loop fp32 path"}
     elif not args.no_e2e:
         pin_in = torch.from_numpy(frames_h).pin_memory()
         pin_out = [torch.empty(o.shape, dtype=torch.float32).pin_memory() for o in outs]
@@ -296,7 +312,8 @@ def run_ours(args, cfg, Ms):
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u8 in, fp16 x fp16 -> fp32 (tensor core kind::f16)", "data": "synthetic (seeded surveillance-like video, synth/)",
         "config": {"workload": args.workload, "W": cfg.W, "H": cfg.H, "T": cfg.T, "streams_per_gpu": n_seq,
-                   "G": cfg.G, "B": cfg.B, "M": list(Ms), "output": args.output,
+                   "G": cfg.G, "B": cfg.B, "M": list(Ms), "output": args.output, "op": args.op,
+                   **({"key_quant_scale": args.key_scale, "key_codec_ms": key_ms} if closed else {}),
                    "l2": f"inputs larger than L2 ({in_mb:.0f} MiB read per launch vs 126 MiB L2); no flush",
                    "parallelism": f"dp{world} (independent sequences per GPU, no collective)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -306,7 +323,7 @@ def run_ours(args, cfg, Ms):
                                   "int16 codes + fp32 scales written once; q16frame runs two passes, so it reads "
                                   "the frames twice against this one-read algorithmic count)")},
         "per_M": per_m,
-        "gpu_launches": K * len(Ms) * (3 if args.output == "q16frame" else 1),
+        "gpu_launches": K * (len(Ms) * (3 if args.output == "q16frame" else 1) + (1 if closed else 0)),
         "clocks": clk.summary(),
         "e2e": e2e,
     }
@@ -505,8 +522,10 @@ def main(argv=None):
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-autotune", action="store_true")
     ap.add_argument("--tune-candidates", type=int, default=6)
-    ap.add_argument("--op", choices=["encode", "adjoint"], default="encode",
-                    help="encode (the north-star hot path, default) or adjoint (f3 back-projection)")
+    ap.add_argument("--op", choices=["encode", "adjoint", "closed_loop"], default="encode",
+                    help="encode (the north-star hot path, default), adjoint (f3 back-projection) or "
+                         "closed_loop (f4: key codec + encode against the decoded keys)")
+    ap.add_argument("--key-scale", type=float, default=1.0, help="closed_loop: key quantiser scale")
     ap.add_argument("--output", choices=list(OUTPUTS), default="f32",
                     help="f32 measurements (headline) or 16-bit codes (f1): per-frame or per-row scales")
     ap.add_argument("--tune-file", default=None, help="json of chosen plan indices (read if present, else written)")

@@ -190,7 +190,8 @@ int cs_adjoint(cs_encoder* enc, const float* meas_dev, int64_t n_frames, float* 
  * which cancels the key codec's error at the decoder (Eq. 4).  The key codec is SPEC's stand-in for
  * H.264 intra: per 8x8 block (frame padded to multiples of 8 by edge
  * replication) s = pixel - 128; fixed-point DCT with Ci = rint(4096 * C) (C the orthonormal DCT-II):
- *   forward  t2 = Ci s Ci^T (exact), q = sign(t2) * floor((|t2| + qstep * 2^23) / (qstep * 2^24))
+ *   forward  t1 = floor((s Ci^T + 2^4) / 2^5), t2 = Ci t1,
+ *            q = sign(t2) * floor((|t2| + qstep * 2^18) / (qstep * 2^19))
  *   inverse  t1 = floor((q*qstep Ci + 2^11) / 2^12), t2 = Ci^T t1,
  *            pixel = clamp(floor((t2 + 2^11) / 2^12) + 128, 0, 255)
  * (R21).  Entropy coding and the CR-23 rate search are not part of this library. */

@@ -297,18 +297,20 @@ def pad8(frame: np.ndarray) -> np.ndarray:
 
 
 def intra_forward(frame: np.ndarray, qsteps: np.ndarray) -> np.ndarray:
-    """Quantised DCT coefficients int16 [nby8][nbx8][8 (v)][8 (u)] of a uint8 frame.
-    Per 8x8 block s (level-shifted by -128): t1 = s Ci^T, t2 = Ci t1 (exact integers, scale 2^24);
-    q = round-half-away-from-zero(t2 / (qstep * 2^24)), clipped to int16."""
+    """Quantised DCT coefficients int16 [nby8][nbx8][8 (v)][8 (u)] of a uint8 frame (R21).
+    Per 8x8 block s (level-shifted by -128): t1 = s Ci^T (exact, |t1| < 2^21);
+    t1 = floor((t1 + 2^4) / 2^5); t2 = Ci t1 (exact, |t2| < 2^30; scale 2^19);
+    q = sign(t2) * floor((|t2| + qstep * 2^18) / (qstep * 2^19))  (round half away from zero)."""
     Ci = dct_basis_int()
     P = pad8(np.asarray(frame)).astype(np.int64) - 128
     nby, nbx = P.shape[0] // 8, P.shape[1] // 8
     out = np.empty((nby, nbx, 8, 8), dtype=np.int16)
-    d = np.asarray(qsteps, dtype=np.int64) << (2 * DCT_BITS)
+    d = np.asarray(qsteps, dtype=np.int64) << 19
     for by in range(nby):
         for bx in range(nbx):
             s = P[by * 8:(by + 1) * 8, bx * 8:(bx + 1) * 8]
-            t2 = Ci @ (s @ Ci.T)
+            t1 = (s @ Ci.T + 16) >> 5
+            t2 = Ci @ t1
             q = np.sign(t2) * ((np.abs(t2) + d // 2) // d)
             out[by, bx] = np.clip(q, -32768, 32767)
     return out

@@ -898,9 +898,13 @@ int cs_key_codec(cs_encoder* e, const uint8_t* frames, int n_seq, int T, const i
     kp.nbx8 = cdiv(g.W, 8);
     kp.nby8 = cdiv(g.H, 8);
     kp.n_blocks = (long long)n_seq * kp.n_gops_T * kp.nby8 * kp.nbx8;
-    const long long warps = (kp.n_blocks + 3) / 4;
-    const int grid = (int)std::max(1LL, std::min((long long)e->sms * 8, (warps + 7) / 8));
-    csenc::kc::cs_key_codec_kernel<<<grid, csenc::kc::kThreads, 0, (cudaStream_t)stream>>>(kp);
+    const long long n_keys = (long long)n_seq * kp.n_gops_T;
+    if (n_keys > 65535 || (long long)kp.nby8 * kp.nbx8 > 0x7FFFFFFFLL)
+        return fail(CS_ERR_UNSUPPORTED, "key codec: more than 65535 key frames in one call");
+    // ~12 CTAs per SM in total (3 resident: 4 waves of slack against imbalance), spread over the keys
+    const int per_key_ctas = (int)((kp.nby8 * (long long)kp.nbx8 + csenc::kc::kThreads / 8 - 1) / (csenc::kc::kThreads / 8));
+    const int gx = (int)std::max(1LL, std::min((long long)per_key_ctas, ((long long)e->sms * 12 + n_keys - 1) / n_keys));
+    csenc::kc::cs_key_codec_kernel<<<dim3(gx, (unsigned)n_keys), csenc::kc::kThreads, 0, (cudaStream_t)stream>>>(kp);
     const cudaError_t err = cudaGetLastError();
     return err == cudaSuccess ? CS_OK : cuda_fail(err, "key codec launch");
 }
