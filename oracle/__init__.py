@@ -32,6 +32,7 @@ Paper passages followed (PAPER.md line numbers, section):
                         (BASELINE.json:5); Table I closed form P:113-126
   f1 quantisation    -- SPEC.md:154-162 (scale = max|y|/32767, codes = round(y/scale)),
                         f32 scale SPEC.md:410; decision precision DESIGN.md R17-R18
+  f2 frame-level A   -- Eq.(1) P:83-85 with one dense A in R^{m x n}, n = W*H
   f3 adjoint         -- SPEC.md:145-153 (A^T v), TVAL3 start point x = A^T y SPEC.md:235;
                         per block x_b = Phi^T y_b reassembled into the frame (inverse of a2)
   f4 closed-loop key -- Eq.(2)-(3) P:87-91 with SPEC's 8x8 DCT intra codec as the
@@ -42,7 +43,7 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = [
-    "quantize", "dequantize", "quantize_frames", "frame_unblocks", "adjoint_blocks", "adjoint",
+    "measure_frame", "block_matrix_as_frame", "quantize", "dequantize", "quantize_frames", "frame_unblocks", "adjoint_blocks", "adjoint",
     "adjoint_tolerance_scale", "JPEG_LUMA", "dct_basis", "dct_basis_int", "key_qsteps", "pad8",
     "intra_forward", "intra_inverse", "decode_key", "encode_stream_closed_loop", "measure_entries", "gop_partition", "cs_frame_count", "block_grid", "frame_blocks", "residual", "measure",
     "tolerance_scale", "encode", "encode_stream", "phi_values", "compression_ratio", "total_cr",
@@ -217,6 +218,50 @@ def quantize_frames(y, group_blocks=None):
             for gi, (b0, b1) in enumerate(group_blocks):
                 codes[i, b0:b1], scales[i, gi] = quantize(y[i, b0:b1])
     return codes, scales
+
+
+# -- f2: paper-faithful frame-level measurement ---------------------------------------------------
+def measure_frame(frames: np.ndarray, A_bits: np.ndarray, G: int, with_scale: bool = True):
+    """Eq. (1) P:83-85 as the paper states it: one dense A (m x n, n = W*H) measures
+    the whole vectorised residual of every CS frame: y = A r, r = vec(F_cs - F_key) row-major
+    (SPEC.md:89).  frames uint8 [T][H][W] of one stream -> (y, S) fp64 [n_cs][m], CS frames in
+    GOP order (a1).  Exact in fp64 while max|A| * 255 * n < 2^29 (all terms multiples of 2^-24),
+    which the function checks."""
+    T, H, W = frames.shape
+    A = phi_values(A_bits)
+    m, n = A.shape
+    if n != W * H:
+        raise ValueError("A must have W*H columns")
+    if A.size and float(np.max(np.abs(A))) * 255.0 * n >= 2.0 ** 29:
+        raise ValueError("entries too large for the exact fp64 sum")
+    n_cs = cs_frame_count(T, G)
+    y = np.empty((n_cs, m))
+    S = np.empty((n_cs, m)) if with_scale else None
+    i = 0
+    for key_t, cs_ts in gop_partition(T, G):
+        for t in cs_ts:
+            r = residual(frames[t], frames[key_t]).reshape(-1).astype(np.float64)
+            y[i] = A @ r
+            if with_scale:
+                S[i] = np.abs(A) @ np.abs(r)
+            i += 1
+    return y, S
+
+
+def block_matrix_as_frame(phi_bits: np.ndarray, W: int, H: int, B: int) -> np.ndarray:
+    """The frame-level A (fp16 bits, [nblk*M][W*H]) that computes the block-based measurement: row
+    (b, i) holds Phi[i] at block b's pixels (inside the frame).  Used to tie f2 to a4."""
+    phi = np.asarray(phi_bits, dtype=np.uint16)
+    M = phi.shape[0]
+    nby, nbx = block_grid(W, H, B)
+    A = np.zeros((nby * nbx * M, H * W), dtype=np.uint16)
+    for b in range(nby * nbx):
+        by, bx = divmod(b, nbx)
+        for j in range(B * B):
+            Y, X = by * B + j // B, bx * B + j % B
+            if Y < H and X < W:
+                A[b * M:(b + 1) * M, Y * W + X] = phi[:, j]
+    return A
 
 
 # -- f3: adjoint / back-projection ---------------------------------------------------------------

@@ -504,3 +504,43 @@ def test_closed_loop_cancellation_eq4(qs):
     err = key_hat.astype(np.int64) - frames[0].astype(np.int64)          # e_coding + e_decoding
     diff = oracle.frame_unblocks(y_open[0] - y[0], cfg.W, cfg.H, B)
     assert np.array_equal(diff, err.astype(np.float64))
+
+
+# ---------------------------------------------------------------- f2: frame-level A (Eq. 1)
+def test_frame_level_reduces_to_block_path():
+    """A built from Phi block by block reproduces the block path's y exactly (reordered) -- ties
+    the frame-level measurement to a4 and catches a wrong vectorisation order (row-major
+    r = vec(F)) or a transposed A."""
+    B, M = 4, 3
+    H, W = 9, 14                                   # ragged: padded blocks outside the frame
+    phi = synth.phi_from_seed(12, M, B * B)
+    rng = np.random.default_rng(13)
+    frames = rng.integers(0, 256, (5, H, W), dtype=np.uint8)
+    A = oracle.block_matrix_as_frame(phi, W, H, B)
+    yf, Sf = oracle.measure_frame(frames, A, 5)
+    yb, Sb = oracle.encode_stream(frames, phi, 5, B)
+    assert np.array_equal(yf, yb.reshape(yb.shape[0], -1))
+    assert np.array_equal(Sf, Sb.reshape(Sb.shape[0], -1))
+
+
+def test_frame_level_special_cases():
+    """A = I (m = n): y is the residual itself; unit residual at pixel j -> v * A[:, j];
+    zero residual -> 0; the paper's QCIF CR-50 shape m = round(25344 / 50) = 507."""
+    H, W = 6, 8
+    n = H * W
+    eye = np.eye(n).astype(np.float16).view(np.uint16)
+    rng = np.random.default_rng(14)
+    fr = rng.integers(0, 256, (3, H, W), dtype=np.uint8)
+    y, _ = oracle.measure_frame(fr, eye, 3)
+    for i in range(2):
+        assert np.array_equal(y[i], (fr[1 + i].astype(float) - fr[0]).ravel())
+    A = synth.phi_from_seed(15, 10, n)
+    Av = oracle.phi_values(A)
+    for j in (0, 17, n - 1):
+        f = np.full((2, H, W), 100, np.uint8)
+        f[1].flat[j] = 37
+        y, _ = oracle.measure_frame(f, A, 2)
+        assert np.array_equal(y[0], -63 * Av[:, j])
+    y, S = oracle.measure_frame(np.repeat(fr[:1], 3, axis=0), A, 3)
+    assert np.all(y == 0) and np.all(S == 0)
+    assert round(176 * 144 / 50) == 507
