@@ -170,6 +170,33 @@ int64_t cs_q16_scale_count(const cs_encoder* enc, int n_seq, int T, int granular
 int cs_encode_batch_q16(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, int T, int granularity,
                         int16_t* codes_dev, float* scales_dev, cs_stream_t stream);
 
+/* ---- paper-faithful frame-level measurement ---------------------- */
+
+/* Eq. (1), as the paper states it: ONE dense measurement matrix A in R^{m x n}, n = W*H
+ * (SPEC.md:133-134), applied to the whole vectorised residual of every CS frame:
+ *     y[cs][i] = sum_{j < n} A[i][j] * (F_cs - F_key)[j / W][j % W]     (row-major vec)
+ * with the GOP structure and key reference of the block path (a1, a3).  A is fp16 (e.g. seeded
+ * N(0, 1/m), m = round(n / CR); QCIF at CR 50: m = 507); products are exact, accumulation is
+ * fp32 on the tensor cores (kind::f16 GEMM, 128 measurements x up to 256 CS frames per tile,
+ * split-K with a deterministic second-pass sum when the batch has fewer tiles than SMs).
+ * Accuracy contract: |y_gpu - y| <= (n/16 + 16) * 2^-23 * sum_j |A[i][j] r_j| (fp32 accumulation
+ * of n/16 tensor-core partial sums; R24). */
+typedef struct cs_frame_encoder cs_frame_encoder;
+
+/* A_fp16: HOST [m][W*H] fp16 bits, copied to the device (m*n*2 bytes).  W % 16 == 0; |A| <= 2048
+ * and finite (CS_ERR_PHI).  gop >= 1. */
+int cs_frame_encoder_create(int W, int H, int gop, int m, const uint16_t* A_fp16, cs_frame_encoder** out);
+int cs_frame_encoder_destroy(cs_frame_encoder* enc);
+
+/* n_seq * (CS frames per stream) * m; -1 on bad arguments. */
+int64_t cs_frame_measurement_count(const cs_frame_encoder* enc, int n_seq, int T);
+
+/* frames_dev = DEVICE uint8 [n_seq][T][H][W]; y_dev = DEVICE fp32 [n_seq * CS_s][m] (CS frames in
+ * the block path's order), both 16-byte aligned.  Asynchronous on `stream` (1 launch, or 2 with
+ * split-K, whose partials are stream-ordered allocations freed on the stream). */
+int cs_frame_encode_batch(cs_frame_encoder* enc, const uint8_t* frames_dev, int n_seq, int T, float* y_dev,
+                          cs_stream_t stream);
+
 /* ---- adjoint / back-projection ---------------------------------- */
 
 /* SPEC.md:145-153 adjoint(A, v) = A^T v, the decoder's start point x = A^T y, for the

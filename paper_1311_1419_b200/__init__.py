@@ -67,6 +67,10 @@ def lib() -> ctypes.CDLL:
             "cs_encode_batch_q16": (c_int, [vp, vp, c_int, c_int, c_int, vp, vp, vp]),
             "cs_q16_scale_count": (c_i64, [vp, c_int, c_int, c_int]),
             "cs_adjoint": (c_int, [vp, vp, c_i64, vp, vp]),
+            "cs_frame_encoder_create": (c_int, [c_int, c_int, c_int, c_int, vp, ctypes.POINTER(vp)]),
+            "cs_frame_encoder_destroy": (c_int, [vp]),
+            "cs_frame_measurement_count": (c_i64, [vp, c_int, c_int]),
+            "cs_frame_encode_batch": (c_int, [vp, vp, c_int, c_int, vp, vp]),
             "cs_key_qsteps": (c_int, [c_dbl, vp]),
             "cs_key_dct_basis": (None, [vp]),
             "cs_key_coef_count": (c_i64, [vp, c_int, c_int]),
@@ -345,4 +349,45 @@ class Encoder:
         fp = frames.ctypes.data if isinstance(frames, np.ndarray) else _ptr(frames)
         op = out.ctypes.data if isinstance(out, np.ndarray) else _ptr(out)
         _check(lib().cs_encode_batch_host(self._h, fp, n_seq, T, op))
+        return out
+
+
+class FrameEncoder:
+    """f2: paper-faithful frame-level measurement y = A vec(F_cs - F_key) (Eq. 1) with one
+    dense A: uint16 [m][W*H] fp16 bit patterns (host), copied to the device."""
+
+    def __init__(self, W: int, H: int, gop: int, m: int, A_bits):
+        A = np.ascontiguousarray(A_bits, dtype=np.uint16)
+        if A.shape != (m, W * H):
+            raise ValueError(f"A must have shape ({m}, {W * H}), got {A.shape}")
+        self.W, self.H, self.G, self.m = W, H, gop, m
+        h = ctypes.c_void_p()
+        _check(lib().cs_frame_encoder_create(W, H, gop, m, A.ctypes.data, ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().cs_frame_encoder_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def out_shape(self, n_seq: int, T: int):
+        return (n_seq * (T - -(-T // self.G)), self.m)
+
+    def encode_batch(self, frames, out=None, stream=None):
+        """frames: CUDA uint8 [n_seq][T][H][W]; returns CUDA float32 [n_cs][m]."""
+        import torch
+        assert frames.is_cuda and frames.dtype == torch.uint8 and frames.is_contiguous()
+        n_seq, T, H, W = frames.shape
+        assert (H, W) == (self.H, self.W)
+        if out is None:
+            out = torch.empty(self.out_shape(n_seq, T), dtype=torch.float32, device=frames.device)
+        assert out.is_cuda and out.dtype == torch.float32 and out.is_contiguous()
+        assert out.numel() >= lib().cs_frame_measurement_count(self._h, n_seq, T)
+        _check(lib().cs_frame_encode_batch(self._h, _ptr(frames), n_seq, T, _ptr(out), _stream_handle(stream)))
         return out
