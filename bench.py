@@ -414,6 +414,87 @@ def run_adjoint(args, cfg, Ms):
     return line
 
 
+# ------------------------------------------------------------------------- f2 frame-level op
+PAPER_F2 = dict(W=176, H=144, G=5, CR=50, S=64, T=400)   # QCIF, key + 4 CS frames, CS CR 50
+
+
+def run_frame(args):
+    """--op frame: the paper-faithful frame-level measurement y = A vec(F_cs - F_key) (Eq. 1) with
+    one dense A (m = round(W*H / 50) = 507), batched over 64 streams x 400 QCIF frames."""
+    import torch
+    import torch.distributed as dist
+    import paper_1311_1419_b200 as P
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    c = PAPER_F2
+    W, H, G, S, T = c["W"], c["H"], c["G"], c["S"], c["T"]
+    n = W * H
+    m = round(n / c["CR"])
+    cfg = synth.CONFIGS["C1"].with_(W=W, H=H, G=G, T=T, S=S)
+    frames = torch.from_numpy(synth.gen_video(cfg, streams=range(rank * S, (rank + 1) * S))).to(dev)
+    A = synth.phi_from_seed(synth.phi_seed(), m, n)
+    fe = P.FrameEncoder(W, H, G, m, A)
+    y = torch.empty(fe.out_shape(S, T), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def launch(i):
+        fe.encode_batch(frames, y, stream)
+
+    ms_total, launch_ms, clk = timed_steps(args, launch, 1, stream, dev, world)
+    K = args.steps
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return None
+    n_cs = y.shape[0]
+    avg = sum(launch_ms[0]) / K
+    flop = 2.0 * m * n * n_cs
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peak, peak_src = float(json.load(f)["bf16_tflops"]), "measured bf16 dense burst (MEASURED_PEAKS.json); fp16 rate = bf16 rate"
+    except Exception:
+        peak, peak_src = 2250.0, "fallback nominal dense fp16 (B200_PROFILING.md)"
+    achieved = flop / (avg * 1e-3) / 1e12
+    ms_step = ms_total / K
+    px = n_cs * n
+    line = {
+        "metric": "CS-frame Gpixels/s measured with one frame-level A (Eq. 1, m = n/50)",
+        "value": world * px / (ms_step * 1e-3) / 1e9, "unit": "Gpixel/s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8 in, fp16 x fp16 -> fp32 (tensor core kind::f16)",
+        "data": "synthetic (seeded surveillance-like video, synth/); A seeded N(0,1/m) fp16",
+        "config": {"workload": "paper-qcif-cr50", "op": "frame", "W": W, "H": H, "G": G, "m": m, "n": n,
+                   "streams_per_gpu": S, "T": T, "cs_frames": n_cs,
+                   "l2": f"frames {S * T * n / 2**20:.0f} MiB per launch (> 126 MiB L2); A {m * n * 2 / 2**20:.1f} MiB L2-resident",
+                   "parallelism": f"dp{world} (independent sequences per GPU, no collective)"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "traffic": None, "peak_source": peak_src,
+                     "kernel": "cs_frame_measure_kernel (algorithmic flop = 2 m n per CS frame)"},
+        "per_launch_ms": {"mean": avg, "median": statistics.median(launch_ms[0])},
+        "gpu_launches": K,
+        "clocks": clk.summary(),
+        "e2e": {"value": None, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                "how": "not measured: the frame-level path has a device-buffer C-ABI call only"},
+    }
+    if not args.no_cpu_baseline:
+        import oracle
+        fr = synth.gen_stream(cfg, 0, T=2 * G)
+        t0 = time.perf_counter()
+        oracle.measure_frame(fr, A, G, with_scale=False)
+        dt = time.perf_counter() - t0
+        ncs = oracle.cs_frame_count(2 * G, G)
+        line["cpu_baseline"] = {"value": ncs * n / dt / 1e9, "unit": "Gpixel/s", "cores": cpu_threads(),
+                                "kind": "oracle", "sample": f"fp64 numpy oracle measure_frame, {ncs} CS frames, {dt:.2f} s"}
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return line
+
+
 def adjoint_cpu_baseline(cfg, Ms, budget_s=15.0):
     """The oracle's adjoint (fp64 numpy) on CS frames of the workload's shape; frames added until
     about half the budget is spent."""
@@ -522,7 +603,7 @@ def main(argv=None):
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-autotune", action="store_true")
     ap.add_argument("--tune-candidates", type=int, default=6)
-    ap.add_argument("--op", choices=["encode", "adjoint", "closed_loop"], default="encode",
+    ap.add_argument("--op", choices=["encode", "adjoint", "closed_loop", "frame"], default="encode",
                     help="encode (the north-star hot path, default), adjoint (f3 back-projection) or "
                          "closed_loop (f4: key codec + encode against the decoded keys)")
     ap.add_argument("--key-scale", type=float, default=1.0, help="closed_loop: key quantiser scale")
@@ -538,6 +619,8 @@ def main(argv=None):
         return run_reference(args, cfg, Ms)
     if args.op == "adjoint":
         return run_adjoint(args, cfg, Ms)
+    if args.op == "frame":
+        return run_frame(args)
     return run_ours(args, cfg, Ms)
 
 

@@ -1030,7 +1030,7 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     {
         cuuint64_t dims[2] = {(cuuint64_t)f->n, (cuuint64_t)f->m};
         cuuint64_t strides[1] = {(cuuint64_t)f->n * 2u};
-        cuuint32_t box[2] = {(cuuint32_t)csenc::frm::kKc, 128u};
+        cuuint32_t box[2] = {(cuuint32_t)csenc::frm::kKc, 256u};
         cuuint32_t estr[2] = {1, 1};
         CUresult r = enc(&fp.amap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, f->A_dev, dims, strides, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1044,18 +1044,20 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     fp.cs_s = (int)cs_s;
     fp.n_win_s = cdiv(n_gops, fp.gw);
     fp.n_win = n_seq * fp.n_win_s;
-    fp.n_mt = cdiv(f->m, 128);
+    fp.n_mp = cdiv(f->m, 256);
     fp.n_chunks = cdiv(f->n, csenc::frm::kKc);
-    const long long tiles = (long long)fp.n_win * fp.n_mt;
+    const long long tiles = (long long)fp.n_win * fp.n_mp;
     long long ks = (f->sms + tiles - 1) / tiles;                   // K splits to fill the SMs
     ks = std::max(1LL, std::min(ks, (long long)std::max(1, fp.n_chunks / 8)));
+    // no empty K split (every unit must issue at least one chunk): ks = ceil(chunks / per-split)
+    const long long per_split = (fp.n_chunks + ks - 1) / ks;
+    ks = (fp.n_chunks + per_split - 1) / per_split;
     fp.n_ks = (int)ks;
     if (tiles * ks > 0x7FFFFFFFLL) return fail(CS_ERR_UNSUPPORTED, "too many work units");
     fp.n_units = (int)(tiles * ks);
     fp.fbox_bytes = (uint32_t)fp.nf_box * (uint32_t)csenc::frm::kKc;
     fp.off_a = align_up(fp.fbox_bytes, 1024);
-    fp.off_b = fp.off_a + 128u * csenc::frm::kKc * 2u;
-    fp.stage_bytes = fp.off_b + 256u * 128u;
+    fp.stage_bytes = fp.off_a + 256u * csenc::frm::kKc * 2u;
     const long avail = (long)f->smem_limit - 1024 - (long)csenc::frm::kOffStage;
     fp.n_stages = (int)std::min<long>(csenc::frm::kMaxStages, avail / (long)fp.stage_bytes);
     if (fp.n_stages < 2) return fail(CS_ERR_UNSUPPORTED, "frame measurement: stages do not fit shared memory");

@@ -6,15 +6,16 @@
 //   D[128 measurements x N CS frames] += A[128 x K] * R[N x K]^T
 // with K = n pixels: tensor-core bound (2 m n flop per frame against n bytes), unlike the block
 // path.  tcgen05.mma kind::f16 (fp16 x fp16 -> fp32), both operands from SMEM (SS form):
-//   A: TMA 2-D box [128 rows][64 fp16] of the device copy of A (SWIZZLE_128B = the UMMA K-major
+//   A: TMA 2-D box [256 rows][64 fp16] of the device copy of A (SWIZZLE_128B = the UMMA K-major
 //      SW128 layout); the copy's columns are permuted within groups of 4 pixels to the converters'
 //      (0,2,1,3) pair order (ptx::residual4), so K index k multiplies pixel 4(k/4)+{0,2,1,3}[k%4].
 //   R: TMA 2-D box [nf rows][64 bytes] of a window of whole GOPs (keys included, SWIZZLE_64B);
 //      4 converter warps form the exact fp16 residual of every CS frame of the window against its
 //      GOP key (same box) and write it as the SW128 K-major B operand.
-// Roles (10 warps): 0-3 converters, 4-7 epilogue, 8 TMA producer, 9 MMA issuer + TMEM allocator.
-// Unit = (K split, window of whole GOPs of one stream, 128-row m-tile); item = one 64-pixel K
-// chunk.  With more than one K split the units write fp32 partials that a second kernel sums in a
+// Roles (14 warps): 0-7 converters, 8-11 epilogue, 12 TMA producer, 13 MMA issuer + TMEM allocator.
+// Unit = (K split, window of whole GOPs of one stream, pair of 128-row m-tiles = one 256-row A box);
+// item = one 64-pixel K chunk: one residual operand feeds both m-tiles' MMAs (D uses all 512 TMEM
+// columns), halving the conversion work and the frame-box traffic per flop.  With more than one K split the units write fp32 partials that a second kernel sums in a
 // fixed order (deterministic).  The epilogue's lane = measurement, so for each CS frame a warp
 // stores 32 consecutive measurements (128 B).
 #pragma once
@@ -27,40 +28,42 @@
 namespace csenc {
 namespace frm {
 
-constexpr int kConvWarps = 4;
-constexpr int kEpiWarp0 = 4;
-constexpr int kProducerWarp = 8;
-constexpr int kMmaWarp = 9;
-constexpr int kThreads = 10 * 32;
-constexpr int kMaxStages = 6;
+constexpr int kConvWarps = 8;
+constexpr int kEpiWarp0 = 8;
+constexpr int kProducerWarp = 12;
+constexpr int kMmaWarp = 13;
+constexpr int kThreads = 14 * 32;
+constexpr int kMaxStages = 4;
 constexpr int kKc = 64;                          // pixels per K chunk
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kOffStage = 1024;
+constexpr uint32_t kOffB = 1024;                 // two residual (B operand) buffers of 32 KB
+constexpr uint32_t kBBytes = 256u * 128u;
+constexpr uint32_t kOffStage = kOffB + 2 * kBBytes;
 
 struct FParams {
     CUtensorMap fmap;         // frames: 2-D [n_seq*T rows][n bytes], box [nf_box][64], SWIZZLE_64B
-    CUtensorMap amap;         // A (permuted): 2-D [m rows][n fp16], box [128][64], SWIZZLE_128B
+    CUtensorMap amap;         // A (permuted): 2-D [m rows][n fp16], box [256][64], SWIZZLE_128B
     float* out;               // y [n_seq*cs_s][m] (n_ks == 1) or partials [n_ks][n_seq*cs_s][m]
     int n, m, G, T, cs_s;     // pixels, measurements, GOP, frames/stream, CS frames/stream
     int gw, nf_box;           // GOPs per window, frame rows per box (= gw * G)
     int n_win_s, n_win;       // windows per stream, all windows
-    int n_mt, n_ks, n_chunks; // m-tiles, K splits, 64-pixel chunks
+    int n_mp, n_ks, n_chunks; // 256-row m-pairs, K splits, 64-pixel chunks
     int n_units;
-    uint32_t fbox_bytes, off_a, off_b, stage_bytes;
+    uint32_t fbox_bytes, off_a, stage_bytes;
     int n_stages;
-    long long part_stride;    // floats per partial plane (n_seq * cs_s * m)
+    long long part_stride;    // floats per partial plane (n_seq * cs_s * m rounded up to 4)
 };
 
 struct FUnit {
-    int s, g0, ngops, n_cs, cs0, mt, kc0, kc1;
+    int s, g0, ngops, n_cs, cs0, mp, ks, kc0, kc1;
 };
 
 __device__ __forceinline__ void decode_funit(const FParams& p, int u, FUnit& w) {
-    // u = (ks * n_win + win) * n_mt + mt: CTAs running together share the K range and window
-    w.mt = u % p.n_mt;
-    const int r = u / p.n_mt;
+    // u = (ks * n_win + win) * n_mp + mp: CTAs running together share the K range and window
+    w.mp = u % p.n_mp;
+    const int r = u / p.n_mp;
     const int win = r % p.n_win;
-    const int ks = r / p.n_win;
+    w.ks = r / p.n_win;
     w.s = win / p.n_win_s;
     const int wi = win - w.s * p.n_win_s;
     w.g0 = wi * p.gw;
@@ -70,7 +73,7 @@ __device__ __forceinline__ void decode_funit(const FParams& p, int u, FUnit& w) 
     w.n_cs = (t_end - w.g0 * p.G) - w.ngops;            // frames in the window minus its keys
     w.cs0 = w.g0 * (p.G - 1);
     const int per = (p.n_chunks + p.n_ks - 1) / p.n_ks;
-    w.kc0 = ks * per;
+    w.kc0 = w.ks * per;
     w.kc1 = min(p.n_chunks, w.kc0 + per);
 }
 
@@ -80,23 +83,25 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31u;
 
-    const uint32_t bar_full = sbase;
-    const uint32_t bar_conv = sbase + 8 * kMaxStages;
-    const uint32_t bar_empty = sbase + 16 * kMaxStages;
-    const uint32_t bar_dfull = sbase + 24 * kMaxStages;
-    const uint32_t bar_dempty = bar_dfull + 16;
-    const uint32_t tmem_slot = bar_dempty + 16;
+    const uint32_t bar_full = sbase;                      // [kMaxStages] TMA -> converters, MMA
+    const uint32_t bar_empty = sbase + 8 * kMaxStages;    // [kMaxStages] MMA -> producer
+    const uint32_t bar_conv = sbase + 16 * kMaxStages;    // [2] converters -> MMA (B buffer written)
+    const uint32_t bar_bempty = bar_conv + 16;            // [2] MMA -> converters (B buffer free)
+    const uint32_t bar_dfull = bar_bempty + 16;
+    const uint32_t bar_dempty = bar_dfull + 8;
+    const uint32_t tmem_slot = bar_dempty + 8;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < p.n_stages; ++i) {
             ptx::mbar_init(bar_full + 8 * i, 1);
-            ptx::mbar_init(bar_conv + 8 * i, kConvWarps);
             ptx::mbar_init(bar_empty + 8 * i, 1);
         }
         for (int i = 0; i < 2; ++i) {
-            ptx::mbar_init(bar_dfull + 8 * i, 1);
-            ptx::mbar_init(bar_dempty + 8 * i, 4);
+            ptx::mbar_init(bar_conv + 8 * i, kConvWarps);
+            ptx::mbar_init(bar_bempty + 8 * i, 1);
         }
+        ptx::mbar_init(bar_dfull, 1);
+        ptx::mbar_init(bar_dempty, 4);
         ptx::fence_mbarrier_init();
     }
     if (warp == kMmaWarp) {
@@ -125,9 +130,9 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                 ptx::mbar_wait(bar_empty + 8 * st, ph ^ 1u);
                 if (lane == 0) {
                     const uint32_t sf = sbase + kOffStage + (uint32_t)st * p.stage_bytes;
-                    ptx::mbar_arrive_expect_tx(bar_full + 8 * st, p.fbox_bytes + 128u * kKc * 2u);
+                    ptx::mbar_arrive_expect_tx(bar_full + 8 * st, p.fbox_bytes + 256u * kKc * 2u);
                     ptx::tma_load_2d(sf, &p.fmap, bar_full + 8 * st, kc * kKc, row0);
-                    ptx::tma_load_2d(sf + p.off_a, &p.amap, bar_full + 8 * st, kc * kKc, w.mt * 128);
+                    ptx::tma_load_2d(sf + p.off_a, &p.amap, bar_full + 8 * st, kc * kKc, w.mp * 256);
                 }
                 __syncwarp();
                 if (++st == p.n_stages) {
@@ -138,29 +143,30 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         }
     } else if (warp < kConvWarps) {
         // ================================================================ residual -> B operand
-        // thread: 8-pixel group q = tid & 7 of CS rows c = tid/8 + 16 i (i < 16).  Row c of a window
+        // thread: 8-pixel group q = tid & 7 of CS rows c = tid/8 + 32 i (i < 8).  Row c of a window
         // is CS frame 1 + c % (G-1) of the window's GOP c / (G-1): frame row and key row packed.
         const int tid = (int)threadIdx.x;
         const int q = tid & 7;
-        uint32_t rows[16];
+        uint32_t rows[8];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const int c = (tid >> 3) + 16 * i;
+        for (int i = 0; i < 8; ++i) {
+            const int c = (tid >> 3) + 32 * i;
             const int gl = c / (p.G - 1), pos = c - gl * (p.G - 1);
             rows[i] = (uint32_t)(gl * p.G + 1 + pos) | ((uint32_t)(gl * p.G) << 16);
         }
-        int st = 0;
-        uint32_t ph = 0;
+        int st = 0, b = 0;
+        uint32_t ph = 0, bph = 0;
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             FUnit w;
             decode_funit(p, u, w);
             for (int kc = w.kc0; kc < w.kc1; ++kc) {
                 ptx::mbar_wait(bar_full + 8 * st, ph);
+                ptx::mbar_wait(bar_bempty + 8 * b, bph ^ 1u);
                 const uint32_t sf = sbase + kOffStage + (uint32_t)st * p.stage_bytes;
-                const uint32_t sb = sf + p.off_b;
+                const uint32_t sb = sbase + kOffB + (uint32_t)b * kBBytes;
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int c = (tid >> 3) + 16 * i;
+                for (int i = 0; i < 8; ++i) {
+                    const int c = (tid >> 3) + 32 * i;
                     if (c < w.n_cs) {
                         const uint32_t t = rows[i] & 0xFFFFu, k = rows[i] >> 16;
                         // SWIZZLE_64B box rows of 64 B: 16-B chunk (q/2) ^ ((row/2) & 3), 8-B half q & 1
@@ -176,85 +182,94 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                 }
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(bar_conv + 8 * st);
+                if (lane == 0) ptx::mbar_arrive(bar_conv + 8 * b);
                 if (++st == p.n_stages) {
                     st = 0;
                     ph ^= 1u;
+                }
+                if (++b == 2) {
+                    b = 0;
+                    bph ^= 1u;
                 }
             }
         }
     } else if (warp == kMmaWarp) {
         // ================================================================ MMA issuer
-        int st = 0;
-        uint32_t ph = 0;
-        int db = 0;
-        uint32_t dph = 0;
+        // D: m-tile 0 at TMEM columns [0, N), m-tile 1 at [256, 256 + N); single-buffered (a unit is
+        // hundreds of chunks long, the epilogue a few thousand cycles)
+        int st = 0, b = 0;
+        uint32_t ph = 0, bph = 0, dph = 0;
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             FUnit w;
             decode_funit(p, u, w);
             const uint32_t nmma = (uint32_t)((w.n_cs + 15) & ~15);
             const uint32_t idesc = (1u << 4) | ((nmma >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-            ptx::mbar_wait(bar_dempty + 8 * db, dph ^ 1u);
+            const bool two = (w.mp * 256 + 128) < p.m;          // second m-tile has rows
+            ptx::mbar_wait(bar_dempty, dph ^ 1u);
             ptx::tc_fence_after();
-            const uint32_t d_tm = tmem_base + (uint32_t)db * 256u;
             for (int kc = w.kc0; kc < w.kc1; ++kc) {
-                ptx::mbar_wait(bar_conv + 8 * st, ph);
+                ptx::mbar_wait(bar_full + 8 * st, ph);
+                ptx::mbar_wait(bar_conv + 8 * b, bph);
                 ptx::tc_fence_after();
                 if (lane == 0) {
-                    const uint32_t sf = sbase + kOffStage + (uint32_t)st * p.stage_bytes;
-                    const uint64_t ad = ptx::smem_desc_swizzled(sf + p.off_a, 128u, 1024u);
-                    const uint64_t bd = ptx::smem_desc_swizzled(sf + p.off_b, 128u, 1024u);
+                    const uint32_t sa = sbase + kOffStage + (uint32_t)st * p.stage_bytes + p.off_a;
+                    const uint64_t a0 = ptx::smem_desc_swizzled(sa, 128u, 1024u);
+                    const uint64_t a1 = ptx::smem_desc_swizzled(sa + 128u * 128u, 128u, 1024u);
+                    const uint64_t bd = ptx::smem_desc_swizzled(sbase + kOffB + (uint32_t)b * kBBytes, 128u, 1024u);
 #pragma unroll
-                    for (int ks = 0; ks < kKc / 16; ++ks)   // K = 16 per MMA: +32 B inside the SW128 rows
-                        ptx::mma_f16_ss(d_tm, ad + (uint64_t)(ks * 2), bd + (uint64_t)(ks * 2), idesc,
-                                        (kc != w.kc0 || ks != 0) ? 1u : 0u);
+                    for (int ks = 0; ks < kKc / 16; ++ks) {   // K = 16 per MMA: +32 B inside the SW128 rows
+                        const uint32_t acc = (kc != w.kc0 || ks != 0) ? 1u : 0u;
+                        ptx::mma_f16_ss(tmem_base, a0 + (uint64_t)(ks * 2), bd + (uint64_t)(ks * 2), idesc, acc);
+                        if (two)
+                            ptx::mma_f16_ss(tmem_base + 256u, a1 + (uint64_t)(ks * 2), bd + (uint64_t)(ks * 2), idesc, acc);
+                    }
                     ptx::tc_commit(bar_empty + 8 * st);
-                    if (kc == w.kc1 - 1) ptx::tc_commit(bar_dfull + 8 * db);
+                    ptx::tc_commit(bar_bempty + 8 * b);
+                    if (kc == w.kc1 - 1) ptx::tc_commit(bar_dfull);
                 }
                 __syncwarp();
                 if (++st == p.n_stages) {
                     st = 0;
                     ph ^= 1u;
                 }
+                if (++b == 2) {
+                    b = 0;
+                    bph ^= 1u;
+                }
             }
-            if (++db == 2) {
-                db = 0;
-                dph ^= 1u;
-            }
+            dph ^= 1u;
         }
     } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
         // ================================================================ epilogue
-        const int ew = warp - kEpiWarp0;
+        const int ew = warp - kEpiWarp0;   // == warp % 4: TMEM lanes 32 ew .. 32 ew + 31
         const uint32_t lane_bits = (uint32_t)(ew * 32) << 16;
-        int db = 0;
         uint32_t dph = 0;
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             FUnit w;
             decode_funit(p, u, w);
-            const int ks = u / (p.n_mt * p.n_win);
-            ptx::mbar_wait(bar_dfull + 8 * db, dph);
+            ptx::mbar_wait(bar_dfull, dph);
             ptx::tc_fence_after();
-            const uint32_t d_tm = tmem_base + lane_bits + (uint32_t)db * 256u;
-            const int i = w.mt * 128 + ew * 32 + (int)lane;       // measurement index of this lane
-            float* const dst0 = p.out + (long long)ks * p.part_stride +
-                                ((long long)w.s * p.cs_s + w.cs0) * p.m + i;
-            for (int j0 = 0; j0 < w.n_cs; j0 += 32) {
-                uint32_t v[32];
-                ptx::tmem_ld_32x32b_x32(d_tm + (uint32_t)j0, v);
-                ptx::tc_wait_ld();
-                if (i < p.m) {
+            for (int half = 0; half < 2; ++half) {
+                const int i = w.mp * 256 + half * 128 + ew * 32 + (int)lane;     // measurement index
+                if (w.mp * 256 + half * 128 >= p.m) break;                        // warp-uniform
+                float* const dst0 = p.out + (long long)w.ks * p.part_stride +
+                                    ((long long)w.s * p.cs_s + w.cs0) * p.m + i;
+                const uint32_t d_tm = tmem_base + lane_bits + (uint32_t)half * 256u;
+                for (int j0 = 0; j0 < w.n_cs; j0 += 32) {
+                    uint32_t v[32];
+                    ptx::tmem_ld_32x32b_x32(d_tm + (uint32_t)j0, v);
+                    ptx::tc_wait_ld();
+                    if (i < p.m) {
 #pragma unroll
-                    for (int k = 0; k < 32; ++k)
-                        if (j0 + k < w.n_cs) dst0[(long long)(j0 + k) * p.m] = __uint_as_float(v[k]);
+                        for (int k = 0; k < 32; ++k)
+                            if (j0 + k < w.n_cs) dst0[(long long)(j0 + k) * p.m] = __uint_as_float(v[k]);
+                    }
                 }
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(bar_dempty + 8 * db);
-            if (++db == 2) {
-                db = 0;
-                dph ^= 1u;
-            }
+            if (lane == 0) ptx::mbar_arrive(bar_dempty);
+            dph ^= 1u;
         }
     }
 
