@@ -1013,9 +1013,34 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     PFN_encodeTiled enc = get_encode_tiled();
     if (!enc) return fail(CS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     const int G = f->G;
-    fp.gw = std::max(1, 256 / G);
     const int n_gops = cdiv(T, G);
-    fp.gw = std::min(fp.gw, n_gops);
+    const int gw_max = std::max(1, 256 / G);          // box rows <= 256, CS rows <= 256
+    fp.n_mp = cdiv(f->m, 256);
+    if (T % G == 0) {
+        // whole GOPs everywhere: windows over the concatenation, sized so the units fill the SMs in
+        // whole waves (k units per SM, the smallest k whose windows fit a box)
+        fp.global_win = 1;
+        fp.total_gops = n_seq * n_gops;
+        fp.gw = std::min(gw_max, fp.total_gops);
+        for (int k = 1; k <= 16; ++k) {
+            const long long want = ((long long)k * f->sms + fp.n_mp - 1) / fp.n_mp;
+            const long long gw = (fp.total_gops + want - 1) / want;
+            if (gw <= gw_max) {
+                fp.gw = (int)std::max(1LL, gw);
+                break;
+            }
+        }
+        fp.n_win_s = 0;
+        fp.n_win = cdiv(fp.total_gops, fp.gw);
+    } else {
+        // windows inside each stream, balanced
+        fp.global_win = 0;
+        fp.total_gops = n_seq * n_gops;
+        fp.n_win_s = cdiv(n_gops, gw_max);
+        fp.gw = cdiv(n_gops, fp.n_win_s);
+        fp.n_win_s = cdiv(n_gops, fp.gw);
+        fp.n_win = n_seq * fp.n_win_s;
+    }
     fp.nf_box = fp.gw * G;
     {
         cuuint64_t dims[2] = {(cuuint64_t)f->n, (cuuint64_t)n_seq * T};
@@ -1042,9 +1067,7 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     fp.G = G;
     fp.T = T;
     fp.cs_s = (int)cs_s;
-    fp.n_win_s = cdiv(n_gops, fp.gw);
-    fp.n_win = n_seq * fp.n_win_s;
-    fp.n_mp = cdiv(f->m, 256);
+
     fp.n_chunks = cdiv(f->n, csenc::frm::kKc);
     const long long tiles = (long long)fp.n_win * fp.n_mp;
     long long ks = (f->sms + tiles - 1) / tiles;                   // K splits to fill the SMs
@@ -1058,10 +1081,12 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     fp.fbox_bytes = (uint32_t)fp.nf_box * (uint32_t)csenc::frm::kKc;
     fp.off_a = align_up(fp.fbox_bytes, 1024);
     fp.stage_bytes = fp.off_a + 256u * csenc::frm::kKc * 2u;
-    const long avail = (long)f->smem_limit - 1024 - (long)csenc::frm::kOffStage;
+    fp.b_bytes = align_up((uint32_t)(fp.gw * (G - 1) + 15) / 16 * 16 * 128u, 1024);
+    fp.off_stage = csenc::frm::kOffB + 2 * fp.b_bytes;
+    const long avail = (long)f->smem_limit - 1024 - (long)fp.off_stage;
     fp.n_stages = (int)std::min<long>(csenc::frm::kMaxStages, avail / (long)fp.stage_bytes);
     if (fp.n_stages < 2) return fail(CS_ERR_UNSUPPORTED, "frame measurement: stages do not fit shared memory");
-    const uint32_t smem = 1024 + csenc::frm::kOffStage + (uint32_t)fp.n_stages * fp.stage_bytes;
+    const uint32_t smem = 1024 + fp.off_stage + (uint32_t)fp.n_stages * fp.stage_bytes;
     const long long ny = (long long)n_seq * cs_s * f->m;
     float* part = nullptr;
     cudaError_t err;

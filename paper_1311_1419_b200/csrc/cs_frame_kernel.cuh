@@ -33,12 +33,10 @@ constexpr int kEpiWarp0 = 8;
 constexpr int kProducerWarp = 12;
 constexpr int kMmaWarp = 13;
 constexpr int kThreads = 14 * 32;
-constexpr int kMaxStages = 4;
+constexpr int kMaxStages = 8;
 constexpr int kKc = 64;                          // pixels per K chunk
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kOffB = 1024;                 // two residual (B operand) buffers of 32 KB
-constexpr uint32_t kBBytes = 256u * 128u;
-constexpr uint32_t kOffStage = kOffB + 2 * kBBytes;
+constexpr uint32_t kOffB = 1024;                 // two residual (B operand) buffers of b_bytes
 
 struct FParams {
     CUtensorMap fmap;         // frames: 2-D [n_seq*T rows][n bytes], box [nf_box][64], SWIZZLE_64B
@@ -47,9 +45,13 @@ struct FParams {
     int n, m, G, T, cs_s;     // pixels, measurements, GOP, frames/stream, CS frames/stream
     int gw, nf_box;           // GOPs per window, frame rows per box (= gw * G)
     int n_win_s, n_win;       // windows per stream, all windows
+    int global_win;           // T % G == 0: windows run over the concatenated GOPs of all streams
+    int total_gops;           // n_seq * T / G (global_win)
     int n_mp, n_ks, n_chunks; // 256-row m-pairs, K splits, 64-pixel chunks
     int n_units;
     uint32_t fbox_bytes, off_a, stage_bytes;
+    uint32_t b_bytes;         // one residual buffer: roundup(window CS rows * 128, 1024)
+    uint32_t off_stage;       // kOffB + 2 * b_bytes
     int n_stages;
     long long part_stride;    // floats per partial plane (n_seq * cs_s * m rounded up to 4)
 };
@@ -64,13 +66,22 @@ __device__ __forceinline__ void decode_funit(const FParams& p, int u, FUnit& w) 
     const int r = u / p.n_mp;
     const int win = r % p.n_win;
     w.ks = r / p.n_win;
-    w.s = win / p.n_win_s;
-    const int wi = win - w.s * p.n_win_s;
-    w.g0 = wi * p.gw;
-    const int n_gops = (p.T + p.G - 1) / p.G;
-    w.ngops = min(p.gw, n_gops - w.g0);
-    const int t_end = min(p.T, (w.g0 + w.ngops) * p.G);
-    w.n_cs = (t_end - w.g0 * p.G) - w.ngops;            // frames in the window minus its keys
+    if (p.global_win) {
+        // every stream is whole GOPs: GOP gg of the concatenation starts at frame row gg * G and
+        // its CS frames are global CS rows gg * (G-1) ... (stream offsets included)
+        w.s = 0;
+        w.g0 = win * p.gw;
+        w.ngops = min(p.gw, p.total_gops - w.g0);
+        w.n_cs = w.ngops * (p.G - 1);
+    } else {
+        w.s = win / p.n_win_s;
+        const int wi = win - w.s * p.n_win_s;
+        w.g0 = wi * p.gw;
+        const int n_gops = (p.T + p.G - 1) / p.G;
+        w.ngops = min(p.gw, n_gops - w.g0);
+        const int t_end = min(p.T, (w.g0 + w.ngops) * p.G);
+        w.n_cs = (t_end - w.g0 * p.G) - w.ngops;        // frames in the window minus its keys
+    }
     w.cs0 = w.g0 * (p.G - 1);
     const int per = (p.n_chunks + p.n_ks - 1) / p.n_ks;
     w.kc0 = w.ks * per;
@@ -129,7 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
             for (int kc = w.kc0; kc < w.kc1; ++kc) {
                 ptx::mbar_wait(bar_empty + 8 * st, ph ^ 1u);
                 if (lane == 0) {
-                    const uint32_t sf = sbase + kOffStage + (uint32_t)st * p.stage_bytes;
+                    const uint32_t sf = sbase + p.off_stage + (uint32_t)st * p.stage_bytes;
                     ptx::mbar_arrive_expect_tx(bar_full + 8 * st, p.fbox_bytes + 256u * kKc * 2u);
                     ptx::tma_load_2d(sf, &p.fmap, bar_full + 8 * st, kc * kKc, row0);
                     ptx::tma_load_2d(sf + p.off_a, &p.amap, bar_full + 8 * st, kc * kKc, w.mp * 256);
@@ -162,8 +173,8 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
             for (int kc = w.kc0; kc < w.kc1; ++kc) {
                 ptx::mbar_wait(bar_full + 8 * st, ph);
                 ptx::mbar_wait(bar_bempty + 8 * b, bph ^ 1u);
-                const uint32_t sf = sbase + kOffStage + (uint32_t)st * p.stage_bytes;
-                const uint32_t sb = sbase + kOffB + (uint32_t)b * kBBytes;
+                const uint32_t sf = sbase + p.off_stage + (uint32_t)st * p.stage_bytes;
+                const uint32_t sb = sbase + kOffB + (uint32_t)b * p.b_bytes;
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     const int c = (tid >> 3) + 32 * i;
@@ -212,10 +223,10 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                 ptx::mbar_wait(bar_conv + 8 * b, bph);
                 ptx::tc_fence_after();
                 if (lane == 0) {
-                    const uint32_t sa = sbase + kOffStage + (uint32_t)st * p.stage_bytes + p.off_a;
+                    const uint32_t sa = sbase + p.off_stage + (uint32_t)st * p.stage_bytes + p.off_a;
                     const uint64_t a0 = ptx::smem_desc_swizzled(sa, 128u, 1024u);
                     const uint64_t a1 = ptx::smem_desc_swizzled(sa + 128u * 128u, 128u, 1024u);
-                    const uint64_t bd = ptx::smem_desc_swizzled(sbase + kOffB + (uint32_t)b * kBBytes, 128u, 1024u);
+                    const uint64_t bd = ptx::smem_desc_swizzled(sbase + kOffB + (uint32_t)b * p.b_bytes, 128u, 1024u);
 #pragma unroll
                     for (int ks = 0; ks < kKc / 16; ++ks) {   // K = 16 per MMA: +32 B inside the SW128 rows
                         const uint32_t acc = (kc != w.kc0 || ks != 0) ? 1u : 0u;

@@ -34,7 +34,8 @@ def check(y_gpu, y, S, n):
 
 
 @pytest.mark.parametrize("W,H,G,T,S,m", [(32, 16, 3, 7, 2, 37), (48, 20, 2, 9, 1, 130), (64, 8, 5, 23, 3, 256),
-                                          (16, 16, 8, 17, 2, 5), (176, 144, 5, 10, 2, 507)])
+                                          (16, 16, 8, 17, 2, 5), (176, 144, 5, 10, 2, 507),
+                                          (32, 16, 4, 8, 5, 300), (96, 32, 3, 300, 3, 64)])
 def test_frame_parity(W, H, G, T, S, m):
     cfg = synth.CONFIGS["C1"].with_(W=W, H=H, G=G, T=T, S=S)
     frames = synth.gen_video(cfg)
