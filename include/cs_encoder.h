@@ -245,6 +245,13 @@ int cs_key_codec(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, int T, c
 int cs_encode_batch_keys(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, int T, const uint8_t* keys_dev,
                          float* meas_dev, cs_stream_t stream);
 
+/* Variant (Eq. (3) P:91 read literally): every CS frame's residual is taken
+ * against the PREVIOUS raw frame, D_t = F_t - F_{t-1} (open loop; the GOP structure still decides
+ * which frames are keys and are not measured).  Same output layout and accuracy contract as
+ * cs_encode_batch; runs the planner's best streamed-key plan (CS_ERR_UNSUPPORTED if none fits). */
+int cs_encode_batch_chained(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, int T, float* meas_dev,
+                            cs_stream_t stream);
+
 /* ---- encode (HOST buffers; synchronous) ------------------------------------------------- */
 
 /* End-to-end call: frames_host = HOST [n_seq][T][H][W] uint8, meas_host = HOST fp32 output

@@ -76,6 +76,7 @@ def lib() -> ctypes.CDLL:
             "cs_key_coef_count": (c_i64, [vp, c_int, c_int]),
             "cs_key_codec": (c_int, [vp, vp, c_int, c_int, vp, vp, vp, vp]),
             "cs_encode_batch_keys": (c_int, [vp, vp, c_int, c_int, vp, vp, vp]),
+            "cs_encode_batch_chained": (c_int, [vp, vp, c_int, c_int, vp, vp]),
             "cs_measurement_count": (c_i64, [vp, c_int, c_int]),
             "cs_compression_ratio": (c_dbl, [vp, c_int, c_dbl, c_int]),
             "cs_compression_ratio_cfg": (c_dbl, [c_int, c_int, c_int, c_int, c_int, c_int, c_dbl, c_int]),
@@ -318,6 +319,15 @@ class Encoder:
             out = torch.empty(self.out_shape(n_seq, T), dtype=torch.float32, device=frames.device)
         _check(lib().cs_encode_batch_keys(self._h, _ptr(frames), n_seq, T, _ptr(keys), _ptr(out),
                                           _stream_handle(stream)))
+        return out
+
+    def encode_batch_chained(self, frames, out=None, stream=None):
+        """Eq. 3 literal variant: residual of every CS frame against the previous raw frame."""
+        import torch
+        n_seq, T = frames.shape[:2]
+        if out is None:
+            out = torch.empty(self.out_shape(n_seq, T), dtype=torch.float32, device=frames.device)
+        _check(lib().cs_encode_batch_chained(self._h, _ptr(frames), n_seq, T, _ptr(out), _stream_handle(stream)))
         return out
 
     def encode_batch_closed_loop(self, frames, qsteps, out=None, stream=None):

@@ -338,6 +338,7 @@ struct cs_encoder {
     size_t ws_frames_bytes = 0, ws_out_bytes = 0;
     cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
     std::vector<Plan> candidates;  // planner's ranked plans (autotune)
+    int chained_plan = -1;         // best KEY_STREAMED candidate (previous-frame reference), -1 = none
     int tuned = -1;                // index of the autotuned plan, -1 = model choice
     void* zeros_dev = nullptr;   // piece_rows * W zero bytes: source for frame rows beyond H
     size_t zeros_bytes = 0;
@@ -362,6 +363,8 @@ namespace {
 // f1 epilogue arguments (qmode 0 = fp32 output)
 struct QArgs {
     const uint8_t* keys = nullptr;   // f4: decoded key frames [n_seq][ceil(T/G)][H][W]
+    int chained = 0;                 // f4 variant: previous-frame reference (needs a KEY_STREAMED plan)
+    const Plan* plan = nullptr;      // plan override (default e->plan)
     int qmode = 0;
     int16_t* codes = nullptr;
     uint32_t* amax = nullptr;
@@ -371,7 +374,7 @@ struct QArgs {
 int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g1, float* out, cudaStream_t stream,
            const QArgs& q = QArgs()) {
     const Geometry& g = e->geo;
-    const Plan& pl = e->plan;
+    const Plan& pl = q.plan ? *q.plan : e->plan;
     if (g1 <= g0 || g.G == 1) return CS_OK;
     if (cs_frames_in_gops(T, g.G, g0, g1) == 0) return CS_OK;
     KParams kp;
@@ -435,6 +438,7 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.trace = e->trace;
     kp.trace_cap = e->trace_cap;
     kp.keys = q.keys;
+    kp.chained = q.chained;
     kp.n_gops_T = cdiv(T, g.G);
     kp.qmode = q.qmode;
     kp.codes = q.codes;
@@ -653,6 +657,11 @@ int cs_encoder_create(int W, int H, int gop, int B, int M, const uint16_t* phi_f
     cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, e->device);
     cudaDeviceGetAttribute(&e->smem_limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device);
     e->candidates = plan_candidates(e->geo, e->smem_limit);
+    for (size_t i = 0; i < e->candidates.size(); ++i)
+        if (!e->candidates[i].key_resident && !e->candidates[i].key_regs) {
+            e->chained_plan = (int)i;
+            break;
+        }
     if (!make_plan(e->geo, e->smem_limit, e->plan)) {
         delete e;
         return fail(CS_ERR_UNSUPPORTED, "no tiling fits shared memory / TMEM for this configuration");
@@ -915,6 +924,20 @@ int cs_key_codec(cs_encoder* e, const uint8_t* frames, int n_seq, int T, const i
     csenc::kc::cs_key_codec_kernel<<<dim3(gx, (unsigned)n_keys), csenc::kc::kThreads, 0, (cudaStream_t)stream>>>(kp);
     const cudaError_t err = cudaGetLastError();
     return err == cudaSuccess ? CS_OK : cuda_fail(err, "key codec launch");
+}
+
+int cs_encode_batch_chained(cs_encoder* e, const uint8_t* frames, int n_seq, int T, float* out, cs_stream_t stream) {
+    if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
+    if (n_seq < 0 || T < 0) return fail(CS_ERR_ARG, "n_seq and T must be >= 0");
+    if (n_seq == 0 || T == 0 || cs_frames_per_stream(T, e->geo.G) == 0) return CS_OK;
+    if (!frames || !out) return fail(CS_ERR_ARG, "NULL buffer");
+    if (!aligned16(frames) || !aligned16(out)) return fail(CS_ERR_ARG, "buffers must be 16-byte aligned");
+    if ((long long)n_seq * T > 0x7FFFFFFFLL) return fail(CS_ERR_UNSUPPORTED, "too many frames");
+    if (e->chained_plan < 0) return fail(CS_ERR_UNSUPPORTED, "no streamed-key plan fits this configuration");
+    QArgs q;
+    q.chained = 1;
+    q.plan = &e->candidates[(size_t)e->chained_plan];
+    return launch(e, frames, n_seq, T, 0, cdiv(T, e->geo.G), out, (cudaStream_t)stream, q);
 }
 
 int cs_encode_batch_keys(cs_encoder* e, const uint8_t* frames, int n_seq, int T, const uint8_t* keys, float* out,

@@ -117,6 +117,9 @@ struct KParams {
     // `frames`, the north star's pass-through); n_gops_T = ceil(T / G)
     const uint8_t* keys;
     int n_gops_T;
+    // f4 variant (KM == KEY_STREAMED plans only): every CS frame's reference is the previous raw
+    // frame (Eq. 3 read literally: D_N = F_N - F_{N-1}) instead of the GOP key
+    int chained;
     // EPI_Q16 (f1)
     int qmode;                // QMode
     int16_t* codes;           // [n_cs][nblk][M] int16, same layout as out
@@ -502,8 +505,9 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                         ptx::mbar_arrive_expect_tx(bar_stage_full + 8 * st,
                                                    (KM == KEY_STREAMED ? 2u : 1u) * p.set_bytes);
                         load_strips<B>(p, dst, cs_f, w.t, k, bar_stage_full + 8 * st, pol_stream);
-                        if constexpr (KM == KEY_STREAMED)
-                            load_strips<B>(p, dst + p.stage_cs_bytes, key_f, w.t, k, bar_stage_full + 8 * st, pol_key);
+                        if constexpr (KM == KEY_STREAMED)   // chained (Eq. 3 literal): reference = previous frame
+                            load_strips<B>(p, dst + p.stage_cs_bytes, p.chained ? cs_f - frame_bytes : key_f, w.t, k,
+                                           bar_stage_full + 8 * st, pol_key);
                     }
                     __syncwarp();
                     if (lane == 0) trace_ev(p, EV_P_ISSUED, n_items);

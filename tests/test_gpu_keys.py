@@ -129,3 +129,22 @@ def test_key_codec_args():
     assert P.lib().cs_key_codec(enc._h, fd.data_ptr(), 1, 4, good.ctypes.data, None, keys.data_ptr(), None) == P.CS_OK
     torch.cuda.synchronize()
     assert int(keys.max()) == int(keys.min())          # all-zero frame decodes to a flat frame
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_chained_reference_parity(name):
+    """f4 variant, Eq. 3 literal: every CS frame against the previous raw frame."""
+    base = synth.CONFIGS[name]
+    cfg = base.with_(T=min(base.T, 2 * base.G + 3), S=min(base.S, 2))
+    frames = synth.gen_video(cfg)
+    M = base.Ms[-1]
+    phi = synth.phi_from_seed(synth.phi_seed(), M, cfg.B ** 2)
+    enc = P.Encoder(cfg.W, cfg.H, cfg.G, cfg.B, M, phi)
+    y_gpu = enc.encode_batch_chained(torch.from_numpy(frames).cuda())
+    torch.cuda.synchronize()
+    y_gpu = y_gpu.cpu().numpy()
+    n_cs = oracle.cs_frame_count(cfg.T, cfg.G)
+    for s in range(cfg.S):
+        y, S = oracle.encode_stream_chained(frames[s], phi, cfg.G, cfg.B)
+        ok, st = oracle.check_tolerance(y_gpu[s * n_cs:(s + 1) * n_cs], y, S, REL)
+        assert ok, st

@@ -544,3 +544,20 @@ def test_frame_level_special_cases():
     y, S = oracle.measure_frame(np.repeat(fr[:1], 3, axis=0), A, 3)
     assert np.all(y == 0) and np.all(S == 0)
     assert round(176 * 144 / 50) == 507
+
+
+def test_chained_reference_variant():
+    """Eq. 3 literal (D_N = F_N - F_{N-1}): the first CS frame of a GOP equals the key-referenced
+    residual; with Phi = I the chained measurements telescope -- their running sum over a GOP is
+    the key-referenced measurement (exact)."""
+    B = 4
+    rng = np.random.default_rng(51)
+    frames = rng.integers(0, 256, (9, 8, 12), dtype=np.uint8)
+    eye = np.eye(B * B).astype(np.float16).view(np.uint16)
+    yc, _ = oracle.encode_stream_chained(frames, eye, 4, B)
+    yk, _ = oracle.encode_stream(frames, eye, 4, B)
+    order = [(k, t) for k, cs in oracle.gop_partition(9, 4) for t in cs]
+    run = None
+    for i, (k, t) in enumerate(order):
+        run = yc[i] if t == k + 1 else run + yc[i]
+        assert np.array_equal(run, yk[i]), (i, k, t)
