@@ -252,6 +252,14 @@ int cs_encode_batch_keys(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, 
 int cs_encode_batch_chained(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, int T, float* meas_dev,
                             cs_stream_t stream);
 
+/* Variant ("per-GOP seeds are derivable (seed xor GOP index)"):
+ * after this call every encode of `enc` measures GOP g of each stream (g = GOP index within the
+ * stream) with phis[g % n_phi] instead of the create-time Phi.  phis: HOST, n_phi matrices of
+ * [M][B*B] fp16 bits (each validated like cs_encoder_create's Phi; copied).  n_phi = 0 restores the
+ * single Phi.  The resident Phi is reloaded into shared memory whenever a CTA's next unit belongs
+ * to a GOP with a different matrix.  Host; not safe concurrently with encodes of `enc`. */
+int cs_encoder_set_gop_phis(cs_encoder* enc, int n_phi, const uint16_t* phis);
+
 /* ---- encode (HOST buffers; synchronous) ------------------------------------------------- */
 
 /* End-to-end call: frames_host = HOST [n_seq][T][H][W] uint8, meas_host = HOST fp32 output

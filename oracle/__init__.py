@@ -45,7 +45,7 @@ import numpy as np
 __all__ = [
     "measure_frame", "block_matrix_as_frame", "quantize", "dequantize", "quantize_frames", "frame_unblocks", "adjoint_blocks", "adjoint",
     "adjoint_tolerance_scale", "JPEG_LUMA", "dct_basis", "dct_basis_int", "key_qsteps", "pad8",
-    "intra_forward", "intra_inverse", "decode_key", "encode_stream_closed_loop", "encode_stream_chained", "measure_entries", "gop_partition", "cs_frame_count", "block_grid", "frame_blocks", "residual", "measure",
+    "intra_forward", "intra_inverse", "decode_key", "encode_stream_closed_loop", "encode_stream_chained", "encode_stream_gop_phis", "measure_entries", "gop_partition", "cs_frame_count", "block_grid", "frame_blocks", "residual", "measure",
     "tolerance_scale", "encode", "encode_stream", "phi_values", "compression_ratio", "total_cr",
     "check_tolerance",
 ]
@@ -394,6 +394,27 @@ def encode_stream_closed_loop(frames: np.ndarray, phi_bits: np.ndarray, G: int, 
     for key_t, _ in gop_partition(frames.shape[0], G):
         frames[key_t] = decode_key(frames[key_t], qsteps)
     return encode_stream(frames, phi_bits, G, B, with_scale)
+
+
+def encode_stream_gop_phis(frames: np.ndarray, phis_bits, G: int, B: int, with_scale: bool = True):
+    """f4 variant, per-GOP matrices (seed xor GOP index): GOP g of the stream is
+    measured with phis_bits[g % len(phis_bits)]; otherwise encode_stream."""
+    T, H, W = frames.shape
+    phis = [phi_values(p) for p in phis_bits]
+    nby, nbx = block_grid(W, H, B)
+    n_cs = cs_frame_count(T, G)
+    y = np.empty((n_cs, nby * nbx, phis[0].shape[0]))
+    S = np.empty_like(y) if with_scale else None
+    i = 0
+    for g, (key_t, cs_ts) in enumerate(gop_partition(T, G)):
+        phi = phis[g % len(phis)]
+        for t in cs_ts:
+            R = frame_blocks(residual(frames[t], frames[key_t]), B)
+            y[i] = measure(R, phi)
+            if with_scale:
+                S[i] = tolerance_scale(R, phi)
+            i += 1
+    return y, S
 
 
 def encode_stream_chained(frames: np.ndarray, phi_bits: np.ndarray, G: int, B: int, with_scale: bool = True):

@@ -77,6 +77,7 @@ def lib() -> ctypes.CDLL:
             "cs_key_codec": (c_int, [vp, vp, c_int, c_int, vp, vp, vp, vp]),
             "cs_encode_batch_keys": (c_int, [vp, vp, c_int, c_int, vp, vp, vp]),
             "cs_encode_batch_chained": (c_int, [vp, vp, c_int, c_int, vp, vp]),
+            "cs_encoder_set_gop_phis": (c_int, [vp, c_int, vp]),
             "cs_measurement_count": (c_i64, [vp, c_int, c_int]),
             "cs_compression_ratio": (c_dbl, [vp, c_int, c_dbl, c_int]),
             "cs_compression_ratio_cfg": (c_dbl, [c_int, c_int, c_int, c_int, c_int, c_int, c_dbl, c_int]),
@@ -320,6 +321,16 @@ class Encoder:
         _check(lib().cs_encode_batch_keys(self._h, _ptr(frames), n_seq, T, _ptr(keys), _ptr(out),
                                           _stream_handle(stream)))
         return out
+
+    def set_gop_phis(self, phis=None):
+        """Per-GOP matrices: phis uint16 [n][M][B*B]; GOP g uses phis[g % n].  None or
+        an empty list restores the single Phi."""
+        if phis is None or len(phis) == 0:
+            _check(lib().cs_encoder_set_gop_phis(self._h, 0, None))
+            return
+        a = np.ascontiguousarray(np.stack([np.asarray(x, dtype=np.uint16) for x in phis]))
+        assert a.shape[1:] == (self.M, self.B * self.B)
+        _check(lib().cs_encoder_set_gop_phis(self._h, a.shape[0], a.ctypes.data))
 
     def encode_batch_chained(self, frames, out=None, stream=None):
         """Eq. 3 literal variant: residual of every CS frame against the previous raw frame."""

@@ -339,6 +339,8 @@ struct cs_encoder {
     cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
     std::vector<Plan> candidates;  // planner's ranked plans (autotune)
     int chained_plan = -1;         // best KEY_STREAMED candidate (previous-frame reference), -1 = none
+    void* phis_dev = nullptr;      // per-GOP Phi copies (arranged like phi_dev), n_phis of phi_bytes
+    int n_phis = 0;
     int tuned = -1;                // index of the autotuned plan, -1 = model choice
     void* zeros_dev = nullptr;   // piece_rows * W zero bytes: source for frame rows beyond H
     size_t zeros_bytes = 0;
@@ -439,6 +441,8 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.trace_cap = e->trace_cap;
     kp.keys = q.keys;
     kp.chained = q.chained;
+    kp.phis = (const uint16_t*)e->phis_dev;
+    kp.n_phis = e->n_phis;
     kp.n_gops_T = cdiv(T, g.G);
     kp.qmode = q.qmode;
     kp.codes = q.codes;
@@ -488,6 +492,23 @@ cudaError_t set_smem_attr_all(int bytes) {
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Phi -> canonical no-swizzle K-major UMMA layout, zero-padded to Mpad rows:
+//   byte(n, k) = (k/8)*LBO + (n/8)*SBO + (n%8)*16 + (k%8)*2.
+// The converters emit each group of four pixels j = 4q..4q+3 of a block row in K order
+// (4q, 4q+2, 4q+1, 4q+3) (see ptx::residual4), so MMA K index k holds pixel
+// j = 4(k/4) + {0,2,1,3}[k%4]; Phi's column k must be pixel j's column.
+std::vector<uint16_t> arrange_phi(const Geometry& g, uint32_t lbo, uint32_t sbo, const uint16_t* phi_fp16) {
+    static const int kPerm[4] = {0, 2, 1, 3};
+    std::vector<uint16_t> arranged((size_t)g.Mpad * g.N, 0);
+    for (int n = 0; n < g.M; ++n)
+        for (int k = 0; k < g.N; ++k) {
+            const int j = (k & ~3) | kPerm[k & 3];
+            size_t byte = (size_t)(k / 8) * lbo + (size_t)(n / 8) * sbo + (size_t)(n % 8) * 16 + (size_t)(k % 8) * 2;
+            arranged[byte / 2] = phi_fp16[(size_t)n * g.N + j];
+        }
+    return arranged;
+}
 
 // ------------------------------------------------------------------------ f3 adjoint (K3)
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -673,23 +694,12 @@ int cs_encoder_create(int W, int H, int gop, int B, int M, const uint16_t* phi_f
         delete e;
         return cuda_fail(err, "cudaFuncSetAttribute");
     }
-    // Phi -> canonical no-swizzle K-major UMMA layout, zero-padded to Mpad rows:
-    //   byte(n, k) = (k/8)*LBO + (n/8)*SBO + (n%8)*16 + (k%8)*2,  SBO = 128, LBO = Mpad*16.
+    // Phi in the canonical UMMA layout (arrange_phi): SBO = 128, LBO = Mpad*16
     const Geometry& g = e->geo;
     e->sbo = 128;
     e->lbo = (uint32_t)g.Mpad * 16u;
     e->phi_bytes = (uint32_t)g.Mpad * (uint32_t)g.N * 2u;
-    // The converters emit each group of four pixels j = 4q..4q+3 of a block row in K order
-    // (4q, 4q+2, 4q+1, 4q+3) (see ptx::residual4), so MMA K index k holds pixel
-    // j = 4(k/4) + {0,2,1,3}[k%4]; Phi's column k must be pixel j's column.
-    static const int kPerm[4] = {0, 2, 1, 3};
-    std::vector<uint16_t> arranged((size_t)g.Mpad * g.N, 0);
-    for (int n = 0; n < M; ++n)
-        for (int k = 0; k < g.N; ++k) {
-            const int j = (k & ~3) | kPerm[k & 3];
-            size_t byte = (size_t)(k / 8) * e->lbo + (size_t)(n / 8) * e->sbo + (size_t)(n % 8) * 16 + (size_t)(k % 8) * 2;
-            arranged[byte / 2] = phi_fp16[(size_t)n * g.N + j];
-        }
+    std::vector<uint16_t> arranged = arrange_phi(g, e->lbo, e->sbo, phi_fp16);
     // instruction descriptor, kind::f16: D fp32 (bit 4), A/B fp16 (0), K-major (0),
     // N>>3 at bits 17-22, M>>4 at bits 24-28 (M = 128 lanes).
     e->idesc = (1u << 4) | ((uint32_t)(g.Mpad >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
@@ -727,6 +737,7 @@ int cs_encoder_destroy(cs_encoder* e) {
     if (e->ws_frames) cudaFree(e->ws_frames);
     if (e->ws_out) cudaFree(e->ws_out);
     if (e->phiT_dev) cudaFree(e->phiT_dev);
+    if (e->phis_dev) cudaFree(e->phis_dev);
     for (auto& s : e->hs)
         if (s) cudaStreamDestroy(s);
     for (auto& ev : e->hev) cudaEventDestroy(ev);
@@ -924,6 +935,34 @@ int cs_key_codec(cs_encoder* e, const uint8_t* frames, int n_seq, int T, const i
     csenc::kc::cs_key_codec_kernel<<<dim3(gx, (unsigned)n_keys), csenc::kc::kThreads, 0, (cudaStream_t)stream>>>(kp);
     const cudaError_t err = cudaGetLastError();
     return err == cudaSuccess ? CS_OK : cuda_fail(err, "key codec launch");
+}
+
+int cs_encoder_set_gop_phis(cs_encoder* e, int n_phi, const uint16_t* phis) {
+    if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
+    if (n_phi < 0 || (n_phi > 0 && !phis)) return fail(CS_ERR_ARG, "n_phi must be >= 0 and phis non-NULL");
+    const Geometry& g = e->geo;
+    const size_t per = (size_t)g.M * g.N;
+    for (int i = 0; i < n_phi; ++i) {
+        const int rc = validate(g.W, g.H, g.G, g.B, g.M, phis + (size_t)i * per);
+        if (rc != CS_OK) return rc;
+    }
+    if (e->phis_dev) cudaFree(e->phis_dev);
+    e->phis_dev = nullptr;
+    e->n_phis = 0;
+    if (n_phi == 0) return CS_OK;
+    cudaError_t err = cudaMalloc(&e->phis_dev, (size_t)n_phi * e->phi_bytes);
+    if (err != cudaSuccess) return fail(CS_ERR_OOM, std::string("cudaMalloc(phis): ") + cudaGetErrorString(err));
+    for (int i = 0; i < n_phi; ++i) {
+        std::vector<uint16_t> a = arrange_phi(g, e->lbo, e->sbo, phis + (size_t)i * per);
+        err = cudaMemcpy((uint8_t*)e->phis_dev + (size_t)i * e->phi_bytes, a.data(), e->phi_bytes, cudaMemcpyHostToDevice);
+        if (err != cudaSuccess) {
+            cudaFree(e->phis_dev);
+            e->phis_dev = nullptr;
+            return cuda_fail(err, "cudaMemcpy(phis)");
+        }
+    }
+    e->n_phis = n_phi;
+    return CS_OK;
 }
 
 int cs_encode_batch_chained(cs_encoder* e, const uint8_t* frames, int n_seq, int T, float* out, cs_stream_t stream) {

@@ -76,7 +76,7 @@ enum QMode : int {
 };
 constexpr int kRowSlots = 40;                    // Q_ROW: max block rows per tile (3 x 40 u32 slots)
 constexpr uint32_t kRowSlotOff = 512;            // Q_ROW slots live in the barrier page (bytes 512..991)
-static_assert(16 * kMaxStages + 32 + 32 * kMaxTmemBufs + 16 <= (int)kRowSlotOff, "barrier block overlaps row slots");
+static_assert(16 * kMaxStages + 32 + 32 * kMaxTmemBufs + 24 <= (int)kRowSlotOff, "barrier block overlaps row slots");
 static_assert(kRowSlotOff + 3 * kRowSlots * 4 <= 1024, "row slots overflow the barrier page");
 
 struct KParams {
@@ -85,6 +85,10 @@ struct KParams {
     float* out;
     const uint16_t* phi;      // device, canonical UMMA layout, phi_bytes
     uint32_t phi_bytes;
+    // f4 variant (per-GOP seeds): n_phis > 0 -> GOP g is measured with
+    // phis[g % n_phis] (each phi_bytes, same layout), reloaded into SMEM when a unit's GOP changes
+    const uint16_t* phis;
+    int n_phis;
     int W, H, M, Mpad, N;
     int nbx, nby, nblk;
     // tiling
@@ -389,6 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
     const uint32_t bar_d_empty = bar_d_full + 8 * kMaxTmemBufs;
     const uint32_t bar_phi = bar_d_empty + 8 * kMaxTmemBufs;
     const uint32_t tmem_slot = bar_phi + 8;
+    const uint32_t bar_phi_empty = bar_phi + 16;   // per-GOP Phi: MMAs on the current Phi done
     const uint32_t s_phi = sbase + p.off_phi;
     const uint32_t s_key = sbase + p.off_key;
     const uint32_t s_stage = sbase + p.off_stage;
@@ -413,6 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
             ptx::mbar_init(bar_d_empty + 8 * i, 4);
         }
         ptx::mbar_init(bar_phi, 1);
+        ptx::mbar_init(bar_phi_empty, 1);
         ptx::fence_mbarrier_init();
     }
     if (warp == kMmaWarp) {
@@ -455,11 +461,15 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
         const uint64_t pol_stream = ptx::policy_evict_first();
         const uint64_t pol_key = ptx::policy_evict_last();
         const size_t frame_bytes = (size_t)p.W * (size_t)p.H;
-        if (elect_one()) {
-            ptx::mbar_arrive_expect_tx(bar_phi, p.phi_bytes);
-            ptx::bulk_load(s_phi, p.phi, p.phi_bytes, bar_phi);
+        if (p.n_phis == 0) {
+            if (elect_one()) {
+                ptx::mbar_arrive_expect_tx(bar_phi, p.phi_bytes);
+                ptx::bulk_load(s_phi, p.phi, p.phi_bytes, bar_phi);
+            }
+            __syncwarp();
         }
-        __syncwarp();
+        int phi_cur = -1;
+        uint32_t phi_loads = 0;
         int st = 0;
         uint32_t ph = 0;
         int kb = 0;
@@ -468,6 +478,20 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             Unit w;
             if (!decode_unit(p, u, w)) continue;
+            if (p.n_phis > 0) {   // per-GOP Phi: reload when the GOP's matrix differs from the resident one
+                const int gsel = w.g % p.n_phis;
+                if (gsel != phi_cur) {
+                    if (phi_loads > 0) ptx::mbar_wait(bar_phi_empty, (phi_loads - 1u) & 1u);
+                    if (elect_one()) {
+                        ptx::mbar_arrive_expect_tx(bar_phi, p.phi_bytes);
+                        ptx::bulk_load(s_phi, reinterpret_cast<const uint8_t*>(p.phis) + (size_t)gsel * p.phi_bytes,
+                                       p.phi_bytes, bar_phi);
+                    }
+                    __syncwarp();
+                    phi_cur = gsel;
+                    ++phi_loads;
+                }
+            }
             const uint8_t* const raw_key = p.frames + (size_t)key_frame(p, w) * frame_bytes;
             const uint8_t* const key_f =
                 p.keys ? p.keys + ((size_t)w.s * p.n_gops_T + (size_t)w.g) * frame_bytes : raw_key;
@@ -523,8 +547,12 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
         // ================================================================ MMA issuer
         // The whole warp walks the schedule (warp-uniform control flow keeps every operand in
         // uniform registers); one elected lane issues the tcgen05 instructions.
-        ptx::mbar_wait(bar_phi, 0);
-        ptx::tc_fence_after();
+        if (p.n_phis == 0) {
+            ptx::mbar_wait(bar_phi, 0);
+            ptx::tc_fence_after();
+        }
+        int phi_cur = -1;
+        uint32_t phi_waits = 0;
         int ab = 0, db = 0;
         uint32_t aph = 0, dph = 0;
         const int ksteps = p.chunk_k / 16;
@@ -538,6 +566,21 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             Unit w;
             if (!decode_unit(p, u, w)) continue;
+            if (p.n_phis > 0) {
+                const int gsel = w.g % p.n_phis;
+                if (gsel != phi_cur) {
+                    // release the resident Phi once every MMA issued so far has completed, then wait
+                    // for the next one
+                    if (phi_waits > 0) {
+                        if (elect_one()) ptx::tc_commit(bar_phi_empty);
+                        __syncwarp();
+                    }
+                    ptx::mbar_wait(bar_phi, phi_waits & 1u);
+                    ptx::tc_fence_after();
+                    phi_cur = gsel;
+                    ++phi_waits;
+                }
+            }
             for (int c = w.c0; c < w.c1; ++c) {
                 ptx::mbar_wait(bar_d_empty + 8 * db, dph ^ 1u);
                 ptx::tc_fence_after();

@@ -148,3 +148,30 @@ def test_chained_reference_parity(name):
         y, S = oracle.encode_stream_chained(frames[s], phi, cfg.G, cfg.B)
         ok, st = oracle.check_tolerance(y_gpu[s * n_cs:(s + 1) * n_cs], y, S, REL)
         assert ok, st
+
+
+@pytest.mark.parametrize("name,M", [("C2", 32), ("C4", 128), ("C5", 4), ("C3", 64)])
+def test_gop_phis_parity(name, M):
+    """f4 variant, per-GOP seeds: GOP g measured with Phi(seed ^ g); the resident
+    Phi is reloaded per unit.  Then n = 0 restores the single Phi (bitwise equal to a fresh run)."""
+    base = synth.CONFIGS[name]
+    cfg = base.with_(T=min(base.T, 3 * base.G + 2), S=min(base.S, 3))
+    frames = synth.gen_video(cfg)
+    n_g = -(-cfg.T // cfg.G)
+    phis = [synth.phi_from_seed(synth.phi_seed() ^ g, M, cfg.B ** 2) for g in range(n_g)]
+    enc = P.Encoder(cfg.W, cfg.H, cfg.G, cfg.B, M, phis[0])
+    fd = torch.from_numpy(frames).cuda()
+    ref = enc.encode_batch(fd).clone()
+    enc.set_gop_phis(phis)
+    y_gpu = enc.encode_batch(fd)
+    torch.cuda.synchronize()
+    yg = y_gpu.cpu().numpy()
+    n_cs = oracle.cs_frame_count(cfg.T, cfg.G)
+    for s in range(cfg.S):
+        y, S = oracle.encode_stream_gop_phis(frames[s], phis, cfg.G, cfg.B)
+        ok, st = oracle.check_tolerance(yg[s * n_cs:(s + 1) * n_cs], y, S, REL)
+        assert ok, st
+    enc.set_gop_phis(None)
+    again = enc.encode_batch(fd)
+    torch.cuda.synchronize()
+    assert torch.equal(again, ref)

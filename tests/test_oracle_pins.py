@@ -561,3 +561,21 @@ def test_chained_reference_variant():
     for i, (k, t) in enumerate(order):
         run = yc[i] if t == k + 1 else run + yc[i]
         assert np.array_equal(run, yk[i]), (i, k, t)
+
+
+def test_gop_phis_variant():
+    """Per-GOP matrices: one matrix repeated == encode_stream; GOP g's rows equal encode_stream
+    with phi_g on that GOP (index g % n)."""
+    rng = np.random.default_rng(61)
+    frames = rng.integers(0, 256, (11, 8, 12), dtype=np.uint8)
+    B, M, G = 4, 5, 3
+    phis = [synth.phi_from_seed(100 ^ g, M, B * B) for g in range(2)]
+    y1, _ = oracle.encode_stream_gop_phis(frames, [phis[0]], G, B)
+    y0, _ = oracle.encode_stream(frames, phis[0], G, B)
+    assert np.array_equal(y1, y0)
+    y2, _ = oracle.encode_stream_gop_phis(frames, phis, G, B)
+    i = 0
+    for g, (k, cs) in enumerate(oracle.gop_partition(11, G)):
+        yg, _ = oracle.encode_stream(frames[k:k + 1 + len(cs)], phis[g % 2], G, B)
+        assert np.array_equal(y2[i:i + len(cs)], yg)
+        i += len(cs)
