@@ -210,6 +210,10 @@ def run_ours(args, cfg, Ms):
         outs = [None] * len(Ms)   # the q16 step does not touch the fp32 buffers; free them
         torch.cuda.empty_cache()
     stream = torch.cuda.current_stream(dev)
+    if args.gop_phis:   # f4 variant: Phi(seed ^ g) per GOP index
+        n_g = -(-cfg.T // cfg.G)
+        for M, e in zip(Ms, encs):
+            e.set_gop_phis([synth.phi_from_seed(synth.phi_seed() ^ g, M, cfg.B ** 2) for g in range(n_g)])
     # plan choice: the fastest of the planner's top plans (outputs are bit-identical across plans);
     # --tune-file reuses earlier choices (e.g. under ncu, so no tuning launches are profiled)
     tuned = {}
@@ -314,6 +318,7 @@ def run_ours(args, cfg, Ms):
         "config": {"workload": args.workload, "W": cfg.W, "H": cfg.H, "T": cfg.T, "streams_per_gpu": n_seq,
                    "G": cfg.G, "B": cfg.B, "M": list(Ms), "output": args.output, "op": args.op,
                    **({"key_quant_scale": args.key_scale, "key_codec_ms": key_ms} if closed else {}),
+                   **({"gop_phis": True} if args.gop_phis else {}),
                    "l2": f"inputs larger than L2 ({in_mb:.0f} MiB read per launch vs 126 MiB L2); no flush",
                    "parallelism": f"dp{world} (independent sequences per GPU, no collective)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -607,6 +612,7 @@ def main(argv=None):
                     help="encode (the north-star hot path, default), adjoint (f3 back-projection) or "
                          "closed_loop (f4: key codec + encode against the decoded keys)")
     ap.add_argument("--key-scale", type=float, default=1.0, help="closed_loop: key quantiser scale")
+    ap.add_argument("--gop-phis", action="store_true", help="encode: one Phi per GOP index (seed ^ g)")
     ap.add_argument("--output", choices=list(OUTPUTS), default="f32",
                     help="f32 measurements (headline) or 16-bit codes (f1): per-frame or per-row scales")
     ap.add_argument("--tune-file", default=None, help="json of chosen plan indices (read if present, else written)")
