@@ -262,11 +262,11 @@ class Encoder:
         return out
 
     # -- 16-bit quantisation (f1)
-    Q16_FRAME, Q16_ROW = 0, 1
+    Q16_FRAME, Q16_ROW, Q16_FRAME_1PASS = 0, 1, 2
 
     def q16_scale_shape(self, n_seq: int, T: int, granularity: int = 0):
         n_cs = self.out_shape(n_seq, T)[0]
-        return (n_cs,) if granularity == self.Q16_FRAME else (n_cs, self.nby)
+        return (n_cs, self.nby) if granularity == self.Q16_ROW else (n_cs,)
 
     def encode_batch_q16(self, frames, granularity: int = 0, codes=None, scales=None, stream=None):
         """frames: CUDA uint8 [n_seq][T][H][W]; returns (codes int16 [n_cs][nblk][M], scales fp32

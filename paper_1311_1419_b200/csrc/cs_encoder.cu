@@ -339,6 +339,8 @@ struct cs_encoder {
     cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
     std::vector<Plan> candidates;  // planner's ranked plans (autotune)
     int chained_plan = -1;         // best KEY_STREAMED candidate (previous-frame reference), -1 = none
+    int frame1_plan = -1;          // f1 single-pass plan: D ring >= 2 (look-back lag >= 1), tiles <= SMs; -1 = none
+    Plan frame1{};                 // that candidate with the D ring as deep as TMEM allows (<= 8)
     void* phis_dev = nullptr;      // per-GOP Phi copies (arranged like phi_dev), n_phis of phi_bytes
     int n_phis = 0;
     int tuned = -1;                // index of the autotuned plan, -1 = model choice
@@ -366,6 +368,8 @@ namespace {
 struct QArgs {
     const uint8_t* keys = nullptr;   // f4: decoded key frames [n_seq][ceil(T/G)][H][W]
     int chained = 0;                 // f4 variant: previous-frame reference (needs a KEY_STREAMED plan)
+    int gop_rounds = 0;              // f1 single pass: whole-GOP units, grid a multiple of n_tiles
+    unsigned* arrivals = nullptr;    // f1 single pass: per-frame arrival counters (zeroed)
     const Plan* plan = nullptr;      // plan override (default e->plan)
     int qmode = 0;
     int16_t* codes = nullptr;
@@ -422,10 +426,16 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.gop_begin = g0;
     kp.n_gops_sel = g1 - g0;
     kp.cs_per_stream_sel = (int)cs_frames_in_gops(T, g.G, g0, g1);
-    WorkSplit ws = choose_split(g, pl, n_seq, g1 - g0, e->sms);
-    kp.n_splits = ws.n_splits;
-    kp.cs_per_unit = ws.cs_per_unit;
-    kp.n_units = ws.n_units;
+    if (q.gop_rounds) {
+        kp.n_splits = 1;
+        kp.cs_per_unit = g.G - 1;
+        kp.n_units = n_seq * (g1 - g0) * pl.n_tiles;
+    } else {
+        WorkSplit ws = choose_split(g, pl, n_seq, g1 - g0, e->sms);
+        kp.n_splits = ws.n_splits;
+        kp.cs_per_unit = ws.cs_per_unit;
+        kp.n_units = ws.n_units;
+    }
     kp.idesc = e->idesc;
     kp.lbo = e->lbo;
     kp.sbo = e->sbo;
@@ -448,15 +458,27 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.codes = q.codes;
     kp.amax = q.amax;
     kp.scales = q.scales;
-    const int grid = std::max(1, std::min(e->sms, kp.n_units));
+    kp.arrivals = q.arrivals;
+    kp.lookback = std::max(1, std::min(std::min(csenc::kMaxLag, pl.n_dbuf - 1), env_int("CSENC_LOOKBACK", 99)));
+    int grid = std::max(1, std::min(e->sms, kp.n_units));
+    if (q.gop_rounds) grid = std::max(1, std::min(e->sms / pl.n_tiles * pl.n_tiles, kp.n_units));
     cudaError_t err;
     const int km = pl.key_regs ? csenc::KEY_REGS : (pl.key_resident ? csenc::KEY_RESIDENT : csenc::KEY_STREAMED);
-    auto go = [&](auto kern) { kern<<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(kp); };
-    const int epi = q.qmode ? csenc::EPI_Q16 : csenc::EPI_F32;
-#define CSENC_CASE(B_, K_)                                                                              \
-    case (B_ * 4 + K_) * 2 + csenc::EPI_F32: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_F32>); break; \
-    case (B_ * 4 + K_) * 2 + csenc::EPI_Q16: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16>); break;
-    switch ((g.B * 4 + km) * 2 + epi) {
+    auto go = [&](auto kern) {
+        if (q.gop_rounds) {   // the look-back needs every CTA resident: cooperative launch guarantees it
+            void* args[] = {&kp};
+            cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(csenc::threads_for<csenc::EPI_Q16F>()), args,
+                                        pl.smem_bytes, stream);
+        } else {
+            kern<<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(kp);
+        }
+    };
+    const int epi = q.qmode == csenc::Q_FRAME1 ? csenc::EPI_Q16F : (q.qmode ? csenc::EPI_Q16 : csenc::EPI_F32);
+#define CSENC_CASE(B_, K_)                                                                                \
+    case (B_ * 4 + K_) * 4 + csenc::EPI_F32: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_F32>); break;   \
+    case (B_ * 4 + K_) * 4 + csenc::EPI_Q16: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16>); break;   \
+    case (B_ * 4 + K_) * 4 + csenc::EPI_Q16F: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16F>); break;
+    switch ((g.B * 4 + km) * 4 + epi) {
         CSENC_CASE(8, csenc::KEY_STREAMED) CSENC_CASE(8, csenc::KEY_RESIDENT) CSENC_CASE(8, csenc::KEY_REGS)
         CSENC_CASE(16, csenc::KEY_STREAMED) CSENC_CASE(16, csenc::KEY_RESIDENT) CSENC_CASE(16, csenc::KEY_REGS)
         CSENC_CASE(32, csenc::KEY_STREAMED) CSENC_CASE(32, csenc::KEY_RESIDENT)
@@ -476,6 +498,9 @@ cudaError_t set_smem_attr_all(int bytes) {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);                         \
     if (r != cudaSuccess) e = r;                                                                          \
     r = cudaFuncSetAttribute(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16>,                           \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);                         \
+    if (r != cudaSuccess) e = r;                                                                          \
+    r = cudaFuncSetAttribute(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16F>,                          \
                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);                         \
     if (r != cudaSuccess) e = r;
     CSENC_ATTR(8, csenc::KEY_STREAMED) CSENC_ATTR(8, csenc::KEY_RESIDENT) CSENC_ATTR(8, csenc::KEY_REGS)
@@ -683,6 +708,17 @@ int cs_encoder_create(int W, int H, int gop, int B, int M, const uint16_t* phi_f
             e->chained_plan = (int)i;
             break;
         }
+    // f1 single pass: the best plan with a D ring deep enough for the look-back whose tiles fit one
+    // round (n_tiles <= SMs)
+    for (size_t i = 0; i < e->candidates.size(); ++i) {
+        Plan c = e->candidates[i];
+        // the look-back holds `lag` accumulators: the D ring as deep as TMEM allows, lag = ring - 1
+        c.n_dbuf = std::min(csenc::kMaxTmemBufs, ((int)csenc::kTmemCols - c.n_abuf * c.a_cols) / c.d_cols);
+        if (c.n_dbuf < 2 || c.n_tiles > e->sms) continue;
+        e->frame1_plan = (int)i;
+        e->frame1 = c;
+        break;
+    }
     if (!make_plan(e->geo, e->smem_limit, e->plan)) {
         delete e;
         return fail(CS_ERR_UNSUPPORTED, "no tiling fits shared memory / TMEM for this configuration");
@@ -1188,7 +1224,7 @@ int cs_adjoint(cs_encoder* e, const float* meas, int64_t n_frames, float* x, cs_
 int64_t cs_q16_scale_count(const cs_encoder* e, int n_seq, int T, int granularity) {
     if (!e || n_seq < 0 || T < 0) return -1;
     const long long n_cs = (long long)n_seq * cs_frames_per_stream(T, e->geo.G);
-    if (granularity == CS_Q16_FRAME) return n_cs;
+    if (granularity == CS_Q16_FRAME || granularity == CS_Q16_FRAME_1PASS) return n_cs;
     if (granularity == CS_Q16_ROW) return n_cs * e->geo.nby;
     return -1;
 }
@@ -1197,7 +1233,8 @@ int cs_encode_batch_q16(cs_encoder* e, const uint8_t* frames, int n_seq, int T, 
                         float* scales, cs_stream_t stream) {
     if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
     if (n_seq < 0 || T < 0) return fail(CS_ERR_ARG, "n_seq and T must be >= 0");
-    if (granularity != CS_Q16_FRAME && granularity != CS_Q16_ROW) return fail(CS_ERR_ARG, "bad granularity");
+    if (granularity != CS_Q16_FRAME && granularity != CS_Q16_ROW && granularity != CS_Q16_FRAME_1PASS)
+        return fail(CS_ERR_ARG, "bad granularity");
     const Geometry& g = e->geo;
     const long long n_cs = (long long)n_seq * cs_frames_per_stream(T, g.G);
     if (n_cs == 0) return CS_OK;
@@ -1216,7 +1253,30 @@ int cs_encode_batch_q16(cs_encoder* e, const uint8_t* frames, int n_seq, int T, 
         q.scales = scales;
         return launch(e, frames, n_seq, T, 0, n_gops, nullptr, st, q);
     }
-    // per-frame scale: zero the |y| maxima, absmax pass, codes pass, finalize
+    if (granularity == CS_Q16_FRAME_1PASS && e->frame1_plan < 0)
+        return fail(CS_ERR_UNSUPPORTED, "single-pass per-frame quantisation: no plan (D ring >= 2, tiles <= SMs)");
+    if (granularity == CS_Q16_FRAME_1PASS) {
+        // per-frame scale in ONE pass: frame-major units, decoupled look-back on per-frame maxima
+        // (workspace: |y| maxima and arrival counters, stream-ordered, zeroed)
+        uint32_t* ws = nullptr;
+        cudaError_t err = cudaMallocAsync((void**)&ws, (size_t)n_cs * 8, st);
+        if (err != cudaSuccess) return fail(CS_ERR_OOM, std::string("q16 workspace: ") + cudaGetErrorString(err));
+        err = cudaMemsetAsync(ws, 0, (size_t)n_cs * 8, st);
+        int rc = err == cudaSuccess ? CS_OK : cuda_fail(err, "cudaMemsetAsync");
+        if (rc == CS_OK) {
+            q.qmode = csenc::Q_FRAME1;
+            q.amax = ws;
+            q.arrivals = ws + n_cs;
+            q.scales = scales;
+            q.gop_rounds = 1;
+            q.plan = &e->frame1;
+            rc = launch(e, frames, n_seq, T, 0, n_gops, nullptr, st, q);
+        }
+        cudaFreeAsync(ws, st);
+        return rc;
+    }
+    // per-frame scale in two passes: zero the |y| maxima, absmax pass, codes pass,
+    // finalize
     q.amax = reinterpret_cast<uint32_t*>(scales);
     cudaError_t err = cudaMemsetAsync(scales, 0, (size_t)n_cs * sizeof(float), st);
     if (err != cudaSuccess) return cuda_fail(err, "cudaMemsetAsync");

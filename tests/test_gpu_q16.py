@@ -230,3 +230,22 @@ def test_q16_bad_args():
     enc1 = P.Encoder(64, 32, 1, 16, 16, synth.phi_from_seed(1, 16, 256))
     c, s = enc1.encode_batch_q16(fd)
     assert c.numel() == 0 and s.numel() == 0
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_q16_frame_single_pass_equals_two_pass(name):
+    """The single-pass per-frame mode (GOP-round look-back) and the two-pass mode quantise the
+    same fp32 measurements with the same per-frame maxima: bitwise identical codes and scales; and
+    both match the oracle."""
+    base = synth.CONFIGS[name]
+    cfg = base.with_(T=min(base.T, 2 * base.G + 3), S=min(base.S, 3))
+    frames = synth.gen_video(cfg)
+    fd = torch.from_numpy(frames).cuda()
+    for M in base.Ms[:2]:
+        phi = synth.phi_from_seed(synth.phi_seed(), M, cfg.B ** 2)
+        enc = P.Encoder(cfg.W, cfg.H, cfg.G, cfg.B, M, phi)
+        c1, s1 = run_q16(enc, fd, P.Encoder.Q16_FRAME_1PASS)
+        c2, s2 = run_q16(enc, fd, P.Encoder.Q16_FRAME)
+        assert torch.equal(c1, c2) and torch.equal(s1, s2)
+        y, S = oracle.encode(frames, phi, cfg.G, cfg.B)
+        check_q16(c1.cpu().numpy(), s1.cpu().numpy(), y, S, enc.nby, enc.nbx, P.Encoder.Q16_FRAME)
