@@ -195,6 +195,11 @@ typedef struct cs_frame_encoder cs_frame_encoder;
 int cs_frame_encoder_create(int W, int H, int gop, int m, const uint16_t* A_fp16, cs_frame_encoder** out);
 int cs_frame_encoder_destroy(cs_frame_encoder* enc);
 
+/* Debug timeline of CTA 0 (as cs_encoder_set_trace): trace_dev[event * cap + i] = clock64 of the i-th
+ * K chunk's event: 0 producer issued the TMA loads, 1 converters saw the data, 2 residual operand
+ * written, 3 MMAs issued.  cap = 0 disables. */
+int cs_frame_encoder_set_trace(cs_frame_encoder* enc, unsigned long long* trace_dev, int cap);
+
 /* n_seq * (CS frames per stream) * m; -1 on bad arguments. */
 int64_t cs_frame_measurement_count(const cs_frame_encoder* enc, int n_seq, int T);
 

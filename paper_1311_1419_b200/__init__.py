@@ -71,6 +71,7 @@ def lib() -> ctypes.CDLL:
             "cs_frame_encoder_destroy": (c_int, [vp]),
             "cs_frame_measurement_count": (c_i64, [vp, c_int, c_int]),
             "cs_frame_encode_batch": (c_int, [vp, vp, c_int, c_int, vp, vp]),
+            "cs_frame_encoder_set_trace": (c_int, [vp, vp, c_int]),
             "cs_key_qsteps": (c_int, [c_dbl, vp]),
             "cs_key_dct_basis": (None, [vp]),
             "cs_key_coef_count": (c_i64, [vp, c_int, c_int]),
@@ -399,6 +400,10 @@ class FrameEncoder:
 
     def out_shape(self, n_seq: int, T: int):
         return (n_seq * (T - -(-T // self.G)), self.m)
+
+    def set_trace(self, buf=None, cap: int = 0):
+        """buf: CUDA int64 tensor of 4 * cap elements (None/0 disables); see cs_frame_encoder_set_trace."""
+        _check(lib().cs_frame_encoder_set_trace(self._h, _ptr(buf) if buf is not None else None, cap))
 
     def encode_batch(self, frames, out=None, stream=None):
         """frames: CUDA uint8 [n_seq][T][H][W]; returns CUDA float32 [n_cs][m]."""

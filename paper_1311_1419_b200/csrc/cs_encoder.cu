@@ -360,6 +360,8 @@ struct cs_frame_encoder {
     int W = 0, H = 0, G = 0, m = 0, n = 0;
     int device = 0, sms = 0, smem_limit = 0;
     void* A_dev = nullptr;   // fp16 [m][n], columns permuted within groups of 4 (converter pair order)
+    unsigned long long* trace = nullptr;   // debug timeline (cs_frame_encoder_set_trace)
+    int trace_cap = 0;
 };
 
 namespace {
@@ -1085,6 +1087,13 @@ int cs_frame_encoder_create(int W, int H, int gop, int m, const uint16_t* A_fp16
     return CS_OK;
 }
 
+int cs_frame_encoder_set_trace(cs_frame_encoder* f, unsigned long long* trace_dev, int cap) {
+    if (!f || cap < 0 || (cap > 0 && !trace_dev)) return fail(CS_ERR_ARG, "bad trace arguments");
+    f->trace = cap > 0 ? trace_dev : nullptr;
+    f->trace_cap = cap;
+    return CS_OK;
+}
+
 int cs_frame_encoder_destroy(cs_frame_encoder* f) {
     if (!f) return CS_OK;
     if (f->A_dev) cudaFree(f->A_dev);
@@ -1185,6 +1194,9 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     fp.n_stages = (int)std::min<long>(csenc::frm::kMaxStages, avail / (long)fp.stage_bytes);
     if (fp.n_stages < 2) return fail(CS_ERR_UNSUPPORTED, "frame measurement: stages do not fit shared memory");
     const uint32_t smem = 1024 + fp.off_stage + (uint32_t)fp.n_stages * fp.stage_bytes;
+    fp.prefetch = env_int("CSENC_FRAME_PREFETCH", 0);
+    fp.trace = f->trace;
+    fp.trace_cap = f->trace_cap;
     const long long ny = (long long)n_seq * cs_s * f->m;
     float* part = nullptr;
     cudaError_t err;

@@ -54,7 +54,15 @@ struct FParams {
     uint32_t off_stage;       // kOffB + 2 * b_bytes
     int n_stages;
     long long part_stride;    // floats per partial plane (n_seq * cs_s * m rounded up to 4)
+    int prefetch;             // frame boxes prefetched into L2 this many chunks ahead (0 = off)
+    unsigned long long* trace;   // debug timeline (CTA 0): [4][trace_cap] clock64, nullptr = off
+    int trace_cap;
 };
+
+// trace events: 0 producer issued, 1 converter data landed, 2 converter done, 3 MMA issued
+__device__ __forceinline__ void ftrace(const FParams& p, int ev, int i) {
+    if (p.trace != nullptr && blockIdx.x == 0 && i < p.trace_cap) p.trace[(size_t)ev * p.trace_cap + i] = clock64();
+}
 
 struct FUnit {
     int s, g0, ngops, n_cs, cs0, mp, ks, kc0, kc1;
@@ -131,20 +139,27 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
 
     if (warp == kProducerWarp) {
         // ================================================================ producer
-        int st = 0;
+        int st = 0, ntr = 0;
         uint32_t ph = 0;
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             FUnit w;
             decode_funit(p, u, w);
             const int row0 = w.s * p.T + w.g0 * p.G;
+            if (lane == 0)   // frames stream from HBM: pull the first boxes of the unit into L2 early
+                for (int kc = w.kc0; kc < min(w.kc1, w.kc0 + p.prefetch); ++kc)
+                    ptx::tma_prefetch_2d(&p.fmap, kc * kKc, row0);
             for (int kc = w.kc0; kc < w.kc1; ++kc) {
                 ptx::mbar_wait(bar_empty + 8 * st, ph ^ 1u);
+                if (lane == 0 && p.prefetch > 0 && kc + p.prefetch < w.kc1)
+                    ptx::tma_prefetch_2d(&p.fmap, (kc + p.prefetch) * kKc, row0);
                 if (lane == 0) {
                     const uint32_t sf = sbase + p.off_stage + (uint32_t)st * p.stage_bytes;
                     ptx::mbar_arrive_expect_tx(bar_full + 8 * st, p.fbox_bytes + 256u * kKc * 2u);
                     ptx::tma_load_2d(sf, &p.fmap, bar_full + 8 * st, kc * kKc, row0);
                     ptx::tma_load_2d(sf + p.off_a, &p.amap, bar_full + 8 * st, kc * kKc, w.mp * 256);
+                    ftrace(p, 0, ntr);
                 }
+                ++ntr;
                 __syncwarp();
                 if (++st == p.n_stages) {
                     st = 0;
@@ -165,13 +180,14 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
             const int gl = c / (p.G - 1), pos = c - gl * (p.G - 1);
             rows[i] = (uint32_t)(gl * p.G + 1 + pos) | ((uint32_t)(gl * p.G) << 16);
         }
-        int st = 0, b = 0;
+        int st = 0, b = 0, ntr = 0;
         uint32_t ph = 0, bph = 0;
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             FUnit w;
             decode_funit(p, u, w);
             for (int kc = w.kc0; kc < w.kc1; ++kc) {
                 ptx::mbar_wait(bar_full + 8 * st, ph);
+                if (tid == 0) ftrace(p, 1, ntr);
                 ptx::mbar_wait(bar_bempty + 8 * b, bph ^ 1u);
                 const uint32_t sf = sbase + p.off_stage + (uint32_t)st * p.stage_bytes;
                 const uint32_t sb = sbase + kOffB + (uint32_t)b * p.b_bytes;
@@ -194,6 +210,8 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(bar_conv + 8 * b);
+                if (tid == 0) ftrace(p, 2, ntr);
+                ++ntr;
                 if (++st == p.n_stages) {
                     st = 0;
                     ph ^= 1u;
@@ -208,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         // ================================================================ MMA issuer
         // D: m-tile 0 at TMEM columns [0, N), m-tile 1 at [256, 256 + N); single-buffered (a unit is
         // hundreds of chunks long, the epilogue a few thousand cycles)
-        int st = 0, b = 0;
+        int st = 0, b = 0, ntr = 0;
         uint32_t ph = 0, bph = 0, dph = 0;
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             FUnit w;
@@ -237,7 +255,9 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                     ptx::tc_commit(bar_empty + 8 * st);
                     ptx::tc_commit(bar_bempty + 8 * b);
                     if (kc == w.kc1 - 1) ptx::tc_commit(bar_dfull);
+                    ftrace(p, 3, ntr);
                 }
+                ++ntr;
                 __syncwarp();
                 if (++st == p.n_stages) {
                     st = 0;

@@ -94,6 +94,12 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, uint
         "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(bar)
         : "memory");
 }
+// Prefetch a 2-D tensor box into L2 (no SMEM destination, no completion tracking).
+__device__ __forceinline__ void tma_prefetch_2d(const void* tmap, int x, int y) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(tmap)),
+                 "r"(x), "r"(y)
+                 : "memory");
+}
 // Make this thread's generic-proxy shared-memory writes visible to the async proxy (tensor core
 // operand reads through descriptors, bulk copies).
 __device__ __forceinline__ void fence_proxy_async_smem() {
