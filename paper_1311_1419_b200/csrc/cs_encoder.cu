@@ -1058,8 +1058,11 @@ int cs_frame_encoder_create(int W, int H, int gop, int m, const uint16_t* A_fp16
     f->device = dev;
     cudaDeviceGetAttribute(&f->sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&f->smem_limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    err = cudaFuncSetAttribute(csenc::frm::cs_frame_measure_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    err = cudaFuncSetAttribute(csenc::frm::cs_frame_measure_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                f->smem_limit);
+    if (err == cudaSuccess)
+        err = cudaFuncSetAttribute(csenc::frm::cs_frame_measure_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   f->smem_limit);
     if (err != cudaSuccess) {
         delete f;
         return cuda_fail(err, "cudaFuncSetAttribute");
@@ -1149,6 +1152,10 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
         fp.n_win = n_seq * fp.n_win_s;
     }
     fp.nf_box = fp.gw * G;
+    // pairs of CTAs (a cluster) can share each A tile by TMA multicast
+    // (measured slower on B200 than independent CTAs: 876 vs 966 TFLOP/s -- the pair is coupled
+    // through the shared stage; opt-in with CSENC_FRAME_CLUSTER=1)
+    const int CL = (fp.n_win >= 2 && env_int("CSENC_FRAME_CLUSTER", 0) == 1) ? 2 : 1;
     {
         cuuint64_t dims[2] = {(cuuint64_t)f->n, (cuuint64_t)n_seq * T};
         cuuint64_t strides[1] = {(cuuint64_t)f->n};
@@ -1162,7 +1169,7 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     {
         cuuint64_t dims[2] = {(cuuint64_t)f->n, (cuuint64_t)f->m};
         cuuint64_t strides[1] = {(cuuint64_t)f->n * 2u};
-        cuuint32_t box[2] = {(cuuint32_t)csenc::frm::kKc, 256u};
+        cuuint32_t box[2] = {(cuuint32_t)csenc::frm::kKc, (cuuint32_t)(256 / CL)};
         cuuint32_t estr[2] = {1, 1};
         CUresult r = enc(&fp.amap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, f->A_dev, dims, strides, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1176,8 +1183,9 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     fp.cs_s = (int)cs_s;
 
     fp.n_chunks = cdiv(f->n, csenc::frm::kKc);
-    const long long tiles = (long long)fp.n_win * fp.n_mp;
-    long long ks = (f->sms + tiles - 1) / tiles;                   // K splits to fill the SMs
+    const long long n_cl = f->sms / CL;                                 // clusters resident at once
+    const long long tiles = (long long)((fp.n_win + CL - 1) / CL) * fp.n_mp;   // cluster work units
+    long long ks = (n_cl + tiles - 1) / tiles;                        // K splits to fill the SMs
     ks = std::max(1LL, std::min(ks, (long long)std::max(1, fp.n_chunks / 8)));
     // no empty K split (every unit must issue at least one chunk): ks = ceil(chunks / per-split)
     const long long per_split = (fp.n_chunks + ks - 1) / ks;
@@ -1189,7 +1197,8 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     fp.off_a = align_up(fp.fbox_bytes, 1024);
     fp.stage_bytes = fp.off_a + 256u * csenc::frm::kKc * 2u;
     fp.b_bytes = align_up((uint32_t)(fp.gw * (G - 1) + 15) / 16 * 16 * 128u, 1024);
-    fp.off_stage = csenc::frm::kOffB + 2 * fp.b_bytes;
+    fp.n_b = std::max(2, std::min(4, env_int("CSENC_FRAME_BBUFS", 2)));
+    fp.off_stage = csenc::frm::kOffB + (uint32_t)fp.n_b * fp.b_bytes;
     const long avail = (long)f->smem_limit - 1024 - (long)fp.off_stage;
     fp.n_stages = (int)std::min<long>(csenc::frm::kMaxStages, avail / (long)fp.stage_bytes);
     if (fp.n_stages < 2) return fail(CS_ERR_UNSUPPORTED, "frame measurement: stages do not fit shared memory");
@@ -1209,9 +1218,23 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
         fp.part_stride = 0;
         fp.out = y;
     }
-    const int grid = std::max(1, std::min(f->sms, fp.n_units));
-    csenc::frm::cs_frame_measure_kernel<<<grid, csenc::frm::kThreads, smem, st>>>(fp);
-    err = cudaGetLastError();
+    const int n_clusters = (int)std::max(1LL, std::min(n_cl, (long long)fp.n_units));
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3((unsigned)(n_clusters * CL));
+    cfg.blockDim = dim3(csenc::frm::kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    err = CL == 2 ? cudaLaunchKernelEx(&cfg, csenc::frm::cs_frame_measure_kernel<2>, fp)
+                  : cudaLaunchKernelEx(&cfg, csenc::frm::cs_frame_measure_kernel<1>, fp);
+    if (err == cudaSuccess) err = cudaGetLastError();
     if (err == cudaSuccess && fp.n_ks > 1) {
         csenc::frm::cs_frame_reduce_kernel<<<f->sms * 4, 256, 0, st>>>(part, y, ny, fp.part_stride, fp.n_ks);
         err = cudaGetLastError();

@@ -40,7 +40,7 @@ constexpr uint32_t kOffB = 1024;                 // two residual (B operand) buf
 
 struct FParams {
     CUtensorMap fmap;         // frames: 2-D [n_seq*T rows][n bytes], box [nf_box][64], SWIZZLE_64B
-    CUtensorMap amap;         // A (permuted): 2-D [m rows][n fp16], box [256][64], SWIZZLE_128B
+    CUtensorMap amap;         // A (permuted): 2-D [m rows][n fp16], box [256 / CL][64], SWIZZLE_128B
     float* out;               // y [n_seq*cs_s][m] (n_ks == 1) or partials [n_ks][n_seq*cs_s][m]
     int n, m, G, T, cs_s;     // pixels, measurements, GOP, frames/stream, CS frames/stream
     int gw, nf_box;           // GOPs per window, frame rows per box (= gw * G)
@@ -51,7 +51,8 @@ struct FParams {
     int n_units;
     uint32_t fbox_bytes, off_a, stage_bytes;
     uint32_t b_bytes;         // one residual buffer: roundup(window CS rows * 128, 1024)
-    uint32_t off_stage;       // kOffB + 2 * b_bytes
+    int n_b;                  // residual buffers (2..4)
+    uint32_t off_stage;       // kOffB + n_b * b_bytes
     int n_stages;
     long long part_stride;    // floats per partial plane (n_seq * cs_s * m rounded up to 4)
     int prefetch;             // frame boxes prefetched into L2 this many chunks ahead (0 = off)
@@ -68,12 +69,29 @@ struct FUnit {
     int s, g0, ngops, n_cs, cs0, mp, ks, kc0, kc1;
 };
 
-__device__ __forceinline__ void decode_funit(const FParams& p, int u, FUnit& w) {
-    // u = (ks * n_win + win) * n_mp + mp: CTAs running together share the K range and window
+// CL CTAs (a cluster) work on one unit = (K split, window group, m-pair) together: CTA `rank` of
+// the cluster takes window group * CL + rank (a window past the end is an empty dummy that still
+// loads and multicasts its share of A).
+template <int CL>
+__device__ __forceinline__ void decode_funit(const FParams& p, int u, int rank, FUnit& w) {
+    // u = (ks * n_grp + grp) * n_mp + mp: clusters running together share the K range
     w.mp = u % p.n_mp;
     const int r = u / p.n_mp;
-    const int win = r % p.n_win;
-    w.ks = r / p.n_win;
+    const int n_grp = (p.n_win + CL - 1) / CL;
+    const int grp = r % n_grp;
+    w.ks = r / n_grp;
+    const int win = grp * CL + rank;
+    const int per = (p.n_chunks + p.n_ks - 1) / p.n_ks;
+    w.kc0 = w.ks * per;
+    w.kc1 = min(p.n_chunks, w.kc0 + per);
+    if (win >= p.n_win) {
+        w.s = 0;
+        w.g0 = 0;
+        w.ngops = 0;
+        w.n_cs = 0;
+        w.cs0 = 0;
+        return;
+    }
     if (p.global_win) {
         // every stream is whole GOPs: GOP gg of the concatenation starts at frame row gg * G and
         // its CS frames are global CS rows gg * (G-1) ... (stream offsets included)
@@ -91,11 +109,9 @@ __device__ __forceinline__ void decode_funit(const FParams& p, int u, FUnit& w) 
         w.n_cs = (t_end - w.g0 * p.G) - w.ngops;        // frames in the window minus its keys
     }
     w.cs0 = w.g0 * (p.G - 1);
-    const int per = (p.n_chunks + p.n_ks - 1) / p.n_ks;
-    w.kc0 = w.ks * per;
-    w.kc1 = min(p.n_chunks, w.kc0 + per);
 }
 
+template <int CL>
 __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __grid_constant__ FParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t sbase = (ptx::smem_addr(smem_raw) + 1023u) & ~1023u;
@@ -104,18 +120,21 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
 
     const uint32_t bar_full = sbase;                      // [kMaxStages] TMA -> converters, MMA
     const uint32_t bar_empty = sbase + 8 * kMaxStages;    // [kMaxStages] MMA -> producer
-    const uint32_t bar_conv = sbase + 16 * kMaxStages;    // [2] converters -> MMA (B buffer written)
-    const uint32_t bar_bempty = bar_conv + 16;            // [2] MMA -> converters (B buffer free)
-    const uint32_t bar_dfull = bar_bempty + 16;
+    const uint32_t bar_conv = sbase + 16 * kMaxStages;    // [4] converters -> MMA (B buffer written)
+    const uint32_t bar_bempty = bar_conv + 32;            // [4] MMA -> converters (B buffer free)
+    const uint32_t bar_dfull = bar_bempty + 32;
     const uint32_t bar_dempty = bar_dfull + 8;
     const uint32_t tmem_slot = bar_dempty + 8;
 
+    const int rank = CL > 1 ? (int)ptx::cluster_ctarank() : 0;
+    const int cid = (int)blockIdx.x / CL, n_cl = (int)gridDim.x / CL;
+    constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
     if (threadIdx.x == 0) {
         for (int i = 0; i < p.n_stages; ++i) {
             ptx::mbar_init(bar_full + 8 * i, 1);
-            ptx::mbar_init(bar_empty + 8 * i, 1);
+            ptx::mbar_init(bar_empty + 8 * i, CL);   // every CTA's MMAs must be done with the (shared) A tile
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < 4; ++i) {
             ptx::mbar_init(bar_conv + 8 * i, kConvWarps);
             ptx::mbar_init(bar_bempty + 8 * i, 1);
         }
@@ -132,7 +151,10 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         ptx::prefetch_tmap(&p.amap);
     }
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CL > 1)
+        ptx::cluster_sync();   // peers' barriers initialised before any multicast lands in them
+    else
+        __syncthreads();
     ptx::tc_fence_after();
     uint32_t tmem_base;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem_base) : "r"(tmem_slot));
@@ -141,9 +163,9 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         // ================================================================ producer
         int st = 0, ntr = 0;
         uint32_t ph = 0;
-        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        for (int u = cid; u < p.n_units; u += n_cl) {
             FUnit w;
-            decode_funit(p, u, w);
+            decode_funit<CL>(p, u, rank, w);
             const int row0 = w.s * p.T + w.g0 * p.G;
             if (lane == 0)   // frames stream from HBM: pull the first boxes of the unit into L2 early
                 for (int kc = w.kc0; kc < min(w.kc1, w.kc0 + p.prefetch); ++kc)
@@ -154,9 +176,17 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                     ptx::tma_prefetch_2d(&p.fmap, (kc + p.prefetch) * kKc, row0);
                 if (lane == 0) {
                     const uint32_t sf = sbase + p.off_stage + (uint32_t)st * p.stage_bytes;
-                    ptx::mbar_arrive_expect_tx(bar_full + 8 * st, p.fbox_bytes + 256u * kKc * 2u);
-                    ptx::tma_load_2d(sf, &p.fmap, bar_full + 8 * st, kc * kKc, row0);
-                    ptx::tma_load_2d(sf + p.off_a, &p.amap, bar_full + 8 * st, kc * kKc, w.mp * 256);
+                    const bool has = w.n_cs > 0;
+                    ptx::mbar_arrive_expect_tx(bar_full + 8 * st, (has ? p.fbox_bytes : 0u) + 256u * kKc * 2u);
+                    if (has) ptx::tma_load_2d(sf, &p.fmap, bar_full + 8 * st, kc * kKc, row0);
+                    if constexpr (CL == 1) {
+                        ptx::tma_load_2d(sf + p.off_a, &p.amap, bar_full + 8 * st, kc * kKc, w.mp * 256);
+                    } else {
+                        // this CTA's share of the 256-row A tile, multicast to every CTA of the cluster
+                        constexpr int kRows = 256 / CL;
+                        ptx::tma_load_2d_mc(sf + p.off_a + (uint32_t)(rank * kRows * kKc * 2), &p.amap, bar_full + 8 * st,
+                                            kc * kKc, w.mp * 256 + rank * kRows, kMask);
+                    }
                     ftrace(p, 0, ntr);
                 }
                 ++ntr;
@@ -182,27 +212,35 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         }
         int st = 0, b = 0, ntr = 0;
         uint32_t ph = 0, bph = 0;
-        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        for (int u = cid; u < p.n_units; u += n_cl) {
             FUnit w;
-            decode_funit(p, u, w);
+            decode_funit<CL>(p, u, rank, w);
             for (int kc = w.kc0; kc < w.kc1; ++kc) {
                 ptx::mbar_wait(bar_full + 8 * st, ph);
                 if (tid == 0) ftrace(p, 1, ntr);
                 ptx::mbar_wait(bar_bempty + 8 * b, bph ^ 1u);
                 const uint32_t sf = sbase + p.off_stage + (uint32_t)st * p.stage_bytes;
                 const uint32_t sb = sbase + kOffB + (uint32_t)b * p.b_bytes;
+                // all loads first (rows past the window read row 0: harmless, not stored), then convert
+                uint2 fv[8], kv[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int c = (tid >> 3) + 32 * i;
+                    const uint32_t rr = c < w.n_cs ? rows[i] : 0u;
+                    const uint32_t t = rr & 0xFFFFu, k = rr >> 16;
+                    // SWIZZLE_64B box rows of 64 B: 16-B chunk (q/2) ^ ((row/2) & 3), 8-B half q & 1
+                    const uint32_t ct = t * 64u + ((((uint32_t)(q >> 1)) ^ ((t >> 1) & 3u)) << 4) + (uint32_t)(q & 1) * 8u;
+                    const uint32_t ck = k * 64u + ((((uint32_t)(q >> 1)) ^ ((k >> 1) & 3u)) << 4) + (uint32_t)(q & 1) * 8u;
+                    fv[i] = ptx::lds64(sf + ct);
+                    kv[i] = ptx::lds64(sf + ck);
+                }
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     const int c = (tid >> 3) + 32 * i;
                     if (c < w.n_cs) {
-                        const uint32_t t = rows[i] & 0xFFFFu, k = rows[i] >> 16;
-                        // SWIZZLE_64B box rows of 64 B: 16-B chunk (q/2) ^ ((row/2) & 3), 8-B half q & 1
-                        const uint32_t ct = t * 64u + ((((uint32_t)(q >> 1)) ^ ((t >> 1) & 3u)) << 4) + (uint32_t)(q & 1) * 8u;
-                        const uint32_t ck = k * 64u + ((((uint32_t)(q >> 1)) ^ ((k >> 1) & 3u)) << 4) + (uint32_t)(q & 1) * 8u;
-                        const uint2 fv = ptx::lds64(sf + ct), kv = ptx::lds64(sf + ck);
                         uint32_t w0, w1, w2, w3;
-                        ptx::residual4(fv.x, kv.x, w0, w1);
-                        ptx::residual4(fv.y, kv.y, w2, w3);
+                        ptx::residual4(fv[i].x, kv[i].x, w0, w1);
+                        ptx::residual4(fv[i].y, kv[i].y, w2, w3);
                         // SWIZZLE_128B B rows of 128 B: 16-B chunk q ^ (c & 7)
                         ptx::sts128(sb + (uint32_t)c * 128u + ((uint32_t)(q ^ (c & 7)) << 4), w0, w1, w2, w3);
                     }
@@ -216,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                     st = 0;
                     ph ^= 1u;
                 }
-                if (++b == 2) {
+                if (++b == p.n_b) {
                     b = 0;
                     bph ^= 1u;
                 }
@@ -228,9 +266,9 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         // hundreds of chunks long, the epilogue a few thousand cycles)
         int st = 0, b = 0, ntr = 0;
         uint32_t ph = 0, bph = 0, dph = 0;
-        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        for (int u = cid; u < p.n_units; u += n_cl) {
             FUnit w;
-            decode_funit(p, u, w);
+            decode_funit<CL>(p, u, rank, w);
             const uint32_t nmma = (uint32_t)((w.n_cs + 15) & ~15);
             const uint32_t idesc = (1u << 4) | ((nmma >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
             const bool two = (w.mp * 256 + 128) < p.m;          // second m-tile has rows
@@ -247,12 +285,16 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                     const uint64_t bd = ptx::smem_desc_swizzled(sbase + kOffB + (uint32_t)b * p.b_bytes, 128u, 1024u);
 #pragma unroll
                     for (int ks = 0; ks < kKc / 16; ++ks) {   // K = 16 per MMA: +32 B inside the SW128 rows
+                        if (nmma == 0) break;                   // empty dummy window (cluster padding)
                         const uint32_t acc = (kc != w.kc0 || ks != 0) ? 1u : 0u;
                         ptx::mma_f16_ss(tmem_base, a0 + (uint64_t)(ks * 2), bd + (uint64_t)(ks * 2), idesc, acc);
                         if (two)
                             ptx::mma_f16_ss(tmem_base + 256u, a1 + (uint64_t)(ks * 2), bd + (uint64_t)(ks * 2), idesc, acc);
                     }
-                    ptx::tc_commit(bar_empty + 8 * st);
+                    if constexpr (CL == 1)
+                        ptx::tc_commit(bar_empty + 8 * st);
+                    else
+                        ptx::tc_commit_mc(bar_empty + 8 * st, kMask);   // frees the stage in every CTA
                     ptx::tc_commit(bar_bempty + 8 * b);
                     if (kc == w.kc1 - 1) ptx::tc_commit(bar_dfull);
                     ftrace(p, 3, ntr);
@@ -263,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                     st = 0;
                     ph ^= 1u;
                 }
-                if (++b == 2) {
+                if (++b == p.n_b) {
                     b = 0;
                     bph ^= 1u;
                 }
@@ -275,9 +317,9 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         const int ew = warp - kEpiWarp0;   // == warp % 4: TMEM lanes 32 ew .. 32 ew + 31
         const uint32_t lane_bits = (uint32_t)(ew * 32) << 16;
         uint32_t dph = 0;
-        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        for (int u = cid; u < p.n_units; u += n_cl) {
             FUnit w;
-            decode_funit(p, u, w);
+            decode_funit<CL>(p, u, rank, w);
             ptx::mbar_wait(bar_dfull, dph);
             ptx::tc_fence_after();
             for (int half = 0; half < 2; ++half) {
@@ -305,7 +347,10 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
     }
 
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CL > 1)
+        ptx::cluster_sync();   // no CTA exits while a peer may still multicast into it
+    else
+        __syncthreads();
     ptx::tc_fence_after();
     if (warp == kMmaWarp) ptx::tmem_dealloc(tmem_base, kTmemCols);
 }
