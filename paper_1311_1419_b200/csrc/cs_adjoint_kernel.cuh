@@ -55,6 +55,7 @@ struct AParams {
     int n_units;
     uint32_t idesc, b_lbo, a_sbo;
     long long x_floats;
+    uint32_t smem_bytes;      // dynamic SMEM from the aligned base (CSENC_CHECKS)
 };
 
 // Staged store of one pixel row of a warp's 32 blocks: lane r holds its block's 4*CPR floats (w);
@@ -110,6 +111,8 @@ __global__ void __launch_bounds__(kThreads, 1) cs_adjoint_kernel(const __grid_co
         ptx::tmem_relinquish();
     }
     if (warp == kProducerWarp && lane == 0) ptx::prefetch_tmap(&p.ymap);
+    CS_CHECK(kOffStage + (uint32_t)p.n_stages * p.stage_bytes <= p.smem_bytes);
+    CS_CHECK(2u * p.a_bytes + p.chunk_bytes <= p.stage_bytes && p.n_stages <= kMaxStages && p.Nc <= 256);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -236,6 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_adjoint_kernel(const __grid_co
                 for (int pr = 0; pr < rows_per_chunk; ++pr) {
                     const int Y = by * B + nc * rows_per_chunk + pr;
                     float* dst = p.x + ((long long)f * p.H + Y) * p.W + col0;
+                    CS_CHECK(Y >= p.H || valid <= 0 || ((long long)f * p.H + Y) * p.W + col0 + valid <= p.x_floats);
                     if constexpr (B == 8) {
                         uint32_t v[8];
                         ptx::tmem_ld_32x32b_x8(d_tm + (uint32_t)(pr * B), v);

@@ -452,6 +452,7 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.trace = e->trace;
     kp.trace_cap = e->trace_cap;
     kp.keys = q.keys;
+    kp.keys_bytes = (long long)n_seq * cdiv(T, g.G) * g.W * g.H;
     kp.chained = q.chained;
     kp.phis = (const uint16_t*)e->phis_dev;
     kp.n_phis = e->n_phis;
@@ -636,6 +637,7 @@ int launch_adjoint(cs_encoder* e, const float* meas, long long n_frames, float* 
     ap.b_lbo = (uint32_t)ap.Nc * 16u;
     ap.a_sbo = 8u * (uint32_t)ap.Kc * 4u;
     ap.x_floats = n_frames * (long long)g.W * g.H;
+    ap.smem_bytes = e->adj_smem - 1024;
     const int grid = std::max(1, std::min(e->sms, ap.n_units));
     switch (g.B) {
         case 8: csenc::adj::cs_adjoint_kernel<8><<<grid, csenc::adj::kThreads, e->adj_smem, stream>>>(ap); break;
@@ -1206,6 +1208,8 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     fp.prefetch = env_int("CSENC_FRAME_PREFETCH", 0);
     fp.trace = f->trace;
     fp.trace_cap = f->trace_cap;
+    fp.out_floats = (long long)n_seq * cs_s * f->m;
+    fp.smem_bytes = smem - 1024;
     const long long ny = (long long)n_seq * cs_s * f->m;
     float* part = nullptr;
     cudaError_t err;

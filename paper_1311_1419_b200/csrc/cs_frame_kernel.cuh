@@ -58,6 +58,8 @@ struct FParams {
     int prefetch;             // frame boxes prefetched into L2 this many chunks ahead (0 = off)
     unsigned long long* trace;   // debug timeline (CTA 0): [4][trace_cap] clock64, nullptr = off
     int trace_cap;
+    long long out_floats;     // floats in one output plane (y, or one partial plane) (CSENC_CHECKS)
+    uint32_t smem_bytes;      // dynamic SMEM from the aligned base (CSENC_CHECKS)
 };
 
 // trace events: 0 producer issued, 1 converter data landed, 2 converter done, 3 MMA issued
@@ -150,6 +152,8 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         ptx::prefetch_tmap(&p.fmap);
         ptx::prefetch_tmap(&p.amap);
     }
+    CS_CHECK(p.off_stage + (uint32_t)p.n_stages * p.stage_bytes <= p.smem_bytes && p.n_stages <= kMaxStages);
+    CS_CHECK(p.off_a + 256u * kKc * 2u <= p.stage_bytes && p.fbox_bytes <= p.off_a && p.n_b <= 4);
     ptx::tc_fence_before();
     if constexpr (CL > 1)
         ptx::cluster_sync();   // peers' barriers initialised before any multicast lands in them
@@ -238,6 +242,8 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                 for (int i = 0; i < 8; ++i) {
                     const int c = (tid >> 3) + 32 * i;
                     if (c < w.n_cs) {
+                        CS_CHECK((rows[i] & 0xFFFFu) < (uint32_t)p.nf_box && (rows[i] >> 16) < (uint32_t)p.nf_box);
+                        CS_CHECK((uint32_t)(c + 1) * 128u <= p.b_bytes);
                         uint32_t w0, w1, w2, w3;
                         ptx::residual4(fv[i].x, kv[i].x, w0, w1);
                         ptx::residual4(fv[i].y, kv[i].y, w2, w3);
@@ -332,6 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                     uint32_t v[32];
                     ptx::tmem_ld_32x32b_x32(d_tm + (uint32_t)j0, v);
                     ptx::tc_wait_ld();
+                    CS_CHECK(i >= p.m || ((long long)w.s * p.cs_s + w.cs0 + w.n_cs - 1) * p.m + i < p.out_floats);
                     if (i < p.m) {
 #pragma unroll
                         for (int k = 0; k < 32; ++k)

@@ -19,6 +19,8 @@
 
 #include <cstdint>
 
+#include "ptx_sm100.cuh"   // CS_CHECK
+
 namespace csenc {
 namespace kc {
 
@@ -168,6 +170,7 @@ __global__ void __launch_bounds__(kThreads, 3) cs_key_codec_kernel(const __grid_
         int qrow[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) qrow[u] = tile[r * 9 + u];
+        CS_CHECK(!valid || gb * 64 + r * 8 + 8 <= p.n_blocks * 64);
         if (valid && p.coef != nullptr) {
             uint4 o;
             o.x = (uint32_t)(qrow[0] & 0xFFFF) | ((uint32_t)qrow[1] << 16);
@@ -200,6 +203,8 @@ __global__ void __launch_bounds__(kThreads, 3) cs_key_codec_kernel(const __grid_
         __syncwarp();
         // ---- decoded row y = r out (cropped to H; W % 16 == 0 so the row is whole)
         const int Yo = by8 * 8 + r;
+        CS_CHECK(!valid || Yo >= p.H ||
+                 (long long)kk * frame_bytes + (long long)Yo * p.W + bx8 * 8 + 8 <= (p.n_blocks / per_key) * (long long)frame_bytes);
         if (valid && Yo < p.H) {
             uint2 w;
             w.x = (uint32_t)tile[r * 9 + 0] | ((uint32_t)tile[r * 9 + 1] << 8) | ((uint32_t)tile[r * 9 + 2] << 16) |

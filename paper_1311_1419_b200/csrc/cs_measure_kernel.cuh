@@ -37,21 +37,7 @@
 #ifndef CSENC_DEBUG
 #define CSENC_DEBUG 0  // 1: compile the ablation switches (KParams::dbg_*) into the kernel
 #endif
-#ifndef CSENC_CHECKS
-#define CSENC_CHECKS 0  // 1: device-side bounds checks (SMEM, TMEM, global output); trap on violation
-#endif
-#if CSENC_CHECKS
-#define CS_CHECK(cond)                                                                            \
-    do {                                                                                          \
-        if (!(cond)) {                                                                            \
-            printf("CSENC_CHECK failed: %s (block %d thread %d, line %d)\n", #cond, blockIdx.x,    \
-                   threadIdx.x, __LINE__);                                                        \
-            __trap();                                                                             \
-        }                                                                                         \
-    } while (0)
-#else
-#define CS_CHECK(cond) ((void)0)
-#endif
+// CS_CHECK (CSENC_CHECKS builds): see ptx_sm100.cuh
 
 namespace csenc {
 
@@ -130,6 +116,7 @@ struct KParams {
     // `frames`, the north star's pass-through); n_gops_T = ceil(T / G)
     const uint8_t* keys;
     int n_gops_T;
+    long long keys_bytes;     // CSENC_CHECKS: size of `keys`
     // f4 variant (KM == KEY_STREAMED plans only): every CS frame's reference is the previous raw
     // frame (Eq. 3 read literally: D_N = F_N - F_{N-1}) instead of the GOP key
     int chained;
@@ -193,7 +180,10 @@ __device__ __forceinline__ void load_strips(const KParams& p, uint32_t dst, cons
         const int y0 = p.single_piece ? t * p.T_r * B : (t * p.T_r + pc) * B + k * p.chunk_rows;
         const int rows = max(0, min(p.piece_rows, p.H - y0));
         const uint32_t d = dst + (uint32_t)pc * p.piece_bytes;
-        CS_CHECK(rows == 0 || (long long)(frame - p.frames) + (long long)y0 * p.W + (long long)rows * p.W <= p.frames_bytes);
+        CS_CHECK(rows == 0 ||
+                 (frame >= p.frames && (long long)(frame - p.frames) + (long long)(y0 + rows) * p.W <= p.frames_bytes) ||
+                 (p.keys != nullptr && frame >= p.keys &&
+                  (long long)(frame - p.keys) + (long long)(y0 + rows) * p.W <= p.keys_bytes));
         CS_CHECK(rows >= p.piece_rows || (uint32_t)(p.piece_rows - rows) * p.W <= p.smem_bytes);
         if (rows > 0) ptx::bulk_load_hint(d, frame + (size_t)y0 * p.W, (uint32_t)rows * p.W, bar, policy);
         if (rows < p.piece_rows)
@@ -890,6 +880,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(am) : "l"(p.amax + cs) : "memory");
                 }
                 am = __shfl_sync(0xFFFFFFFFu, am, 0);
+                CS_CHECK((cs + 1) * p.nblk * (long long)p.M <= p.out_floats);
                 if (tr) trace_ev(p, EV_C_AEMPTY, n_items);   // look-back wait done
                 const float inv = q16_inv(q16_scale(am));
                 if (t == 0 && ew == 0 && lane == 0) p.scales[cs] = q16_scale(am);
@@ -1064,6 +1055,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                             const int r = (int)((rowpack >> (6 * f)) & 63u);
                             const int rlo = (int)((lopack >> (6 * f)) & 63u);
                             const int rhi = (int)((hipack >> (6 * f)) & 63u);
+                            CS_CHECK(rhi < kRowSlots);
                             for (int rr = rlo; rr <= rhi; ++rr) {
                                 const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, r == rr ? mf : 0u);
                                 if (lane == 0 && m != 0) ptx::atom_smem_max(slots + (uint32_t)rr * 4u, m);

@@ -4,6 +4,25 @@
 // cuda/__ptx/instructions/generated/{mbarrier_*,cp_async_bulk*,tcgen05_*}.h.
 #pragma once
 #include <cstdint>
+#include <cstdio>
+
+// Device-side bounds checks (the memory-safety gate on a pool without compute-sanitizer): a
+// CSENC_CHECKS=1 build traps with a message on any violated SMEM / TMEM / global-memory bound.
+#ifndef CSENC_CHECKS
+#define CSENC_CHECKS 0
+#endif
+#if CSENC_CHECKS
+#define CS_CHECK(cond)                                                                            \
+    do {                                                                                          \
+        if (!(cond)) {                                                                            \
+            printf("CSENC_CHECK failed: %s (block %d thread %d, line %d)\n", #cond, blockIdx.x,    \
+                   threadIdx.x, __LINE__);                                                        \
+            __trap();                                                                             \
+        }                                                                                         \
+    } while (0)
+#else
+#define CS_CHECK(cond) ((void)0)
+#endif
 
 namespace csenc {
 namespace ptx {

@@ -1,7 +1,9 @@
 """Bounds-checked kernel build (CSENC_CHECKS=1: every bulk copy, converter SMEM read, TMEM column
 range and output store is range-checked on the device; a violation traps).  compute-sanitizer is
 not available on the GPU pool, so this is the memory-safety gate: small cases covering every
-block size, key mode, folds, partial blocks and ragged GOPs, for the top plans of each."""
+block size, key mode, folds, partial blocks and ragged GOPs for the top plans of each, every q16
+mode, closed-loop / chained keys, per-GOP Phi, the adjoint and the frame-level GEMM (single CTA,
+2-CTA cluster, split-K) -- tools/sanitize_cases.py."""
 import os
 import subprocess
 import sys
@@ -19,7 +21,8 @@ def test_bounds_checked_build_runs_clean():
         pytest.skip("needs a CUDA device")
     from paper_1311_1419_b200 import _build
     lib = os.path.join(_build.LIB_DIR, "libcsenc_checks.so")
-    if not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(os.path.join(_build.CSRC, "cs_measure_kernel.cuh")):
+    deps = [os.path.join(_build.CSRC, f) for f in os.listdir(_build.CSRC)]
+    if not os.path.exists(lib) or os.path.getmtime(lib) < max(os.path.getmtime(d) for d in deps):
         _build.build(out=lib, defines=("CSENC_CHECKS=1",))
     env = dict(os.environ, CSENC_LIB=lib)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sanitize_cases.py")], env=env,
