@@ -133,8 +133,7 @@ int cs_encode_gop(cs_encoder* enc, const uint8_t* frames_dev, int n_frames, floa
 /* Encode n_seq independent streams of T frames each: frames_dev = DEVICE [n_seq][T][H][W]
  * uint8; meas_dev = DEVICE fp32, cs_measurement_count(enc, n_seq, T) floats, layout above.
  * ONE kernel launch covers every GOP of every stream (persistent grid of one CTA per SM).
- * No allocation (graph-capturable after the first call for a given (frames_dev, n_seq, T),
- * which encodes and caches the TMA descriptor on the host). */
+ * No allocation and no host synchronisation: capturable in a CUDA graph (tests/test_gpu_graph.py). */
 int cs_encode_batch(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, int T, float* meas_dev,
                     cs_stream_t stream);
 
