@@ -403,6 +403,7 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.T_r = pl.T_r;
     kp.F = pl.F;
     kp.L = pl.L;
+    kp.Lq = env_int("CSENC_LANE_SPREAD", 1) ? (pl.L + 3) / 4 : 32;   // spread the tile's lanes over the 4 quarters
     kp.n_tiles = pl.n_tiles;
     kp.chunk_rows = pl.chunk_rows;
     kp.n_chunks = pl.n_chunks;

@@ -88,6 +88,8 @@ struct KParams {
     int nbx, nby, nblk;
     // tiling
     int T_r, F, L, n_tiles;
+    int Lq;                   // logical lanes per TMEM lane quarter: physical lane 32q + r holds logical
+                              // lane q*Lq + r (r < Lq), so small tiles use all four SM sub-partitions
     int chunk_rows, n_chunks, chunk_k;
     int pieces;               // strips per stage: 1 (all T_r*B rows, n_chunks == 1) or T_r
     int piece_rows;           // rows per strip
@@ -435,11 +437,12 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         // Per (fold, lane) table: byte offset of the lane's block (its row 0 in the chunk) inside
         // a stage, and meta = row offset of the block within the tile | B=32 right-half-valid
         // (bit 16) | lane-valid (bit 17).
-        const int lane_idx = threadIdx.x;
+        const int lane_idx = threadIdx.x;                            // physical TMEM lane
+        const int lq = (lane_idx >> 5) * p.Lq + (lane_idx & 31);     // logical lane
         for (int f = 0; f < p.F; ++f) {
             uint32_t off = 0, meta = 0;
-            const int b = f * p.L + lane_idx;
-            if (lane_idx < p.L && b < p.T_r * p.nbx) {
+            const int b = f * p.L + lq;
+            if ((lane_idx & 31) < p.Lq && lq < p.L && b < p.T_r * p.nbx) {
                 const int brow = b / p.nbx, bx = b - brow * p.nbx;
                 const int pc = p.single_piece ? 0 : brow;
                 const int row = p.single_piece ? brow * B : 0;
@@ -836,8 +839,8 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         uint64_t rowpack = 0, lopack = 0, hipack = 0;
         if (qmode == Q_ROW) {
             for (int f = 0; f < p.F; ++f) {
-                const int b = f * p.L + lane_idx;
-                const bool ok = lane_idx < p.L && b < p.T_r * p.nbx;
+                const int b = f * p.L + ew * p.Lq + (int)lane;
+                const bool ok = (int)lane < p.Lq && ew * p.Lq + (int)lane < p.L && b < p.T_r * p.nbx;
                 const uint32_t r = ok ? (uint32_t)(b / p.nbx) : 63u;
                 const uint32_t lo = __reduce_min_sync(0xFFFFFFFFu, r);
                 const uint32_t hi = __reduce_max_sync(0xFFFFFFFFu, ok ? r : 0u);
@@ -887,10 +890,10 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                 const uint32_t d_tm = tmem_base + lane_bits + d_col0 + (uint32_t)qdb * (uint32_t)p.d_cols;
                 int16_t* const codes_cs = p.codes + (cs * p.nblk + blk0) * (long long)p.M;
                 for (int f = 0; f < p.F; ++f) {
-                    const int row0 = f * p.L + ew * 32;
+                    const int row0 = f * p.L + ew * p.Lq;
                     const int b = row0 + (int)lane;
-                    const bool valid = lane_idx < p.L && b < blocks_here;
-                    const int rows_valid = min(32, min(p.L - ew * 32, blocks_here - row0));
+                    const bool valid = (int)lane < p.Lq && ew * p.Lq + (int)lane < p.L && b < blocks_here;
+                    const int rows_valid = min(p.Lq, min(p.L - ew * p.Lq, blocks_here - row0));
                     if (smode == 0) {
                         uint32_t v[16];
                         ptx::tmem_ld_32x32b_x16(d_tm + (uint32_t)(f * p.Mpad), v);
@@ -947,8 +950,8 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                 const uint32_t d_tm = tmem_base + lane_bits + d_col0 + (uint32_t)db * (uint32_t)p.d_cols;
                 float mff = 0.0f;
                 for (int f = 0; f < p.F; ++f) {
-                    const int b = f * p.L + lane_idx;
-                    const bool valid = lane_idx < p.L && b < blocks_here;
+                    const int b = f * p.L + ew * p.Lq + (int)lane;
+                    const bool valid = (int)lane < p.Lq && ew * p.Lq + (int)lane < p.L && b < blocks_here;
                     float mf = 0.0f;
                     for (int j0 = 0; j0 < p.Mpad; j0 += 32) {
                         uint32_t v[32];
@@ -1030,8 +1033,8 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                                        (uint32_t)lane_idx * 4u, 0u);
                     uint32_t mx = 0;
                     for (int f = 0; f < p.F; ++f) {
-                        const int b = f * p.L + lane_idx;
-                        const bool valid = lane_idx < p.L && b < blocks_here;
+                        const int b = f * p.L + ew * p.Lq + (int)lane;
+                        const bool valid = (int)lane < p.Lq && ew * p.Lq + (int)lane < p.L && b < blocks_here;
                         float mff = 0.0f;
                         for (int j0 = 0; j0 < p.Mpad; j0 += 32) {
                             uint32_t v[32];
@@ -1081,10 +1084,10 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                     }
                     int16_t* const codes_cs = p.codes + (cs_global * p.nblk + blk0) * (long long)p.M;
                     for (int f = 0; f < p.F; ++f) {
-                        const int row0 = f * p.L + ew * 32;
+                        const int row0 = f * p.L + ew * p.Lq;
                         const int b = row0 + (int)lane;
-                        const bool valid = lane_idx < p.L && b < blocks_here;
-                        const int rows_valid = min(32, min(p.L - ew * 32, blocks_here - row0));
+                        const bool valid = (int)lane < p.Lq && ew * p.Lq + (int)lane < p.L && b < blocks_here;
+                        const int rows_valid = min(p.Lq, min(p.L - ew * p.Lq, blocks_here - row0));
                         if (qmode == Q_ROW) {
                             const int r = (int)((rowpack >> (6 * f)) & 63u);
                             if (r != inv_row) {   // rows only grow with f: at most rows-per-tile updates
@@ -1177,10 +1180,10 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                 CS_CHECK(d_col0 + (uint32_t)(db + 1) * (uint32_t)p.d_cols <= kTmemCols);
                 CS_CHECK((cs_global + 1) * p.nblk * (long long)p.M <= p.out_floats);
                 for (int f = 0; f < p.F; ++f) {
-                    const int row0 = f * p.L + ew * 32;            // tile block of this warp's lane 0
+                    const int row0 = f * p.L + ew * p.Lq;            // tile block of this warp's lane 0
                     const int b = row0 + (int)lane;
-                    const bool valid = lane_idx < p.L && b < blocks_here;
-                    const int rows_valid = min(32, min(p.L - ew * 32, blocks_here - row0));
+                    const bool valid = (int)lane < p.Lq && ew * p.Lq + (int)lane < p.L && b < blocks_here;
+                    const int rows_valid = min(p.Lq, min(p.L - ew * p.Lq, blocks_here - row0));
                     if (mode == 0) {
                         uint32_t v[16];
                         ptx::tmem_ld_32x32b_x16(d_tm + (uint32_t)(f * p.Mpad), v);
