@@ -51,3 +51,29 @@ def shard_streams(n_streams: int, world: int, rank: int):
     base, extra = divmod(n_streams, world)
     s0 = rank * base + min(rank, extra)
     return s0, s0 + base + (1 if rank < extra else 0)
+
+
+def gather_measurements(local, dst: int = 0, group=None):
+    """Optional payload gather to one sink (off the encode path): every rank's
+    measurement shard (a tensor whose leading dimension is CS frames, same trailing shape on all
+    ranks, possibly empty) is concatenated on rank `dst` in rank order -- with shard_gops /
+    shard_streams that is the single-device output order.  Works with NCCL (CUDA tensors, over
+    NVLink) and gloo (CPU).  Returns the concatenation on `dst`, None on the other ranks."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n = torch.tensor([local.shape[0]], dtype=torch.int64, device=local.device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(s.item()) for s in sizes]
+    mx = max(sizes)
+    pad = torch.zeros((mx,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    if local.shape[0]:
+        pad[: local.shape[0]] = local
+    bufs = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
+    dist.gather(pad, bufs, dst=dst, group=group)
+    if rank != dst:
+        return None
+    return torch.cat([b[:k] for b, k in zip(bufs, sizes)], dim=0)

@@ -24,6 +24,38 @@ def _free_port():
     return p
 
 
+def _gather_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = synth.CONFIGS["C2"].with_(T=21, W=48, H=32)
+    frames = synth.gen_stream(cfg, 0)
+    phi = synth.phi_from_seed(5, cfg.M, cfg.B ** 2)
+    g0, g1 = pdist.shard_gops(cfg.T, cfg.G, world, rank)
+    y_local, _ = oracle.encode_stream(frames[g0 * cfg.G:min(g1 * cfg.G, cfg.T)], phi, cfg.G, cfg.B, with_scale=False)
+    got = pdist.gather_measurements(torch.from_numpy(y_local), dst=0)
+    if rank == 0:
+        y_all, _ = oracle.encode_stream(frames, phi, cfg.G, cfg.B, with_scale=False)
+        q.put(bool(np.array_equal(got.numpy(), y_all)))
+    else:
+        q.put(got is None)
+    dist.destroy_process_group()
+
+
+def test_gather_measurements_two_ranks():
+    """dist.gather_measurements reassembles GOP-range shards (uneven sizes) on rank 0."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res), res
+
+
 def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
