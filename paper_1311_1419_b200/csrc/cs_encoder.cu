@@ -1,10 +1,10 @@
-// cs_encoder.cu -- libcsenc.so: C ABI (include/cs_encoder.h), planner, TMA descriptors, launch.
+// cs_encoder.cu -- libcsenc.so, the north-star path (K1): planner, launch and the C ABI of the
+// block-based encoder (create/destroy, autotune, encode calls and their f1 / f4 variants, the
+// host-buffer pipeline, CR accounting).  The f2 / f3 / f4-codec host code is in cs_frame.cu,
+// cs_adjoint.cu and cs_keys.cu; shared declarations in cs_internal.h.
 //
-// Host logic only; the device work is the single kernel in cs_measure_kernel.cuh.  No CPU
-// fallback exists: every encode runs the sm_100a kernel or returns an error.
-#include <cuda.h>
-#include <cuda_runtime.h>
-
+// Host logic only; the device work is the kernel in cs_measure_kernel.cuh.  No CPU fallback exists:
+// every encode runs the sm_100a kernel or returns an error.
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -15,58 +15,15 @@
 #include <string>
 #include <vector>
 
-#include "../../include/cs_encoder.h"
+#include "cs_internal.h"
 #include "cs_measure_kernel.cuh"
-#include "cs_adjoint_kernel.cuh"
-#include "cs_key_codec_kernel.cuh"
-#include "cs_frame_kernel.cuh"
 
 using csenc::KParams;
 
-namespace {
-
-thread_local std::string g_err;
-
-int fail(int code, const std::string& msg) {
-    g_err = msg;
-    return code;
-}
-int cuda_fail(cudaError_t e, const char* what) {
-    return fail(CS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
-}
+namespace csenc {
+namespace host {
 
 constexpr long kMaxPhiBytes = 160 * 1024;  // Phi is SMEM-resident for the whole kernel
-
-inline int cdiv(int a, int b) { return (a + b - 1) / b; }
-inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
-
-float half_bits_to_float(uint16_t h) {
-    uint32_t s = (h >> 15) & 1u, e = (h >> 10) & 0x1Fu, m = h & 0x3FFu;
-    float v;
-    if (e == 0)
-        v = std::ldexp((float)m, -24);
-    else if (e == 31)
-        v = m ? NAN : INFINITY;
-    else
-        v = std::ldexp((float)(m | 0x400u), (int)e - 25);
-    return s ? -v : v;
-}
-
-// ------------------------------------------------------------------------------------ planner
-struct Plan {
-    int T_r = 0, F = 0, L = 0, n_tiles = 0;
-    int chunk_rows = 0, n_chunks = 0, chunk_k = 0;
-    int pieces = 0, piece_rows = 0, single_piece = 0;
-    uint32_t piece_bytes = 0, stage_cs_bytes = 0, stage_bytes = 0, key_bytes = 0;
-    int key_resident = 0, key_regs = 0, n_stages = 0, prefetch_items = 0;
-    uint32_t off_tab = 0, off_epi = 0, off_phi = 0, off_key = 0, off_stage = 0, smem_bytes = 0;
-    int a_cols = 0, d_cols = 0, tmem_cols = 0, n_abuf = 2, n_dbuf = 2;
-    double score = -1.0;
-};
-
-struct Geometry {
-    int W, H, G, B, M, N, Mpad, nbx, nby, nblk;
-};
 
 // key_mode: 0 = key strip streamed with every item, 1 = resident in SMEM (double-buffered),
 //           2 = in converter registers (arrives once per unit through a ring slot)
@@ -174,11 +131,6 @@ bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem
     s *= 0.85 + 0.15 * ring_q;
     p.score = s;
     return true;
-}
-
-int env_int(const char* name, int dflt) {
-    const char* v = std::getenv(name);
-    return v ? std::atoi(v) : dflt;
 }
 
 // All feasible plans, best model score first (the autotuner times the first few).
@@ -302,13 +254,6 @@ Geometry make_geometry(int W, int H, int gop, int B, int M) {
     return g;
 }
 
-long long cs_frames_per_stream(int T, int G) { return (long long)T - cdiv(T, G); }
-long long cs_frames_in_gops(int T, int G, int g0, int g1) {
-    long long n = 0;
-    for (int g = g0; g < g1; ++g) n += std::max(0, std::min(G, T - g * G) - 1);
-    return n;
-}
-
 double cr_formula(const Geometry& g, int T, double key_cr, int bits) {
     if (T == 0) T = g.G;
     const long long n_key = cdiv(T, g.G);
@@ -319,50 +264,11 @@ double cr_formula(const Geometry& g, int T, double key_cr, int bits) {
     return orig / (key_bits + meas_bits);
 }
 
-}  // namespace
+}  // namespace host
+}  // namespace csenc
 
 // ====================================================================================== encoder
-struct cs_encoder {
-    Geometry geo{};
-    Plan plan{};
-    int device = 0;
-    int sms = 0;
-    int smem_limit = 0;
-    void* phi_dev = nullptr;
-    uint32_t phi_bytes = 0;
-    uint32_t idesc = 0, lbo = 0, sbo = 0;
-    std::mutex ws_mu;  // host-path workspace
-    // host-path workspace
-    uint8_t* ws_frames = nullptr;
-    float* ws_out = nullptr;
-    size_t ws_frames_bytes = 0, ws_out_bytes = 0;
-    cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
-    std::vector<Plan> candidates;  // planner's ranked plans (autotune)
-    int chained_plan = -1;         // best KEY_STREAMED candidate (previous-frame reference), -1 = none
-    int frame1_plan = -1;          // f1 single-pass plan: D ring >= 2 (look-back lag >= 1), tiles <= SMs; -1 = none
-    Plan frame1{};                 // that candidate with the D ring as deep as TMEM allows (<= 8)
-    void* phis_dev = nullptr;      // per-GOP Phi copies (arranged like phi_dev), n_phis of phi_bytes
-    int n_phis = 0;
-    int tuned = -1;                // index of the autotuned plan, -1 = model choice
-    void* zeros_dev = nullptr;   // piece_rows * W zero bytes: source for frame rows beyond H
-    size_t zeros_bytes = 0;
-    unsigned long long* trace = nullptr;  // device buffer (debug timeline), caller-owned
-    int trace_cap = 0;
-    std::vector<cudaEvent_t> hev;
-    // f3 adjoint (K3): Phi^T chunks (tf32, no-swizzle K-major), plan; phiT_dev == nullptr when M % 4 != 0
-    void* phiT_dev = nullptr;
-    int adj_Kc = 0, adj_n_kc = 0, adj_Nc = 0, adj_n_nc = 0, adj_stages = 0;
-    uint32_t adj_chunk_bytes = 0, adj_stage_bytes = 0, adj_smem = 0;
-};
-
-// f2: frame-level measurement matrix A (m x n, n = W*H) and its geometry
-struct cs_frame_encoder {
-    int W = 0, H = 0, G = 0, m = 0, n = 0;
-    int device = 0, sms = 0, smem_limit = 0;
-    void* A_dev = nullptr;   // fp16 [m][n], columns permuted within groups of 4 (converter pair order)
-    unsigned long long* trace = nullptr;   // debug timeline (cs_frame_encoder_set_trace)
-    int trace_cap = 0;
-};
+using namespace csenc::host;
 
 namespace {
 
@@ -511,16 +417,11 @@ cudaError_t set_smem_attr_all(int bytes) {
     CSENC_ATTR(16, csenc::KEY_STREAMED) CSENC_ATTR(16, csenc::KEY_RESIDENT) CSENC_ATTR(16, csenc::KEY_REGS)
     CSENC_ATTR(32, csenc::KEY_STREAMED) CSENC_ATTR(32, csenc::KEY_RESIDENT)
 #undef CSENC_ATTR
-    r = cudaFuncSetAttribute(csenc::adj::cs_adjoint_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    if (r != cudaSuccess) e = r;
-    r = cudaFuncSetAttribute(csenc::adj::cs_adjoint_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    if (r != cudaSuccess) e = r;
-    r = cudaFuncSetAttribute(csenc::adj::cs_adjoint_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    r = adjoint_set_smem_attr(bytes);
     if (r != cudaSuccess) e = r;
     return e;
 }
 
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // Phi -> canonical no-swizzle K-major UMMA layout, zero-padded to Mpad rows:
 //   byte(n, k) = (k/8)*LBO + (n/8)*SBO + (n%8)*16 + (k%8)*2.
@@ -539,117 +440,6 @@ std::vector<uint16_t> arrange_phi(const Geometry& g, uint32_t lbo, uint32_t sbo,
     return arranged;
 }
 
-// ------------------------------------------------------------------------ f3 adjoint (K3)
-typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-PFN_encodeTiled get_encode_tiled() {
-    static PFN_encodeTiled fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void* ptr = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_encodeTiled>(ptr);
-    });
-    return fn;
-}
-
-// Plan and Phi^T for the adjoint: K chunk Kc (8/16/32 floats = the swizzle span of the Y box),
-// output chunk Nc = min(N, 256) columns; Phi^T chunk (nc, kc) in the no-swizzle K-major tf32 layout
-//   byte(n, k) = (k/4) * LBO + (n/8) * 128 + (n%8) * 16 + (k%4) * 4,  LBO = Nc * 16,
-// value Phi[kc*Kc + k][nc*Nc + n] (0 for k >= M).  Skipped (phiT_dev stays NULL) when M % 4 != 0:
-// the Y rows must be 16-byte multiples for the tensor map.
-int prepare_adjoint(cs_encoder* e, const uint16_t* phi_fp16) {
-    const Geometry& g = e->geo;
-    if (g.M % 4 != 0) return CS_OK;
-    e->adj_Kc = g.M <= 8 ? 8 : (g.M <= 16 ? 16 : 32);
-    e->adj_n_kc = cdiv(g.M, e->adj_Kc);
-    e->adj_Nc = std::min(g.N, 256);
-    e->adj_n_nc = g.N / e->adj_Nc;
-    e->adj_chunk_bytes = (uint32_t)e->adj_Nc * (uint32_t)e->adj_Kc * 4u;
-    const uint32_t a_bytes = 128u * (uint32_t)e->adj_Kc * 4u;
-    e->adj_stage_bytes = align_up(2 * a_bytes + e->adj_chunk_bytes, 1024);
-    const long avail = (long)e->smem_limit - 1024 - (long)csenc::adj::kOffStage;
-    e->adj_stages = (int)std::min<long>(csenc::adj::kMaxStages, avail / (long)e->adj_stage_bytes);
-    if (e->adj_stages < 2) return fail(CS_ERR_UNSUPPORTED, "adjoint: stages do not fit shared memory");
-    e->adj_smem = 1024 + csenc::adj::kOffStage + (uint32_t)e->adj_stages * e->adj_stage_bytes;
-    const size_t bytes = (size_t)e->adj_n_nc * e->adj_n_kc * e->adj_chunk_bytes;
-    std::vector<float> h(bytes / 4, 0.0f);
-    const uint32_t lbo = (uint32_t)e->adj_Nc * 16u;
-    for (int nc = 0; nc < e->adj_n_nc; ++nc)
-        for (int kc = 0; kc < e->adj_n_kc; ++kc) {
-            const size_t base = (size_t)(nc * e->adj_n_kc + kc) * e->adj_chunk_bytes;
-            for (int n = 0; n < e->adj_Nc; ++n)
-                for (int k = 0; k < e->adj_Kc; ++k) {
-                    const int m = kc * e->adj_Kc + k, j = nc * e->adj_Nc + n;
-                    const size_t byte = base + (size_t)(k / 4) * lbo + (size_t)(n / 8) * 128 + (size_t)(n % 8) * 16 +
-                                        (size_t)(k % 4) * 4;
-                    h[byte / 4] = m < g.M ? half_bits_to_float(phi_fp16[(size_t)m * g.N + j]) : 0.0f;
-                }
-        }
-    cudaError_t err = cudaMalloc(&e->phiT_dev, bytes);
-    if (err != cudaSuccess) return fail(CS_ERR_OOM, std::string("cudaMalloc(Phi^T): ") + cudaGetErrorString(err));
-    err = cudaMemcpy(e->phiT_dev, h.data(), bytes, cudaMemcpyHostToDevice);
-    if (err != cudaSuccess) return cuda_fail(err, "cudaMemcpy(Phi^T)");
-    return CS_OK;
-}
-
-int launch_adjoint(cs_encoder* e, const float* meas, long long n_frames, float* x, cudaStream_t stream) {
-    const Geometry& g = e->geo;
-    csenc::adj::AParams ap;
-    std::memset(&ap, 0, sizeof(ap));
-    PFN_encodeTiled enc = get_encode_tiled();
-    if (!enc) return fail(CS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    const long long rows = n_frames * g.nblk;
-    cuuint64_t dims[2] = {(cuuint64_t)g.M, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)g.M * 4u};
-    cuuint32_t box[2] = {(cuuint32_t)e->adj_Kc, 128u};
-    cuuint32_t estr[2] = {1, 1};
-    const CUtensorMapSwizzle sw = e->adj_Kc == 32 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                  : (e->adj_Kc == 16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
-    CUresult r = enc(&ap.ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(meas), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(CS_ERR_CUDA, "cuTensorMapEncodeTiled(y) failed (code " + std::to_string((int)r) + ")");
-    ap.phiT = (const uint8_t*)e->phiT_dev;
-    ap.x = x;
-    ap.W = g.W;
-    ap.H = g.H;
-    ap.M = g.M;
-    ap.nbx = g.nbx;
-    ap.nby = g.nby;
-    ap.nblk = g.nblk;
-    ap.parts = cdiv(g.nbx, 128);
-    ap.L = cdiv(g.nbx, ap.parts);
-    ap.Kc = e->adj_Kc;
-    ap.n_kc = e->adj_n_kc;
-    ap.Nc = e->adj_Nc;
-    ap.n_nc = e->adj_n_nc;
-    ap.a_bytes = 128u * (uint32_t)e->adj_Kc * 4u;
-    ap.chunk_bytes = e->adj_chunk_bytes;
-    ap.stage_bytes = e->adj_stage_bytes;
-    ap.n_stages = e->adj_stages;
-    ap.n_units = (int)(n_frames * g.nby * ap.parts);
-    // kind::tf32: D fp32 (bit 4), A/B tf32 (2 at bits 7 and 10), K-major, N>>3 at 17, M>>4 at 24
-    ap.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(ap.Nc >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-    ap.b_lbo = (uint32_t)ap.Nc * 16u;
-    ap.a_sbo = 8u * (uint32_t)ap.Kc * 4u;
-    ap.x_floats = n_frames * (long long)g.W * g.H;
-    ap.smem_bytes = e->adj_smem - 1024;
-    const int grid = std::max(1, std::min(e->sms, ap.n_units));
-    switch (g.B) {
-        case 8: csenc::adj::cs_adjoint_kernel<8><<<grid, csenc::adj::kThreads, e->adj_smem, stream>>>(ap); break;
-        case 16: csenc::adj::cs_adjoint_kernel<16><<<grid, csenc::adj::kThreads, e->adj_smem, stream>>>(ap); break;
-        case 32: csenc::adj::cs_adjoint_kernel<32><<<grid, csenc::adj::kThreads, e->adj_smem, stream>>>(ap); break;
-        default: return fail(CS_ERR_UNSUPPORTED, "block size");
-    }
-    cudaError_t err = cudaGetLastError();
-    return err == cudaSuccess ? CS_OK : cuda_fail(err, "adjoint launch");
-}
-
 // f1, per-frame scale: amax bits (pass 1) -> fp32 scales in place, after pass 2 has read them.
 __global__ void q16_finalize_kernel(uint32_t* amax, long long n) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -661,8 +451,6 @@ __global__ void q16_finalize_kernel(uint32_t* amax, long long n) {
 // ============================================================================================ ABI
 extern "C" {
 
-const char* cs_last_error(void) { return g_err.c_str(); }
-const char* cs_version(void) { return "csenc 0.1 (sm_100a, tcgen05/TMEM/TMA)"; }
 
 int cs_validate_config(int W, int H, int gop, int B, int M, const uint16_t* phi_fp16) {
     return validate(W, H, gop, B, M, phi_fp16);
@@ -921,63 +709,6 @@ int cs_encode_gop(cs_encoder* e, const uint8_t* frames, int n_frames, float* out
     return cs_encode_batch_gops(e, frames, 1, n_frames, 0, 1, out, stream);
 }
 
-void cs_key_dct_basis(int32_t out[64]) {
-    for (int i = 0; i < 64; ++i) out[i] = csenc::kc::kDctHost[i];
-}
-
-int cs_key_qsteps(double quant_scale, int32_t out[64]) {
-    if (!out) return fail(CS_ERR_ARG, "out is NULL");
-    if (!(quant_scale > 0.0) || !std::isfinite(quant_scale)) return fail(CS_ERR_ARG, "quant_scale must be > 0");
-    for (int i = 0; i < 64; ++i) {
-        const double v = std::nearbyint(quant_scale * csenc::kc::kJpegLuma[i]);  // round half to even
-        out[i] = (int32_t)std::min(4096.0, std::max(1.0, v));
-    }
-    return CS_OK;
-}
-
-int64_t cs_key_coef_count(const cs_encoder* e, int n_seq, int T) {
-    if (!e || n_seq < 0 || T < 0) return -1;
-    const Geometry& g = e->geo;
-    return (int64_t)n_seq * cdiv(T, g.G) * cdiv(g.H, 8) * cdiv(g.W, 8) * 64;
-}
-
-int cs_key_codec(cs_encoder* e, const uint8_t* frames, int n_seq, int T, const int32_t* qsteps, int16_t* coef,
-                 uint8_t* keys, cs_stream_t stream) {
-    if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
-    if (n_seq < 0 || T < 0) return fail(CS_ERR_ARG, "n_seq and T must be >= 0");
-    if (n_seq == 0 || T == 0) return CS_OK;
-    if (!frames || !keys || !qsteps) return fail(CS_ERR_ARG, "NULL buffer");
-    if (!aligned16(frames) || !aligned16(keys) || (coef && !aligned16(coef)))
-        return fail(CS_ERR_ARG, "buffers must be 16-byte aligned");
-    const Geometry& g = e->geo;
-    csenc::kc::KCParams kp;
-    std::memset(&kp, 0, sizeof(kp));
-    for (int i = 0; i < 64; ++i) {
-        if (qsteps[i] < 1 || qsteps[i] > 4096) return fail(CS_ERR_ARG, "quantiser steps must be in [1, 4096]");
-        kp.qsteps[i] = qsteps[i];
-    }
-    kp.frames = frames;
-    kp.coef = coef;
-    kp.keys = keys;
-    kp.W = g.W;
-    kp.H = g.H;
-    kp.T = T;
-    kp.G = g.G;
-    kp.n_gops_T = cdiv(T, g.G);
-    kp.nbx8 = cdiv(g.W, 8);
-    kp.nby8 = cdiv(g.H, 8);
-    kp.n_blocks = (long long)n_seq * kp.n_gops_T * kp.nby8 * kp.nbx8;
-    const long long n_keys = (long long)n_seq * kp.n_gops_T;
-    if (n_keys > 65535 || (long long)kp.nby8 * kp.nbx8 > 0x7FFFFFFFLL)
-        return fail(CS_ERR_UNSUPPORTED, "key codec: more than 65535 key frames in one call");
-    // ~12 CTAs per SM in total (3 resident: 4 waves of slack against imbalance), spread over the keys
-    const int per_key_ctas = (int)((kp.nby8 * (long long)kp.nbx8 + csenc::kc::kThreads / 8 - 1) / (csenc::kc::kThreads / 8));
-    const int gx = (int)std::max(1LL, std::min((long long)per_key_ctas, ((long long)e->sms * 12 + n_keys - 1) / n_keys));
-    csenc::kc::cs_key_codec_kernel<<<dim3(gx, (unsigned)n_keys), csenc::kc::kThreads, 0, (cudaStream_t)stream>>>(kp);
-    const cudaError_t err = cudaGetLastError();
-    return err == cudaSuccess ? CS_OK : cuda_fail(err, "key codec launch");
-}
-
 int cs_encoder_set_gop_phis(cs_encoder* e, int n_phi, const uint16_t* phis) {
     if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
     if (n_phi < 0 || (n_phi > 0 && !phis)) return fail(CS_ERR_ARG, "n_phi must be >= 0 and phis non-NULL");
@@ -1031,234 +762,6 @@ int cs_encode_batch_keys(cs_encoder* e, const uint8_t* frames, int n_seq, int T,
     QArgs q;
     q.keys = keys;
     return launch(e, frames, n_seq, T, 0, cdiv(T, e->geo.G), out, (cudaStream_t)stream, q);
-}
-
-int cs_frame_encoder_create(int W, int H, int gop, int m, const uint16_t* A_fp16, cs_frame_encoder** out) {
-    if (!out) return fail(CS_ERR_ARG, "out is NULL");
-    *out = nullptr;
-    if (!A_fp16) return fail(CS_ERR_ARG, "A is NULL");
-    if (W < 1 || H < 1 || gop < 1 || m < 1) return fail(CS_ERR_ARG, "W, H, gop and m must be >= 1");
-    if (W % 16 != 0) return fail(CS_ERR_UNSUPPORTED, "W must be a multiple of 16 (TMA row pitch)");
-    const long long n = (long long)W * H;
-    if (n > (1LL << 30) || (long long)m * n > (1LL << 34)) return fail(CS_ERR_UNSUPPORTED, "A too large");
-    for (long long i = 0; i < (long long)m * n; ++i) {
-        const float v = half_bits_to_float(A_fp16[i]);
-        if (!std::isfinite(v) || std::fabs(v) > 2048.0f) return fail(CS_ERR_PHI, "A has a non-finite entry or |entry| > 2048");
-    }
-    int dev = 0, major = 0, minor = 0;
-    cudaError_t err = cudaGetDevice(&dev);
-    if (err != cudaSuccess) return cuda_fail(err, "cudaGetDevice");
-    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
-    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
-    if (major != 10 || minor != 0) return fail(CS_ERR_UNSUPPORTED, "device is not sm_100 (B200)");
-    cs_frame_encoder* f = new (std::nothrow) cs_frame_encoder();
-    if (!f) return fail(CS_ERR_OOM, "host allocation failed");
-    f->W = W;
-    f->H = H;
-    f->G = gop;
-    f->m = m;
-    f->n = (int)n;
-    f->device = dev;
-    cudaDeviceGetAttribute(&f->sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaDeviceGetAttribute(&f->smem_limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    err = cudaFuncSetAttribute(csenc::frm::cs_frame_measure_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               f->smem_limit);
-    if (err == cudaSuccess)
-        err = cudaFuncSetAttribute(csenc::frm::cs_frame_measure_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   f->smem_limit);
-    if (err != cudaSuccess) {
-        delete f;
-        return cuda_fail(err, "cudaFuncSetAttribute");
-    }
-    // column k of the device copy holds pixel 4(k/4) + {0,2,1,3}[k%4] (the residual4 pair order)
-    static const int kPerm[4] = {0, 2, 1, 3};
-    std::vector<uint16_t> perm((size_t)m * n);
-    for (long long r = 0; r < m; ++r)
-        for (long long k = 0; k < n; ++k) {
-            const long long j = (k & ~3LL) | kPerm[k & 3];
-            perm[(size_t)(r * n + k)] = j < n ? A_fp16[r * n + j] : 0;
-        }
-    err = cudaMalloc(&f->A_dev, perm.size() * 2);
-    if (err != cudaSuccess) {
-        delete f;
-        return fail(CS_ERR_OOM, std::string("cudaMalloc(A): ") + cudaGetErrorString(err));
-    }
-    err = cudaMemcpy(f->A_dev, perm.data(), perm.size() * 2, cudaMemcpyHostToDevice);
-    if (err != cudaSuccess) {
-        cudaFree(f->A_dev);
-        delete f;
-        return cuda_fail(err, "cudaMemcpy(A)");
-    }
-    *out = f;
-    return CS_OK;
-}
-
-int cs_frame_encoder_set_trace(cs_frame_encoder* f, unsigned long long* trace_dev, int cap) {
-    if (!f || cap < 0 || (cap > 0 && !trace_dev)) return fail(CS_ERR_ARG, "bad trace arguments");
-    f->trace = cap > 0 ? trace_dev : nullptr;
-    f->trace_cap = cap;
-    return CS_OK;
-}
-
-int cs_frame_encoder_destroy(cs_frame_encoder* f) {
-    if (!f) return CS_OK;
-    if (f->A_dev) cudaFree(f->A_dev);
-    delete f;
-    return CS_OK;
-}
-
-int64_t cs_frame_measurement_count(const cs_frame_encoder* f, int n_seq, int T) {
-    if (!f || n_seq < 0 || T < 0) return -1;
-    return (int64_t)n_seq * cs_frames_per_stream(T, f->G) * f->m;
-}
-
-int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq, int T, float* y, cs_stream_t stream) {
-    if (!f) return fail(CS_ERR_ARG, "encoder is NULL");
-    if (n_seq < 0 || T < 0) return fail(CS_ERR_ARG, "n_seq and T must be >= 0");
-    const long long cs_s = cs_frames_per_stream(T, f->G);
-    if (n_seq == 0 || cs_s == 0) return CS_OK;
-    if (!frames || !y) return fail(CS_ERR_ARG, "NULL buffer");
-    if (!aligned16(frames) || !aligned16(y)) return fail(CS_ERR_ARG, "buffers must be 16-byte aligned");
-    if ((long long)n_seq * T > 0x7FFFFFFFLL) return fail(CS_ERR_UNSUPPORTED, "too many frames");
-    const cudaStream_t st = (cudaStream_t)stream;
-    csenc::frm::FParams fp;
-    std::memset(&fp, 0, sizeof(fp));
-    PFN_encodeTiled enc = get_encode_tiled();
-    if (!enc) return fail(CS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    const int G = f->G;
-    const int n_gops = cdiv(T, G);
-    const int gw_max = std::max(1, 256 / G);          // box rows <= 256, CS rows <= 256
-    fp.n_mp = cdiv(f->m, 256);
-    if (T % G == 0) {
-        // whole GOPs everywhere: windows over the concatenation, sized so the units fill the SMs in
-        // whole waves (k units per SM, the smallest k whose windows fit a box)
-        fp.global_win = 1;
-        fp.total_gops = n_seq * n_gops;
-        fp.gw = std::min(gw_max, fp.total_gops);
-        for (int k = 1; k <= 16; ++k) {
-            const long long want = ((long long)k * f->sms + fp.n_mp - 1) / fp.n_mp;
-            const long long gw = (fp.total_gops + want - 1) / want;
-            if (gw <= gw_max) {
-                fp.gw = (int)std::max(1LL, gw);
-                break;
-            }
-        }
-        fp.n_win_s = 0;
-        fp.n_win = cdiv(fp.total_gops, fp.gw);
-    } else {
-        // windows inside each stream, balanced
-        fp.global_win = 0;
-        fp.total_gops = n_seq * n_gops;
-        fp.n_win_s = cdiv(n_gops, gw_max);
-        fp.gw = cdiv(n_gops, fp.n_win_s);
-        fp.n_win_s = cdiv(n_gops, fp.gw);
-        fp.n_win = n_seq * fp.n_win_s;
-    }
-    fp.nf_box = fp.gw * G;
-    // pairs of CTAs (a cluster) can share each A tile by TMA multicast
-    // (measured slower on B200 than independent CTAs: 876 vs 966 TFLOP/s -- the pair is coupled
-    // through the shared stage; opt-in with CSENC_FRAME_CLUSTER=1)
-    const int CL = (fp.n_win >= 2 && env_int("CSENC_FRAME_CLUSTER", 0) == 1) ? 2 : 1;
-    {
-        cuuint64_t dims[2] = {(cuuint64_t)f->n, (cuuint64_t)n_seq * T};
-        cuuint64_t strides[1] = {(cuuint64_t)f->n};
-        cuuint32_t box[2] = {(cuuint32_t)csenc::frm::kKc, (cuuint32_t)fp.nf_box};
-        cuuint32_t estr[2] = {1, 1};
-        CUresult r = enc(&fp.fmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(frames), dims, strides, box,
-                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return fail(CS_ERR_CUDA, "cuTensorMapEncodeTiled(frames) failed (code " + std::to_string((int)r) + ")");
-    }
-    {
-        cuuint64_t dims[2] = {(cuuint64_t)f->n, (cuuint64_t)f->m};
-        cuuint64_t strides[1] = {(cuuint64_t)f->n * 2u};
-        cuuint32_t box[2] = {(cuuint32_t)csenc::frm::kKc, (cuuint32_t)(256 / CL)};
-        cuuint32_t estr[2] = {1, 1};
-        CUresult r = enc(&fp.amap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, f->A_dev, dims, strides, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return fail(CS_ERR_CUDA, "cuTensorMapEncodeTiled(A) failed (code " + std::to_string((int)r) + ")");
-    }
-    fp.n = f->n;
-    fp.m = f->m;
-    fp.G = G;
-    fp.T = T;
-    fp.cs_s = (int)cs_s;
-
-    fp.n_chunks = cdiv(f->n, csenc::frm::kKc);
-    const long long n_cl = f->sms / CL;                                 // clusters resident at once
-    const long long tiles = (long long)((fp.n_win + CL - 1) / CL) * fp.n_mp;   // cluster work units
-    long long ks = (n_cl + tiles - 1) / tiles;                        // K splits to fill the SMs
-    ks = std::max(1LL, std::min(ks, (long long)std::max(1, fp.n_chunks / 8)));
-    // no empty K split (every unit must issue at least one chunk): ks = ceil(chunks / per-split)
-    const long long per_split = (fp.n_chunks + ks - 1) / ks;
-    ks = (fp.n_chunks + per_split - 1) / per_split;
-    fp.n_ks = (int)ks;
-    if (tiles * ks > 0x7FFFFFFFLL) return fail(CS_ERR_UNSUPPORTED, "too many work units");
-    fp.n_units = (int)(tiles * ks);
-    fp.fbox_bytes = (uint32_t)fp.nf_box * (uint32_t)csenc::frm::kKc;
-    fp.off_a = align_up(fp.fbox_bytes, 1024);
-    fp.stage_bytes = fp.off_a + 256u * csenc::frm::kKc * 2u;
-    fp.b_bytes = align_up((uint32_t)(fp.gw * (G - 1) + 15) / 16 * 16 * 128u, 1024);
-    fp.n_b = std::max(2, std::min(4, env_int("CSENC_FRAME_BBUFS", 2)));
-    fp.off_stage = csenc::frm::kOffB + (uint32_t)fp.n_b * fp.b_bytes;
-    const long avail = (long)f->smem_limit - 1024 - (long)fp.off_stage;
-    fp.n_stages = (int)std::min<long>(csenc::frm::kMaxStages, avail / (long)fp.stage_bytes);
-    if (fp.n_stages < 2) return fail(CS_ERR_UNSUPPORTED, "frame measurement: stages do not fit shared memory");
-    const uint32_t smem = 1024 + fp.off_stage + (uint32_t)fp.n_stages * fp.stage_bytes;
-    fp.prefetch = env_int("CSENC_FRAME_PREFETCH", 0);
-    fp.trace = f->trace;
-    fp.trace_cap = f->trace_cap;
-    fp.out_floats = (long long)n_seq * cs_s * f->m;
-    fp.smem_bytes = smem - 1024;
-    const long long ny = (long long)n_seq * cs_s * f->m;
-    float* part = nullptr;
-    cudaError_t err;
-    if (fp.n_ks > 1) {
-        fp.part_stride = (ny + 3) / 4 * 4;
-        err = cudaMallocAsync((void**)&part, (size_t)fp.part_stride * fp.n_ks * sizeof(float), st);
-        if (err != cudaSuccess) return fail(CS_ERR_OOM, std::string("partials: ") + cudaGetErrorString(err));
-        fp.out = part;
-    } else {
-        fp.part_stride = 0;
-        fp.out = y;
-    }
-    const int n_clusters = (int)std::max(1LL, std::min(n_cl, (long long)fp.n_units));
-    cudaLaunchConfig_t cfg;
-    std::memset(&cfg, 0, sizeof(cfg));
-    cfg.gridDim = dim3((unsigned)(n_clusters * CL));
-    cfg.blockDim = dim3(csenc::frm::kThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)CL;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    err = CL == 2 ? cudaLaunchKernelEx(&cfg, csenc::frm::cs_frame_measure_kernel<2>, fp)
-                  : cudaLaunchKernelEx(&cfg, csenc::frm::cs_frame_measure_kernel<1>, fp);
-    if (err == cudaSuccess) err = cudaGetLastError();
-    if (err == cudaSuccess && fp.n_ks > 1) {
-        csenc::frm::cs_frame_reduce_kernel<<<f->sms * 4, 256, 0, st>>>(part, y, ny, fp.part_stride, fp.n_ks);
-        err = cudaGetLastError();
-    }
-    if (part) cudaFreeAsync(part, st);
-    return err == cudaSuccess ? CS_OK : cuda_fail(err, "frame measurement launch");
-}
-
-int cs_adjoint(cs_encoder* e, const float* meas, int64_t n_frames, float* x, cs_stream_t stream) {
-    if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
-    if (n_frames < 0) return fail(CS_ERR_ARG, "n_frames must be >= 0");
-    if (n_frames == 0) return CS_OK;
-    if (!meas || !x) return fail(CS_ERR_ARG, "NULL buffer");
-    if (!aligned16(meas) || !aligned16(x)) return fail(CS_ERR_ARG, "buffers must be 16-byte aligned");
-    if (!e->phiT_dev) return fail(CS_ERR_UNSUPPORTED, "adjoint needs M % 4 == 0 (16-byte measurement rows)");
-    const Geometry& g = e->geo;
-    if (n_frames * (long long)g.nblk >= 0x7FFFFFFFLL || n_frames * (long long)g.nby * cdiv(g.nbx, 128) >= 0x7FFFFFFFLL)
-        return fail(CS_ERR_UNSUPPORTED, "too many frames for one call");
-    return launch_adjoint(e, meas, n_frames, x, (cudaStream_t)stream);
 }
 
 int64_t cs_q16_scale_count(const cs_encoder* e, int n_seq, int T, int granularity) {

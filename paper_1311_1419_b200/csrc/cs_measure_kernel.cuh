@@ -1154,7 +1154,6 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         // XOR-swizzled SMEM tile so that every st.global.v4 instruction writes whole 64/128-byte
         // row segments (bank-conflict-free on both sides).  Other M: scalar stores.
         const int ew = warp - kEpiWarp0;
-        const int lane_idx = ew * 32 + (int)lane;
         const uint32_t lane_bits = (uint32_t)(ew * 32) << 16;
         const uint32_t stage_tile = sbase + p.off_epi + (uint32_t)ew * 4096u;
         const int mode = (p.M == 4) ? 0 : ((p.M & 3) == 0 ? 1 : 2);
