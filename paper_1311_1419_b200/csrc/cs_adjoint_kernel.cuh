@@ -236,25 +236,18 @@ __global__ void __launch_bounds__(kThreads, 1) cs_adjoint_kernel(const __grid_co
                 ptx::mbar_wait(bar_dfull + 8 * db, dph);
                 ptx::tc_fence_after();
                 const uint32_t d_tm = tmem_base + lane_bits + (uint32_t)db * 256u;
-                for (int pr = 0; pr < rows_per_chunk; ++pr) {
-                    const int Y = by * B + nc * rows_per_chunk + pr;
-                    float* dst = p.x + ((long long)f * p.H + Y) * p.W + col0;
-                    CS_CHECK(Y >= p.H || valid <= 0 || ((long long)f * p.H + Y) * p.W + col0 + valid <= p.x_floats);
-                    if constexpr (B == 8) {
-                        uint32_t v[8];
-                        ptx::tmem_ld_32x32b_x8(d_tm + (uint32_t)(pr * B), v);
-                        ptx::tc_wait_ld();
-                        if (Y < p.H && valid > 0) row_store<2>(v, tile, lane, dst, valid);
-                    } else if constexpr (B == 16) {
-                        uint32_t v[16];
-                        ptx::tmem_ld_32x32b_x16(d_tm + (uint32_t)(pr * B), v);
-                        ptx::tc_wait_ld();
-                        if (Y < p.H && valid > 0) row_store<4>(v, tile, lane, dst, valid);
-                    } else {
-                        uint32_t v[32];
-                        ptx::tmem_ld_32x32b_x32(d_tm + (uint32_t)(pr * B), v);
-                        ptx::tc_wait_ld();
-                        if (Y < p.H && valid > 0) row_store<8>(v, tile, lane, dst, valid);
+                // one 32-column TMEM load covers 32 / B pixel rows (B = 8: 4 rows, B = 16: 2, B = 32: 1)
+                constexpr int kRowsPerLd = 32 / B;
+                for (int pr0 = 0; pr0 < rows_per_chunk; pr0 += kRowsPerLd) {
+                    uint32_t v[32];
+                    ptx::tmem_ld_32x32b_x32(d_tm + (uint32_t)(pr0 * B), v);
+                    ptx::tc_wait_ld();
+#pragma unroll
+                    for (int k = 0; k < kRowsPerLd; ++k) {
+                        const int Y = by * B + nc * rows_per_chunk + pr0 + k;
+                        float* dst = p.x + ((long long)f * p.H + Y) * p.W + col0;
+                        CS_CHECK(Y >= p.H || valid <= 0 || ((long long)f * p.H + Y) * p.W + col0 + valid <= p.x_floats);
+                        if (Y < p.H && valid > 0) row_store<B / 4>(v + k * B, tile, lane, dst, valid);
                     }
                 }
                 ptx::tc_fence_before();
