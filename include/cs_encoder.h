@@ -281,6 +281,14 @@ int cs_encoder_set_gop_phis(cs_encoder* enc, int n_phi, const uint16_t* phis);
  * kept until destroy). */
 int cs_encode_batch_host(cs_encoder* enc, const uint8_t* frames_host, int n_seq, int T, float* meas_host);
 
+/* The same for several encoders over the SAME frames (e.g. several measurement matrices / rates,
+ * the M sweep): encs[0..n_enc-1] must share W, H, gop and device (B and M may differ; no encoder
+ * twice); meas_host[k] receives encoder k's output.  Each frame group crosses PCIe once, all
+ * encoders run on it, and every output is copied back as soon as its encode finishes.  Uses the
+ * first encoder's frame workspace and streams; locks every encoder's workspace. */
+int cs_encode_batch_host_multi(cs_encoder* const* encs, int n_enc, const uint8_t* frames_host, int n_seq, int T,
+                               float* const* meas_host);
+
 /* ---- accounting (host only) ------------------------------------------------------------- */
 
 /* Number of fp32 measurements cs_encode_batch writes for n_seq streams of T frames

@@ -64,6 +64,7 @@ def lib() -> ctypes.CDLL:
             "cs_encode_batch": (c_int, [vp, vp, c_int, c_int, vp, vp]),
             "cs_encode_batch_gops": (c_int, [vp, vp, c_int, c_int, c_int, c_int, vp, vp]),
             "cs_encode_batch_host": (c_int, [vp, vp, c_int, c_int, vp]),
+            "cs_encode_batch_host_multi": (c_int, [vp, c_int, vp, c_int, c_int, vp]),
             "cs_encode_batch_q16": (c_int, [vp, vp, c_int, c_int, c_int, vp, vp, vp]),
             "cs_q16_scale_count": (c_i64, [vp, c_int, c_int, c_int]),
             "cs_adjoint": (c_int, [vp, vp, c_i64, vp, vp]),
@@ -372,6 +373,20 @@ class Encoder:
         op = out.ctypes.data if isinstance(out, np.ndarray) else _ptr(out)
         _check(lib().cs_encode_batch_host(self._h, fp, n_seq, T, op))
         return out
+
+
+def encode_batch_host_multi(encoders, frames, outs=None):
+    """Several encoders (same W, H, gop) over the same HOST frames [n_seq][T][H][W]: each frame group
+    crosses PCIe once.  frames: numpy or (pinned) CPU tensor; returns the list of host outputs."""
+    n_seq, T = frames.shape[:2]
+    if outs is None:
+        outs = [np.empty(e.out_shape(n_seq, T), dtype=np.float32) for e in encoders]
+    hs = (ctypes.c_void_p * len(encoders))(*[e._h.value for e in encoders])
+    ps = (ctypes.c_void_p * len(outs))(*[o.ctypes.data if isinstance(o, np.ndarray) else _ptr(o) for o in outs])
+    fp = frames.ctypes.data if isinstance(frames, np.ndarray) else _ptr(frames)
+    _check(lib().cs_encode_batch_host_multi(ctypes.cast(hs, ctypes.c_void_p), len(encoders), fp, n_seq, T,
+                                            ctypes.cast(ps, ctypes.c_void_p)))
+    return outs
 
 
 class FrameEncoder:

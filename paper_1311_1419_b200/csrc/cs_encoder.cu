@@ -834,18 +834,33 @@ int cs_encode_batch_q16(cs_encoder* e, const uint8_t* frames, int n_seq, int T, 
     return err == cudaSuccess ? CS_OK : cuda_fail(err, "finalize launch");
 }
 
-int cs_encode_batch_host(cs_encoder* e, const uint8_t* frames_host, int n_seq, int T, float* out_host) {
-    if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
+int cs_encode_batch_host_multi(cs_encoder* const* encs, int n_enc, const uint8_t* frames_host, int n_seq, int T,
+                               float* const* outs_host) {
+    if (!encs || n_enc < 1) return fail(CS_ERR_ARG, "encoders: need at least one");
+    for (int k = 0; k < n_enc; ++k) {
+        if (!encs[k]) return fail(CS_ERR_ARG, "encoder is NULL");
+        for (int j = 0; j < k; ++j)
+            if (encs[j] == encs[k]) return fail(CS_ERR_ARG, "the same encoder twice");
+        const Geometry& a = encs[0]->geo;
+        const Geometry& c = encs[k]->geo;
+        if (c.W != a.W || c.H != a.H || c.G != a.G || encs[k]->device != encs[0]->device)
+            return fail(CS_ERR_ARG, "encoders must share W, H, gop and device");
+    }
     if (n_seq < 0 || T < 0) return fail(CS_ERR_ARG, "n_seq and T must be >= 0");
+    cs_encoder* const e = encs[0];   // frames workspace, streams and events
     const Geometry& g = e->geo;
     const long long cs_s = cs_frames_per_stream(T, g.G);
     if (n_seq == 0 || T == 0 || cs_s == 0) return CS_OK;
-    if (!frames_host || !out_host) return fail(CS_ERR_ARG, "NULL buffer");
+    if (!frames_host || !outs_host) return fail(CS_ERR_ARG, "NULL buffer");
+    for (int k = 0; k < n_enc; ++k)
+        if (!outs_host[k]) return fail(CS_ERR_ARG, "NULL output buffer");
     const size_t frame_bytes = (size_t)g.W * g.H;
     const size_t in_bytes = (size_t)n_seq * T * frame_bytes;
-    const size_t cs_meas = (size_t)g.nblk * g.M;  // floats per CS frame
-    const size_t out_bytes = (size_t)n_seq * cs_s * cs_meas * sizeof(float);
-    std::lock_guard<std::mutex> lk(e->ws_mu);  // the workspace is per encoder
+    // workspaces are per encoder: lock them in address order (no deadlock between concurrent callers)
+    std::vector<cs_encoder*> order(encs, encs + n_enc);
+    std::sort(order.begin(), order.end());
+    std::vector<std::unique_lock<std::mutex>> locks;
+    for (cs_encoder* x : order) locks.emplace_back(x->ws_mu);
     cudaError_t err;
     if (e->ws_frames_bytes < in_bytes) {
         if (e->ws_frames) cudaFree(e->ws_frames);
@@ -855,19 +870,24 @@ int cs_encode_batch_host(cs_encoder* e, const uint8_t* frames_host, int n_seq, i
             return fail(CS_ERR_OOM, std::string("workspace: ") + cudaGetErrorString(err));
         e->ws_frames_bytes = in_bytes;
     }
-    if (e->ws_out_bytes < out_bytes) {
-        if (e->ws_out) cudaFree(e->ws_out);
-        e->ws_out = nullptr;
-        e->ws_out_bytes = 0;
-        if ((err = cudaMalloc(&e->ws_out, out_bytes)) != cudaSuccess)
-            return fail(CS_ERR_OOM, std::string("workspace: ") + cudaGetErrorString(err));
-        e->ws_out_bytes = out_bytes;
+    for (int k = 0; k < n_enc; ++k) {
+        cs_encoder* x = encs[k];
+        const size_t out_bytes = (size_t)n_seq * cs_s * x->geo.nblk * x->geo.M * sizeof(float);
+        if (x->ws_out_bytes < out_bytes) {
+            if (x->ws_out) cudaFree(x->ws_out);
+            x->ws_out = nullptr;
+            x->ws_out_bytes = 0;
+            if ((err = cudaMalloc(&x->ws_out, out_bytes)) != cudaSuccess)
+                return fail(CS_ERR_OOM, std::string("workspace: ") + cudaGetErrorString(err));
+            x->ws_out_bytes = out_bytes;
+        }
     }
-    for (auto& s : e->hs)
-        if (!s && (err = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess)
+    for (auto& st : e->hs)
+        if (!st && (err = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess)
             return cuda_fail(err, "cudaStreamCreate");
-    // Groups: chunks of streams (n_seq > 1) or of GOPs (n_seq == 1).  Copy-in of group i+1
-    // overlaps the encode of group i and the copy-out of group i-1.
+    // Groups: chunks of streams (n_seq > 1) or of GOPs (n_seq == 1).  Copy-in of group i+1 overlaps
+    // the encodes of group i and the copy-outs of group i-1; each frame group crosses PCIe once
+    // whatever the number of encoders.
     struct Grp {
         int s0, s1, g0, g1;
     };
@@ -880,7 +900,8 @@ int cs_encode_batch_host(cs_encoder* e, const uint8_t* frames_host, int n_seq, i
         const int per = std::max(1, n_gops / 8);
         for (int gg = 0; gg < n_gops; gg += per) groups.push_back({0, 1, gg, std::min(n_gops, gg + per)});
     }
-    while (e->hev.size() < 2 * groups.size()) {
+    const size_t n_ev = groups.size() * (size_t)(1 + n_enc);
+    while (e->hev.size() < n_ev) {
         cudaEvent_t ev;
         if ((err = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
             return cuda_fail(err, "cudaEventCreate");
@@ -904,27 +925,29 @@ int cs_encode_batch_host(cs_encoder* e, const uint8_t* frames_host, int n_seq, i
             rc = cuda_fail(err, "H2D");
             break;
         }
-        cudaEventRecord(e->hev[2 * i], s_in);
-        cudaStreamWaitEvent(s_run, e->hev[2 * i], 0);
-        size_t o0, o1;  // output float range
-        if (n_seq > 1) {
-            o0 = (size_t)gr.s0 * cs_s * cs_meas;
-            o1 = (size_t)gr.s1 * cs_s * cs_meas;
-            rc = cs_encode_batch(e, e->ws_frames + f0 * frame_bytes, gr.s1 - gr.s0, T, e->ws_out + o0, s_run);
-        } else {
-            o0 = (size_t)cs_frames_in_gops(T, g.G, 0, gr.g0) * cs_meas;
-            o1 = (size_t)cs_frames_in_gops(T, g.G, 0, gr.g1) * cs_meas;
-            rc = cs_encode_batch_gops(e, e->ws_frames, 1, T, gr.g0, gr.g1, e->ws_out + o0, s_run);
-        }
-        if (rc != CS_OK) break;
-        cudaEventRecord(e->hev[2 * i + 1], s_run);
-        cudaStreamWaitEvent(s_out, e->hev[2 * i + 1], 0);
-        if (o1 > o0) {
-            err = cudaMemcpyAsync(out_host + o0, e->ws_out + o0, (o1 - o0) * sizeof(float), cudaMemcpyDeviceToHost,
-                                  s_out);
-            if (err != cudaSuccess) {
-                rc = cuda_fail(err, "D2H");
-                break;
+        cudaEvent_t* ev = &e->hev[i * (size_t)(1 + n_enc)];
+        cudaEventRecord(ev[0], s_in);
+        cudaStreamWaitEvent(s_run, ev[0], 0);
+        for (int k = 0; k < n_enc && rc == CS_OK; ++k) {
+            cs_encoder* x = encs[k];
+            const size_t cs_meas = (size_t)x->geo.nblk * x->geo.M;   // floats per CS frame
+            size_t o0, o1;  // output float range
+            if (n_seq > 1) {
+                o0 = (size_t)gr.s0 * cs_s * cs_meas;
+                o1 = (size_t)gr.s1 * cs_s * cs_meas;
+                rc = cs_encode_batch(x, e->ws_frames + f0 * frame_bytes, gr.s1 - gr.s0, T, x->ws_out + o0, s_run);
+            } else {
+                o0 = (size_t)cs_frames_in_gops(T, g.G, 0, gr.g0) * cs_meas;
+                o1 = (size_t)cs_frames_in_gops(T, g.G, 0, gr.g1) * cs_meas;
+                rc = cs_encode_batch_gops(x, e->ws_frames, 1, T, gr.g0, gr.g1, x->ws_out + o0, s_run);
+            }
+            if (rc != CS_OK) break;
+            cudaEventRecord(ev[1 + k], s_run);
+            cudaStreamWaitEvent(s_out, ev[1 + k], 0);
+            if (o1 > o0) {
+                err = cudaMemcpyAsync(outs_host[k] + o0, x->ws_out + o0, (o1 - o0) * sizeof(float),
+                                      cudaMemcpyDeviceToHost, s_out);
+                if (err != cudaSuccess) rc = cuda_fail(err, "D2H");
             }
         }
     }
@@ -934,6 +957,10 @@ int cs_encode_batch_host(cs_encoder* e, const uint8_t* frames_host, int n_seq, i
     if (e2 != cudaSuccess) return cuda_fail(e2, "encode");
     if (e3 != cudaSuccess) return cuda_fail(e3, "sync");
     return CS_OK;
+}
+
+int cs_encode_batch_host(cs_encoder* e, const uint8_t* frames_host, int n_seq, int T, float* out_host) {
+    return cs_encode_batch_host_multi(&e, 1, frames_host, n_seq, T, &out_host);
 }
 
 }  // extern "C"

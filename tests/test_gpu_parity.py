@@ -308,3 +308,23 @@ def test_all_candidate_plans_bitwise_identical():
         out = enc.encode_batch(fd)
         torch.cuda.synchronize()
         assert torch.equal(out, ref) and chosen["smem_bytes"] > 0
+
+
+def test_host_multi_encoder_path():
+    """cs_encode_batch_host_multi: several encoders (different M and B) over the same host frames
+    give exactly the device-path outputs; mismatched geometry is rejected."""
+    cfg = synth.CONFIGS["C2"].with_(T=19, S=3)
+    frames = synth.gen_video(cfg)
+    encs = [P.Encoder(cfg.W, cfg.H, cfg.G, B, M, synth.phi_from_seed(7 + M, M, B * B))
+            for B, M in ((16, 16), (16, 64), (8, 12), (32, 40))]
+    outs = P.encode_batch_host_multi(encs, frames)
+    fd = torch.from_numpy(frames).cuda()
+    for e, o in zip(encs, outs):
+        ref = e.encode_batch(fd)
+        torch.cuda.synchronize()
+        assert np.array_equal(o, ref.cpu().numpy())
+    other = P.Encoder(cfg.W, cfg.H, cfg.G + 1, 16, 16, synth.phi_from_seed(1, 16, 256))
+    with pytest.raises(P.CSError):
+        P.encode_batch_host_multi([encs[0], other], frames)
+    with pytest.raises(P.CSError):
+        P.encode_batch_host_multi([encs[0], encs[0]], frames)
