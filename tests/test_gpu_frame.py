@@ -117,3 +117,19 @@ def test_frame_args():
     fe = P.FrameEncoder(32, 16, 1, 4, A)                                      # G = 1: no CS frames
     y = fe.encode_batch(torch.zeros((2, 3, 16, 32), dtype=torch.uint8, device="cuda"))
     assert y.numel() == 0
+
+
+@pytest.mark.parametrize("two_sm", ["0", "1"])
+def test_frame_paths_single_cta_and_pair(two_sm, monkeypatch):
+    """Both frame-GEMM kernels -- K4 (one CTA per tile) and K4b (CTA pairs, 2-SM MMA, opt-in) -- give
+    the oracle's measurements (windows within and across streams, split-K)."""
+    monkeypatch.setenv("CSENC_FRAME_2SM", two_sm)
+    for (W, H, G, T, S, m) in [(176, 144, 5, 40, 4, 507), (64, 16, 3, 8, 3, 100), (48, 32, 4, 11, 2, 300)]:
+        cfg = synth.CONFIGS["C1"].with_(W=W, H=H, G=G, T=T, S=S)
+        frames = synth.gen_video(cfg)
+        A = synth.phi_from_seed(11 + m, m, W * H)
+        y_gpu = P.FrameEncoder(W, H, G, m, A).encode_batch(torch.from_numpy(frames).cuda()).cpu().numpy()
+        n_cs = oracle.cs_frame_count(T, G)
+        for s in range(S):
+            y, Sc = oracle.measure_frame(frames[s], A, G)
+            check(y_gpu[s * n_cs:(s + 1) * n_cs], y, Sc, W * H)
