@@ -119,7 +119,7 @@ int cs_encoder_plan(const cs_encoder* enc, cs_plan_info* info);
  * buffer free, 4 converter A written, 5 MMA A ready, 6 MMA issued+committed, 7 epilogue
  * accumulator ready, 8 epilogue done, 9 converter tcgen05.st issued.  cap = 0 disables (default).  Not thread-safe with
  * concurrent encodes of the same encoder. */
-#define CS_TRACE_EVENTS 10
+#define CS_TRACE_EVENTS 12
 int cs_encoder_set_trace(cs_encoder* enc, unsigned long long* trace_dev, int cap);
 
 /* ---- encode (device buffers; asynchronous) ---------------------------------------------- */

@@ -383,12 +383,17 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
             kern<<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(kp);
         }
     };
-    const int epi = q.qmode == csenc::Q_FRAME1 ? csenc::EPI_Q16F : (q.qmode ? csenc::EPI_Q16 : csenc::EPI_F32);
+    int epi = q.qmode == csenc::Q_FRAME1 ? csenc::EPI_Q16F : (q.qmode ? csenc::EPI_Q16 : csenc::EPI_F32);
+    if (q.qmode == csenc::Q_ROW)
+        epi = (pl.F == 1 && g.Mpad <= 32 && g.Mpad == g.M && pl.T_r <= csenc::kRowRegRows) ? csenc::EPI_Q16RR
+                                                                                            : csenc::EPI_Q16R;
 #define CSENC_CASE(B_, K_)                                                                                \
-    case (B_ * 4 + K_) * 4 + csenc::EPI_F32: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_F32>); break;   \
-    case (B_ * 4 + K_) * 4 + csenc::EPI_Q16: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16>); break;   \
-    case (B_ * 4 + K_) * 4 + csenc::EPI_Q16F: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16F>); break;
-    switch ((g.B * 4 + km) * 4 + epi) {
+    case (B_ * 4 + K_) * 8 + csenc::EPI_F32: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_F32>); break;   \
+    case (B_ * 4 + K_) * 8 + csenc::EPI_Q16: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16>); break;   \
+    case (B_ * 4 + K_) * 8 + csenc::EPI_Q16F: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16F>); break; \
+    case (B_ * 4 + K_) * 8 + csenc::EPI_Q16R: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16R>); break; \
+    case (B_ * 4 + K_) * 8 + csenc::EPI_Q16RR: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16RR>); break;
+    switch ((g.B * 4 + km) * 8 + epi) {
         CSENC_CASE(8, csenc::KEY_STREAMED) CSENC_CASE(8, csenc::KEY_RESIDENT) CSENC_CASE(8, csenc::KEY_REGS)
         CSENC_CASE(16, csenc::KEY_STREAMED) CSENC_CASE(16, csenc::KEY_RESIDENT) CSENC_CASE(16, csenc::KEY_REGS)
         CSENC_CASE(32, csenc::KEY_STREAMED) CSENC_CASE(32, csenc::KEY_RESIDENT)
@@ -411,6 +416,12 @@ cudaError_t set_smem_attr_all(int bytes) {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);                         \
     if (r != cudaSuccess) e = r;                                                                          \
     r = cudaFuncSetAttribute(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16F>,                          \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);                         \
+    if (r != cudaSuccess) e = r;                                                                          \
+    r = cudaFuncSetAttribute(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16R>,                          \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);                         \
+    if (r != cudaSuccess) e = r;                                                                          \
+    r = cudaFuncSetAttribute(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16RR>,                         \
                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);                         \
     if (r != cudaSuccess) e = r;
     CSENC_ATTR(8, csenc::KEY_STREAMED) CSENC_ATTR(8, csenc::KEY_RESIDENT) CSENC_ATTR(8, csenc::KEY_REGS)

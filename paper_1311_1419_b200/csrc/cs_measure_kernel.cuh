@@ -56,7 +56,16 @@ constexpr uint32_t kTmemCols = 512;
 
 enum KeyMode : int { KEY_STREAMED = 0, KEY_RESIDENT = 1, KEY_REGS = 2 };
 // epilogue variants (template EPI): fp32 measurements (a6), or 16-bit codes (f1)
-enum Epilogue : int { EPI_F32 = 0, EPI_Q16 = 1, EPI_Q16F = 2 };   // EPI_Q16F: Q_FRAME1 look-back only
+// One instantiation per variant keeps each kernel's code small: the four roles' loops share the SM's
+// instruction cache (measured: a 64-value register path in the shared q16 kernel cost the other
+// modes 7-10%; split out, the row mode gained 38% at M = 16/32).
+enum Epilogue : int {
+    EPI_F32 = 0,    // fp32 measurements
+    EPI_Q16 = 1,    // Q_ABSMAX / Q_FRAME (the two passes of the per-frame scale)
+    EPI_Q16F = 2,   // Q_FRAME1 look-back only
+    EPI_Q16R = 3,   // Q_ROW, general (two TMEM passes, named barrier)
+    EPI_Q16RR = 4,  // Q_ROW, register path: one fold, M = 16 or 32, <= kRowRegRows block rows
+};
 // EPI_Q16 sub-modes (KParams::qmode)
 enum QMode : int {
     Q_ABSMAX = 1,     // pass 1 of the per-frame scale: atomicMax of |y| bits into amax[cs], no stores
@@ -73,6 +82,16 @@ constexpr int kRowSlots = 40;                    // Q_ROW: max block rows per ti
 constexpr uint32_t kRowSlotOff = 512;            // Q_ROW slots live in the barrier page (bytes 512..991)
 static_assert(16 * kMaxStages + 32 + 32 * kMaxTmemBufs + 24 <= (int)kRowSlotOff, "barrier block overlaps row slots");
 static_assert(kRowSlotOff + 3 * kRowSlots * 4 <= 1024, "row slots overflow the barrier page");
+// Q_ROW register path (one fold, M = 16 or 32, <= 32 block rows): values stay in registers between the
+// row reduction and the codes; each epilogue warp's row maxima go to its own slots in the upper half
+// of its 4 KB staging tile (codes use <= 2 KB of it), kRowBufs items deep, behind row_full mbarriers.
+constexpr int kRowBufs = 4;
+constexpr int kRowRegRows = 32;
+constexpr uint32_t kRowBarOff = 448;             // row_full[kRowBufs] (4 epilogue-warp arrivals each)
+constexpr uint32_t kRowSlotTileOff = 2048;
+static_assert(16 * kMaxStages + 32 + 32 * kMaxTmemBufs + 24 <= (int)kRowBarOff, "barrier block overlaps row barriers");
+static_assert(kRowBarOff + 8 * kRowBufs <= kRowSlotOff, "row barriers overlap the row slots");
+static_assert(kRowSlotTileOff + kRowBufs * kRowRegRows * 4 <= 4096, "row slots overflow the staging tile");
 
 struct KParams {
     const uint8_t* frames;    // device [n_seq][T][H][W]
@@ -143,6 +162,8 @@ enum : int {
     EV_E_DFULL,       // epilogue: accumulator ready
     EV_E_DONE,        // epilogue: stores issued, D released
     EV_C_CONV,        // converter: all tcgen05.st issued (before wait::st)
+    EV_E_ARRIVED,     // epilogue (Q_ROW register path): row maxima published
+    EV_E_ROWS,        // epilogue (Q_ROW register path): all 4 warps' row maxima present
     EV_COUNT
 };
 
@@ -422,6 +443,8 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         }
         ptx::mbar_init(bar_phi, 1);
         ptx::mbar_init(bar_phi_empty, 1);
+        if (EPI == EPI_Q16RR)
+            for (int i = 0; i < kRowBufs; ++i) ptx::mbar_init(sbase + kRowBarOff + 8 * i, 4);   // row_full
         if (EPI == EPI_Q16F)
             for (int i = 0; i < kPubSlots; ++i) {
                 ptx::mbar_init(sbase + kPubBarOff + 8 * i, 4);                   // pub_full: 4 epilogue warps
@@ -453,7 +476,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
             asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(e), "r"(off), "r"(meta));
         }
     }
-    if (EPI == EPI_Q16 && threadIdx.x < 3 * kRowSlots) ptx::sts32(sbase + kRowSlotOff + threadIdx.x * 4u, 0u);
+    if (EPI == EPI_Q16R && threadIdx.x < 3 * kRowSlots) ptx::sts32(sbase + kRowSlotOff + threadIdx.x * 4u, 0u);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -832,7 +855,9 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         const int lane_idx = ew * 32 + (int)lane;
         const uint32_t lane_bits = (uint32_t)(ew * 32) << 16;
         const uint32_t stage_tile = sbase + p.off_epi + (uint32_t)ew * 4096u;
-        const int qmode = p.qmode;
+        // the mode is fixed by the instantiation where it can be (dead modes compile away)
+        const int qmode = (EPI == EPI_Q16R || EPI == EPI_Q16RR) ? (int)Q_ROW
+                        : EPI == EPI_Q16F ? (int)Q_FRAME1 : (p.qmode == Q_ABSMAX ? (int)Q_ABSMAX : (int)Q_FRAME);
         const int smode = (p.M == 4) ? 0 : ((p.M & 7) == 0 ? 1 : 2);   // store mode
         // Q_ROW: block row (within the tile) of this lane's block in fold f, and the warp's lowest /
         // highest row in fold f, 6 bits per fold (rows < kRowSlots <= 63; fixed for the kernel)
@@ -1010,6 +1035,86 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
             }
             for (; npend > 0; --npend, phead = (phead + 1) & kMaxLag)
                 quantise(pdb[phead], pcs[phead], pblk0[phead], pbh[phead], pt[phead]);
+        } else if constexpr (EPI == EPI_Q16RR) {
+            CS_CHECK(p.F == 1 && p.Mpad <= 32 && p.Mpad == p.M && p.T_r <= kRowRegRows);
+            // Q_ROW, register path (M = 16 or 32, one fold): the accumulator is read from TMEM once and
+            // released at once; the row maxima of the 4 warps meet in SMEM behind a row_full mbarrier;
+            // the codes are made from the registers.  Slot reuse: a warp writes buffer j % 4 at item j after waiting for
+            // every warp's item j-1 arrival, which each warp makes after reading item j-2's slots.
+            const uint32_t my_slots = stage_tile + kRowSlotTileOff;
+            const uint32_t slots0 = sbase + p.off_epi + kRowSlotTileOff;   // warp k's slots: + k * 4096
+            const int r_lane = (int)(rowpack & 63u);
+            const int rlo = (int)(lopack & 63u), rhi = (int)(hipack & 63u);
+            const int row0 = ew * p.Lq;
+            const bool valid_l = (int)lane < p.Lq && row0 + (int)lane < p.L;
+            for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+                Unit w;
+                if (!decode_unit(p, u, w)) continue;
+                const int rows_here = min(p.T_r, p.nby - w.t * p.T_r);
+                const int blocks_here = rows_here * p.nbx;
+                const int blk0 = w.t * p.T_r * p.nbx;
+                const bool valid = valid_l && row0 + (int)lane < blocks_here;
+                for (int c = w.c0; c < w.c1; ++c) {
+                    ptx::mbar_wait(bar_d_full + 8 * db, dph);
+                    ptx::tc_fence_after();
+                    if (tr) trace_ev(p, EV_E_DFULL, n_items);
+                    const long long cs_global = (long long)w.s * p.cs_per_stream_sel +
+                                                (long long)(w.g - p.gop_begin) * (p.G - 1) + c;
+                    CS_CHECK((cs_global + 1) * p.nblk * (long long)p.M <= p.out_floats);
+                    const uint32_t d_tm = tmem_base + lane_bits + d_col0 + (uint32_t)db * (uint32_t)p.d_cols;
+                    uint32_t v[32];
+                    if (p.Mpad == 32) ptx::tmem_ld_32x32b_x32(d_tm, v);
+                    else ptx::tmem_ld_32x32b_x16(d_tm, *reinterpret_cast<uint32_t(*)[16]>(v));
+                    ptx::tc_wait_ld();
+                    ptx::tc_fence_before();   // accumulator in registers: hand it back to the MMA now
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(bar_d_empty + 8 * db);
+                    float mff = 0.0f;
+#pragma unroll
+                    for (int q = 0; q < 32; ++q)
+                        if (q < p.Mpad) mff = fmaxf(mff, fabsf(__uint_as_float(v[q])));
+                    const uint32_t mf = valid ? __float_as_uint(mff) : 0u;
+                    // lane rr <- maximum of block row rr over this warp's lanes (0 for rows it lacks)
+                    uint32_t acc = 0;
+                    for (int rr = rlo; rr <= rhi; ++rr) {
+                        const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, r_lane == rr ? mf : 0u);
+                        if ((int)lane == rr) acc = m;
+                    }
+                    const uint32_t buf = (uint32_t)(n_items % kRowBufs);
+                    if ((int)lane < p.T_r) ptx::sts32(my_slots + (buf * kRowRegRows + lane) * 4u, acc);
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(sbase + kRowBarOff + 8 * buf);
+                    if (tr) trace_ev(p, EV_E_ARRIVED, n_items);
+                    ptx::mbar_wait(sbase + kRowBarOff + 8 * buf, (uint32_t)(n_items / kRowBufs) & 1u);
+                    if (tr) trace_ev(p, EV_E_ROWS, n_items);
+                    // both row maxima (the scale this lane writes, the row of its block) in one round of
+                    // SMEM loads: the epilogue's shared-memory traffic queues behind the converters'
+                    const uint32_t a_s = slots0 + (buf * kRowRegRows + (uint32_t)min(lane_idx, p.T_r - 1)) * 4u;
+                    const uint32_t a_r = slots0 + (buf * kRowRegRows + (uint32_t)(valid ? r_lane : 0)) * 4u;
+                    const uint32_t s0 = ptx::lds32(a_s), s1 = ptx::lds32(a_s + 4096u), s2 = ptx::lds32(a_s + 8192u),
+                                   s3 = ptx::lds32(a_s + 12288u);
+                    const uint32_t q0 = ptx::lds32(a_r), q1 = ptx::lds32(a_r + 4096u), q2 = ptx::lds32(a_r + 8192u),
+                                   q3 = ptx::lds32(a_r + 12288u);
+                    const uint32_t m_s = max(max(s0, s1), max(s2, s3)), m_r = max(max(q0, q1), max(q2, q3));
+                    if (lane_idx < rows_here) p.scales[cs_global * p.nby + w.t * p.T_r + lane_idx] = q16_scale(m_s);
+                    const float inv = q16_inv(q16_scale(valid ? m_r : 0u));
+                    int16_t* const codes_cs = p.codes + (cs_global * p.nblk + blk0) * (long long)p.M;
+                    if (valid) {   // codes straight from registers: the lane's row is 2M contiguous bytes
+                        uint32_t* dst = reinterpret_cast<uint32_t*>(codes_cs + (long long)(row0 + (int)lane) * p.M);
+#pragma unroll
+                        for (int q = 0; q < 32; q += 8)
+                            if (q < p.Mpad)
+                                ptx::stg128(dst + q / 2, q16_pack(v[q], v[q + 1], inv), q16_pack(v[q + 2], v[q + 3], inv),
+                                            q16_pack(v[q + 4], v[q + 5], inv), q16_pack(v[q + 6], v[q + 7], inv));
+                    }
+                    if (tr) trace_ev(p, EV_E_DONE, n_items);
+                    ++n_items;
+                    if (++db == p.n_dbuf) {
+                        db = 0;
+                        dph ^= 1u;
+                    }
+                }
+            }
         } else
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             Unit w;

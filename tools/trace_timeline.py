@@ -50,6 +50,10 @@ def main(workload="C4", M=None, cap=256, T=None, q16=None):
         "tma latency (c_full - p_issued)": med(d["c_full"] - d["p_issued"]),
         "epilogue (e_done - e_dfull)": med(d["e_done"] - d["e_dfull"]),
     }
+    if (d["e_arrived"] > 0).any():
+        rep["  epilogue ld+reduce (e_arrived - e_dfull)"] = med(d["e_arrived"] - d["e_dfull"])
+        rep["  epilogue row wait (e_rows - e_arrived)"] = med(d["e_rows"] - d["e_arrived"])
+        rep["  epilogue scale+codes (e_done - e_rows)"] = med(d["e_done"] - d["e_rows"])
     for k, v in rep.items():
         print(f"  {k:45s} {v:9.0f} cycles")
     # utilisation over the traced window (items 2..n-2 to skip the prologue)
