@@ -385,14 +385,15 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     };
     int epi = q.qmode == csenc::Q_FRAME1 ? csenc::EPI_Q16F : (q.qmode ? csenc::EPI_Q16 : csenc::EPI_F32);
     if (q.qmode == csenc::Q_ROW)
-        epi = (pl.F == 1 && g.Mpad <= 32 && g.Mpad == g.M && pl.T_r <= csenc::kRowRegRows) ? csenc::EPI_Q16RR
-                                                                                            : csenc::EPI_Q16R;
+        epi = (pl.F != 1 || g.Mpad != g.M || pl.T_r > csenc::kRowRegRows || g.Mpad > 64) ? csenc::EPI_Q16R
+              : g.Mpad <= 32 ? csenc::EPI_Q16RR : csenc::EPI_Q16RR64;
 #define CSENC_CASE(B_, K_)                                                                                \
     case (B_ * 4 + K_) * 8 + csenc::EPI_F32: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_F32>); break;   \
     case (B_ * 4 + K_) * 8 + csenc::EPI_Q16: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16>); break;   \
     case (B_ * 4 + K_) * 8 + csenc::EPI_Q16F: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16F>); break; \
     case (B_ * 4 + K_) * 8 + csenc::EPI_Q16R: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16R>); break; \
-    case (B_ * 4 + K_) * 8 + csenc::EPI_Q16RR: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16RR>); break;
+    case (B_ * 4 + K_) * 8 + csenc::EPI_Q16RR: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16RR>); break; \
+    case (B_ * 4 + K_) * 8 + csenc::EPI_Q16RR64: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16RR64>); break;
     switch ((g.B * 4 + km) * 8 + epi) {
         CSENC_CASE(8, csenc::KEY_STREAMED) CSENC_CASE(8, csenc::KEY_RESIDENT) CSENC_CASE(8, csenc::KEY_REGS)
         CSENC_CASE(16, csenc::KEY_STREAMED) CSENC_CASE(16, csenc::KEY_RESIDENT) CSENC_CASE(16, csenc::KEY_REGS)
@@ -422,6 +423,9 @@ cudaError_t set_smem_attr_all(int bytes) {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);                         \
     if (r != cudaSuccess) e = r;                                                                          \
     r = cudaFuncSetAttribute(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16RR>,                         \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);                         \
+    if (r != cudaSuccess) e = r;                                                                          \
+    r = cudaFuncSetAttribute(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16RR64>,                       \
                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);                         \
     if (r != cudaSuccess) e = r;
     CSENC_ATTR(8, csenc::KEY_STREAMED) CSENC_ATTR(8, csenc::KEY_RESIDENT) CSENC_ATTR(8, csenc::KEY_REGS)

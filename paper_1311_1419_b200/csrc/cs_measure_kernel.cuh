@@ -65,6 +65,7 @@ enum Epilogue : int {
     EPI_Q16F = 2,   // Q_FRAME1 look-back only
     EPI_Q16R = 3,   // Q_ROW, general (two TMEM passes, named barrier)
     EPI_Q16RR = 4,  // Q_ROW, register path: one fold, M = 16 or 32, <= kRowRegRows block rows
+    EPI_Q16RR64 = 5,  // the same for M = 48 or 64
 };
 // EPI_Q16 sub-modes (KParams::qmode)
 enum QMode : int {
@@ -443,7 +444,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         }
         ptx::mbar_init(bar_phi, 1);
         ptx::mbar_init(bar_phi_empty, 1);
-        if (EPI == EPI_Q16RR)
+        if (EPI == EPI_Q16RR || EPI == EPI_Q16RR64)
             for (int i = 0; i < kRowBufs; ++i) ptx::mbar_init(sbase + kRowBarOff + 8 * i, 4);   // row_full
         if (EPI == EPI_Q16F)
             for (int i = 0; i < kPubSlots; ++i) {
@@ -856,7 +857,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         const uint32_t lane_bits = (uint32_t)(ew * 32) << 16;
         const uint32_t stage_tile = sbase + p.off_epi + (uint32_t)ew * 4096u;
         // the mode is fixed by the instantiation where it can be (dead modes compile away)
-        const int qmode = (EPI == EPI_Q16R || EPI == EPI_Q16RR) ? (int)Q_ROW
+        const int qmode = (EPI == EPI_Q16R || EPI == EPI_Q16RR || EPI == EPI_Q16RR64) ? (int)Q_ROW
                         : EPI == EPI_Q16F ? (int)Q_FRAME1 : (p.qmode == Q_ABSMAX ? (int)Q_ABSMAX : (int)Q_FRAME);
         const int smode = (p.M == 4) ? 0 : ((p.M & 7) == 0 ? 1 : 2);   // store mode
         // Q_ROW: block row (within the tile) of this lane's block in fold f, and the warp's lowest /
@@ -1035,9 +1036,10 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
             }
             for (; npend > 0; --npend, phead = (phead + 1) & kMaxLag)
                 quantise(pdb[phead], pcs[phead], pblk0[phead], pbh[phead], pt[phead]);
-        } else if constexpr (EPI == EPI_Q16RR) {
-            CS_CHECK(p.F == 1 && p.Mpad <= 32 && p.Mpad == p.M && p.T_r <= kRowRegRows);
-            // Q_ROW, register path (M = 16 or 32, one fold): the accumulator is read from TMEM once and
+        } else if constexpr (EPI == EPI_Q16RR || EPI == EPI_Q16RR64) {
+            constexpr int NV = EPI == EPI_Q16RR ? 32 : 64;   // accumulator columns held in registers
+            CS_CHECK(p.F == 1 && p.Mpad <= NV && p.Mpad == p.M && p.T_r <= kRowRegRows);
+            // Q_ROW, register path (M = 16..64, one fold): the accumulator is read from TMEM once and
             // released at once; the row maxima of the 4 warps meet in SMEM behind a row_full mbarrier;
             // the codes are made from the registers.  Slot reuse: a warp writes buffer j % 4 at item j after waiting for
             // every warp's item j-1 arrival, which each warp makes after reading item j-2's slots.
@@ -1062,16 +1064,21 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                                                 (long long)(w.g - p.gop_begin) * (p.G - 1) + c;
                     CS_CHECK((cs_global + 1) * p.nblk * (long long)p.M <= p.out_floats);
                     const uint32_t d_tm = tmem_base + lane_bits + d_col0 + (uint32_t)db * (uint32_t)p.d_cols;
-                    uint32_t v[32];
-                    if (p.Mpad == 32) ptx::tmem_ld_32x32b_x32(d_tm, v);
-                    else ptx::tmem_ld_32x32b_x16(d_tm, *reinterpret_cast<uint32_t(*)[16]>(v));
+                    uint32_t v[NV];
+                    if (NV == 32 && p.Mpad == 32) ptx::tmem_ld_32x32b_x32(d_tm, *reinterpret_cast<uint32_t(*)[32]>(v));
+                    if (NV == 32 && p.Mpad == 16) ptx::tmem_ld_32x32b_x16(d_tm, *reinterpret_cast<uint32_t(*)[16]>(v));
+                    if (NV == 64) {
+                        ptx::tmem_ld_32x32b_x32(d_tm, *reinterpret_cast<uint32_t(*)[32]>(v));
+                        if (p.Mpad == 64) ptx::tmem_ld_32x32b_x32(d_tm + 32u, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+                        else ptx::tmem_ld_32x32b_x16(d_tm + 32u, *reinterpret_cast<uint32_t(*)[16]>(v + 32));
+                    }
                     ptx::tc_wait_ld();
                     ptx::tc_fence_before();   // accumulator in registers: hand it back to the MMA now
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(bar_d_empty + 8 * db);
                     float mff = 0.0f;
 #pragma unroll
-                    for (int q = 0; q < 32; ++q)
+                    for (int q = 0; q < NV; ++q)
                         if (q < p.Mpad) mff = fmaxf(mff, fabsf(__uint_as_float(v[q])));
                     const uint32_t mf = valid ? __float_as_uint(mff) : 0u;
                     // lane rr <- maximum of block row rr over this warp's lanes (0 for rows it lacks)
@@ -1099,13 +1106,28 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                     if (lane_idx < rows_here) p.scales[cs_global * p.nby + w.t * p.T_r + lane_idx] = q16_scale(m_s);
                     const float inv = q16_inv(q16_scale(valid ? m_r : 0u));
                     int16_t* const codes_cs = p.codes + (cs_global * p.nblk + blk0) * (long long)p.M;
-                    if (valid) {   // codes straight from registers: the lane's row is 2M contiguous bytes
-                        uint32_t* dst = reinterpret_cast<uint32_t*>(codes_cs + (long long)(row0 + (int)lane) * p.M);
+                    if constexpr (NV == 32) {
+                        if (valid) {   // codes straight from registers: the lane's row is 2M <= 64 contiguous bytes
+                            uint32_t* dst = reinterpret_cast<uint32_t*>(codes_cs + (long long)(row0 + (int)lane) * p.M);
 #pragma unroll
-                        for (int q = 0; q < 32; q += 8)
-                            if (q < p.Mpad)
-                                ptx::stg128(dst + q / 2, q16_pack(v[q], v[q + 1], inv), q16_pack(v[q + 2], v[q + 3], inv),
-                                            q16_pack(v[q + 4], v[q + 5], inv), q16_pack(v[q + 6], v[q + 7], inv));
+                            for (int q = 0; q < NV; q += 8)
+                                if (q < p.Mpad)
+                                    ptx::stg128(dst + q / 2, q16_pack(v[q], v[q + 1], inv), q16_pack(v[q + 2], v[q + 3], inv),
+                                                q16_pack(v[q + 4], v[q + 5], inv), q16_pack(v[q + 6], v[q + 7], inv));
+                        }
+                    } else {   // 96-128 B rows: through the swizzled staging tile, whole 64-B row segments per store
+                        const int rows_valid = min(p.Lq, min(p.L - row0, blocks_here - row0));
+#pragma unroll
+                        for (int j0 = 0; j0 < NV; j0 += 32) {
+                            uint32_t wd[16];
+#pragma unroll
+                            for (int q = 0; q < 16; ++q) wd[q] = q16_pack(v[j0 + 2 * q], v[j0 + 2 * q + 1], inv);
+                            uint32_t* dst_row0 = reinterpret_cast<uint32_t*>(codes_cs + (long long)row0 * p.M + j0);
+                            if (p.Mpad - j0 >= 32)
+                                stage_store_codes<4>(wd, stage_tile, lane, dst_row0, p.M / 2, j0 / 2, p.M / 2, rows_valid);
+                            else
+                                stage_store_codes<2>(wd, stage_tile, lane, dst_row0, p.M / 2, j0 / 2, p.M / 2, rows_valid);
+                        }
                     }
                     if (tr) trace_ev(p, EV_E_DONE, n_items);
                     ++n_items;

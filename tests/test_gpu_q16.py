@@ -98,6 +98,11 @@ CASES = [
     ("b16_m128", 352, 288, 3, 3, 16, 128),
     ("b32_m64", 640, 100, 3, 3, 32, 64),
     ("b32_m72", 96, 64, 3, 3, 32, 72),
+    # row-scale register paths (one fold, M = 16/32 and 48/64): multi-row tiles, ragged last tile
+    ("b16_m16", 208, 90, 5, 4, 16, 16),
+    ("b16_m32", 400, 150, 4, 2, 16, 32),
+    ("b16_m48", 176, 60, 4, 3, 16, 48),
+    ("b8_m16", 128, 56, 5, 3, 8, 16),
 ]
 
 
