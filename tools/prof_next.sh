@@ -3,8 +3,9 @@
 # (gpu__time_duration, --clock-control none) and one --set full capture of the op's main kernel.
 # usage: tools/prof_next.sh [tag]      -> gpurun_out/<tag>/<op>/{bench.json,launches.csv,prof.ncu-rep}
 TAG=${1:-r01next}
-run_op () {  # name, kernel regex, skip, count, bench args...
+run_op () {  # name, kernel regex, skip, count, bench args...   (ONLY="a b" restricts to those ops)
   local name=$1 rx=$2 skip=$3 cnt=$4; shift 4
+  if [ -n "$ONLY" ] && [[ " $ONLY " != *" $name "* ]]; then return; fi
   local OUT=gpurun_out/$TAG/$name
   mkdir -p $OUT
   local CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --tune-file $OUT/plans.json $*"
