@@ -1,0 +1,7 @@
+L=paper_1311_1419_b200/_lib
+python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --tune-file /tmp/t.json > /dev/null 2>&1
+for e in "" "CSENC_DBG_FLAGS=8" "CSENC_DBG_LOAD_ONLY=1" "CSENC_DBG_FLAGS=2"; do
+  env $e CSENC_LIB=$L/libcsenc_dbg.so python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --tune-file /tmp/t.json 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1])
+print('$e', {k:(round(v['ms_mean']*1e3,1), round(v['gpix_s'])) for k,v in d['per_M'].items()})"
+done
