@@ -345,7 +345,7 @@ def run_ours(args, cfg, Ms):
         "clocks": clk.summary(),
         "e2e": e2e,
     }
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:   # (rank 0 at N=1 only)
         line["cpu_baseline"] = cpu_baseline(cfg, Ms, budget_s=args.cpu_budget, output=args.output)
     print(json.dumps(line))
     if world > 1:
@@ -424,7 +424,7 @@ def run_adjoint(args, cfg, Ms):
         "e2e": {"value": None, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                 "how": "not measured: the adjoint has a device-buffer C-ABI call only"},
     }
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:   # (rank 0 at N=1 only)
         line["cpu_baseline"] = adjoint_cpu_baseline(cfg, Ms, args.cpu_budget)
     print(json.dumps(line))
     if world > 1:
@@ -498,7 +498,7 @@ def run_frame(args):
         "e2e": {"value": None, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                 "how": "not measured: the frame-level path has a device-buffer C-ABI call only"},
     }
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:   # (rank 0 at N=1 only)
         import oracle
         fr = synth.gen_stream(cfg, 0, T=2 * G)
         t0 = time.perf_counter()
