@@ -285,6 +285,7 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
                 break;
             }
         }
+        if (const int gwf = env_int("CSENC_FRAME_GW", 0)) fp.gw = std::max(1, std::min(gw_max, gwf));   // experiment knob
         fp.n_win_s = 0;
         fp.n_win = cdiv(fp.total_gops, fp.gw);
     } else {
@@ -332,6 +333,7 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     const long long tiles = (long long)((fp.n_win + CL - 1) / CL) * fp.n_mp;   // cluster work units
     long long ks = (n_cl + tiles - 1) / tiles;                        // K splits to fill the SMs
     ks = std::max(1LL, std::min(ks, (long long)std::max(1, fp.n_chunks / 8)));
+    if (const int ksf = env_int("CSENC_FRAME_KS", 0)) ks = std::max(1, std::min(ksf, fp.n_chunks));   // experiment knob
     // no empty K split (every unit must issue at least one chunk): ks = ceil(chunks / per-split)
     const long long per_split = (fp.n_chunks + ks - 1) / ks;
     ks = (fp.n_chunks + per_split - 1) / per_split;
