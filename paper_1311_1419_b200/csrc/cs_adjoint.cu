@@ -87,6 +87,14 @@ int launch_adjoint(cs_encoder* e, const float* meas, long long n_frames, float* 
     ap.stage_bytes = e->adj_stage_bytes;
     ap.n_stages = e->adj_stages;
     ap.n_units = (int)(n_frames * g.nby * ap.parts);
+    // flat tiles (128 consecutive blocks across block rows) when every warp's 32 blocks stay in one
+    // block row: fewer, fuller units for narrow-block frames (C5: 113 instead of 180 per frame)
+    ap.flat = (g.nbx % 32 == 0 && env_int("CSENC_ADJ_FLAT", 1)) ? 1 : 0;
+    if (ap.flat) {
+        ap.tiles_pf = cdiv(g.nblk, 128);
+        ap.L = 128;
+        ap.n_units = (int)(n_frames * ap.tiles_pf);
+    }
     // kind::tf32: D fp32 (bit 4), A/B tf32 (2 at bits 7 and 10), K-major, N>>3 at 17, M>>4 at 24
     ap.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(ap.Nc >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     ap.b_lbo = (uint32_t)ap.Nc * 16u;

@@ -48,6 +48,9 @@ struct AParams {
     float* x;                 // device: [n_frames][H][W]
     int W, H, M, nbx, nby, nblk;
     int parts, L;             // tiles per block row, blocks per tile (<= 128)
+    // flat != 0 (nbx % 32 == 0): a tile is 128 consecutive blocks of the frame's raster order, across
+    // block rows (each epilogue warp's 32 blocks still lie in one block row); tiles_pf per frame
+    int flat, tiles_pf;
     int Kc, n_kc;             // K per stage (8/16/32), K chunks
     int Nc, n_nc;             // output columns per item (<= 256), items per tile
     uint32_t a_bytes, chunk_bytes, stage_bytes;
@@ -119,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_adjoint_kernel(const __grid_co
     uint32_t tmem_base;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem_base) : "r"(tmem_slot));
 
-    const int per_frame = p.nby * p.parts;
+    const int per_frame = p.flat ? p.tiles_pf : p.nby * p.parts;
 
     if (warp == kProducerWarp) {
         // ================================================================ producer
@@ -128,7 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_adjoint_kernel(const __grid_co
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             const int f = u / per_frame, rem = u - f * per_frame;
             const int by = rem / p.parts, part = rem - by * p.parts;
-            const int row0 = f * p.nblk + by * p.nbx + part * p.L;
+            const int row0 = p.flat ? f * p.nblk + rem * 128 : f * p.nblk + by * p.nbx + part * p.L;
             for (int nc = 0; nc < p.n_nc; ++nc) {
                 for (int kc = 0; kc < p.n_kc; ++kc) {
                     ptx::mbar_wait(bar_empty + 8 * st, ph ^ 1u);
@@ -227,9 +230,18 @@ __global__ void __launch_bounds__(kThreads, 1) cs_adjoint_kernel(const __grid_co
         uint32_t dph = 0;
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             const int f = u / per_frame, rem = u - f * per_frame;
-            const int by = rem / p.parts, part = rem - by * p.parts;
-            const int bx0 = part * p.L + ew * 32;                        // first block of this warp
-            const int nv = min(32, min(p.L - ew * 32, p.nbx - bx0));      // blocks of this warp (may be <= 0)
+            int by, bx0, nv;   // block row, first block of this warp, blocks of this warp (may be <= 0)
+            if (p.flat) {
+                const int b0 = rem * 128 + ew * 32;
+                by = b0 / p.nbx;
+                bx0 = b0 - by * p.nbx;
+                nv = min(32, p.nblk - b0);
+            } else {
+                by = rem / p.parts;
+                const int part = rem - by * p.parts;
+                bx0 = part * p.L + ew * 32;
+                nv = min(32, min(p.L - ew * 32, p.nbx - bx0));
+            }
             const int col0 = bx0 * B;
             const int valid = nv > 0 ? min(nv * B, p.W - col0) : 0;
             for (int nc = 0; nc < p.n_nc; ++nc) {

@@ -53,6 +53,10 @@ CASES = [
     (32, 32, 16, 256, 2),
     (1280, 24, 8, 16, 3),       # nbx = 160 > 128: two 80-block parts per block row
     (2096, 16, 16, 32, 1),      # nbx = 131: parts of 66 / 65 blocks
+    # nbx % 32 == 0: flat 128-block tiles across block rows
+    (512, 40, 16, 32, 3),       # nbx = 32, ragged H, one partial tile per frame
+    (2048, 16, 32, 64, 2),      # nbx = 64, B = 32 (4 output chunks)
+    (1024, 72, 8, 8, 2),        # nbx = 128, 9 whole tiles per frame
 ]
 
 
