@@ -341,15 +341,23 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     if (tiles * ks > 0x7FFFFFFFLL) return fail(CS_ERR_UNSUPPORTED, "too many work units");
     fp.n_units = (int)(tiles * ks);
     fp.fbox_bytes = (uint32_t)fp.nf_box * (uint32_t)csenc::frm::kKc;
-    fp.off_a = align_up(fp.fbox_bytes, 1024);
-    fp.stage_bytes = fp.off_a + 256u * csenc::frm::kKc * 2u;
+    fp.stage_bytes = align_up(fp.fbox_bytes, 1024);                    // frames ring slot
+    const uint32_t a_slot = 256u * csenc::frm::kKc * 2u;                // A ring slot (32 KB)
     fp.b_bytes = align_up((uint32_t)(fp.gw * (G - 1) + 15) / 16 * 16 * 128u, 1024);
     fp.n_b = std::max(2, std::min(4, env_int("CSENC_FRAME_BBUFS", 2)));
     fp.off_stage = csenc::frm::kOffB + (uint32_t)fp.n_b * fp.b_bytes;
+    // A ring: 3 slots (A is L2-resident: short latency); frames ring: the rest, up to kMaxStages
+    // (frames come from HBM and are consumed first)
     const long avail = (long)f->smem_limit - 1024 - (long)fp.off_stage;
-    fp.n_stages = (int)std::min<long>(csenc::frm::kMaxStages, avail / (long)fp.stage_bytes);
-    if (fp.n_stages < 2) return fail(CS_ERR_UNSUPPORTED, "frame measurement: stages do not fit shared memory");
-    const uint32_t smem = 1024 + fp.off_stage + (uint32_t)fp.n_stages * fp.stage_bytes;
+    fp.n_a = std::max(2, std::min(csenc::frm::kMaxStages, env_int("CSENC_FRAME_ASLOTS", 3)));
+    fp.n_stages = (int)std::min<long>(csenc::frm::kMaxStages, (avail - (long)fp.n_a * a_slot) / (long)fp.stage_bytes);
+    while (fp.n_stages < 2 && fp.n_a > 2) {
+        --fp.n_a;
+        fp.n_stages = (int)std::min<long>(csenc::frm::kMaxStages, (avail - (long)fp.n_a * a_slot) / (long)fp.stage_bytes);
+    }
+    if (fp.n_stages < 2) return fail(CS_ERR_UNSUPPORTED, "frame measurement: rings do not fit shared memory");
+    fp.off_a = fp.off_stage + (uint32_t)fp.n_stages * fp.stage_bytes;   // 1024-aligned (slots are)
+    const uint32_t smem = 1024 + fp.off_a + (uint32_t)fp.n_a * a_slot;
     fp.prefetch = env_int("CSENC_FRAME_PREFETCH", 0);
     fp.trace = f->trace;
     fp.trace_cap = f->trace_cap;

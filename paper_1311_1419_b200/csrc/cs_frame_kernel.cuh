@@ -12,7 +12,10 @@
 //   R: TMA 2-D box [nf rows][64 bytes] of a window of whole GOPs (keys included, SWIZZLE_64B);
 //      4 converter warps form the exact fp16 residual of every CS frame of the window against its
 //      GOP key (same box) and write it as the SW128 K-major B operand.
-// Roles (14 warps): 0-7 converters, 8-11 epilogue, 12 TMA producer, 13 MMA issuer + TMEM allocator.
+// Roles (15 warps): 0-7 converters, 8-11 epilogue, 12 frames producer, 13 MMA issuer + TMEM allocator,
+// 14 A producer.  The frame boxes (from HBM, needed first: by the converters) and the A tiles (from L2,
+// needed last: by the MMA) run in two rings of their own depths, so the frames are fetched far ahead
+// (up to 8 chunks) while A occupies only the slots the MMA is about to use.
 // Unit = (K split, window of whole GOPs of one stream, pair of 128-row m-tiles = one 256-row A box);
 // item = one 64-pixel K chunk: one residual operand feeds both m-tiles' MMAs (D uses all 512 TMEM
 // columns), halving the conversion work and the frame-box traffic per flop.  With more than one K split the units write fp32 partials that a second kernel sums in a
@@ -30,9 +33,10 @@ namespace frm {
 
 constexpr int kConvWarps = 8;
 constexpr int kEpiWarp0 = 8;
-constexpr int kProducerWarp = 12;
+constexpr int kProducerWarp = 12;   // frame boxes
 constexpr int kMmaWarp = 13;
-constexpr int kThreads = 14 * 32;
+constexpr int kAProducerWarp = 14;  // A tiles
+constexpr int kThreads = 15 * 32;
 constexpr int kMaxStages = 8;
 constexpr int kKc = 64;                          // pixels per K chunk
 constexpr uint32_t kTmemCols = 512;
@@ -49,11 +53,14 @@ struct FParams {
     int total_gops;           // n_seq * T / G (global_win)
     int n_mp, n_ks, n_chunks; // 256-row m-pairs, K splits, 64-pixel chunks
     int n_units;
-    uint32_t fbox_bytes, off_a, stage_bytes;
+    uint32_t fbox_bytes;      // one frame box (nf_box rows x 64 B)
+    uint32_t off_a;           // A ring: n_a slots of 256 * kKc fp16 (32 KB), 1024-aligned
+    int n_a;
+    uint32_t stage_bytes;     // frames ring slot (fbox_bytes rounded up to 1024)
     uint32_t b_bytes;         // one residual buffer: roundup(window CS rows * 128, 1024)
     int n_b;                  // residual buffers (2..4)
-    uint32_t off_stage;       // kOffB + n_b * b_bytes
-    int n_stages;
+    uint32_t off_stage;       // frames ring: kOffB + n_b * b_bytes
+    int n_stages;             // frames ring slots
     long long part_stride;    // floats per partial plane (n_seq * cs_s * m rounded up to 4)
     int prefetch;             // frame boxes prefetched into L2 this many chunks ahead (0 = off)
     unsigned long long* trace;   // debug timeline (CTA 0): [4][trace_cap] clock64, nullptr = off
@@ -120,8 +127,10 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31u;
 
-    const uint32_t bar_full = sbase;                      // [kMaxStages] TMA -> converters, MMA
-    const uint32_t bar_empty = sbase + 8 * kMaxStages;    // [kMaxStages] MMA -> producer
+    const uint32_t bar_full = sbase;                      // [kMaxStages] frame box landed -> converters
+    const uint32_t bar_empty = sbase + 8 * kMaxStages;    // [kMaxStages] converters done -> frames producer
+    const uint32_t bar_afull = sbase + 32 * kMaxStages;   // [kMaxStages] A tile landed -> MMA
+    const uint32_t bar_aempty = sbase + 40 * kMaxStages;  // [kMaxStages] MMA done -> A producer
     const uint32_t bar_conv = sbase + 16 * kMaxStages;    // [4] converters -> MMA (B buffer written)
     const uint32_t bar_bempty = bar_conv + 32;            // [4] MMA -> converters (B buffer free)
     const uint32_t bar_dfull = bar_bempty + 32;
@@ -134,7 +143,11 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
     if (threadIdx.x == 0) {
         for (int i = 0; i < p.n_stages; ++i) {
             ptx::mbar_init(bar_full + 8 * i, 1);
-            ptx::mbar_init(bar_empty + 8 * i, CL);   // every CTA's MMAs must be done with the (shared) A tile
+            ptx::mbar_init(bar_empty + 8 * i, kConvWarps);
+        }
+        for (int i = 0; i < p.n_a; ++i) {
+            ptx::mbar_init(bar_afull + 8 * i, 1);
+            ptx::mbar_init(bar_aempty + 8 * i, CL);   // every CTA's MMAs must be done with the (shared) A tile
         }
         for (int i = 0; i < 4; ++i) {
             ptx::mbar_init(bar_conv + 8 * i, kConvWarps);
@@ -152,8 +165,9 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         ptx::prefetch_tmap(&p.fmap);
         ptx::prefetch_tmap(&p.amap);
     }
-    CS_CHECK(p.off_stage + (uint32_t)p.n_stages * p.stage_bytes <= p.smem_bytes && p.n_stages <= kMaxStages);
-    CS_CHECK(p.off_a + 256u * kKc * 2u <= p.stage_bytes && p.fbox_bytes <= p.off_a && p.n_b <= 4);
+    CS_CHECK(p.off_stage + (uint32_t)p.n_stages * p.stage_bytes <= p.off_a && p.n_stages <= kMaxStages);
+    CS_CHECK(p.off_a + (uint32_t)p.n_a * 256u * kKc * 2u <= p.smem_bytes && p.n_a <= kMaxStages);
+    CS_CHECK(p.fbox_bytes <= p.stage_bytes && p.n_b <= 4);
     ptx::tc_fence_before();
     if constexpr (CL > 1)
         ptx::cluster_sync();   // peers' barriers initialised before any multicast lands in them
@@ -180,16 +194,11 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                     ptx::tma_prefetch_2d(&p.fmap, (kc + p.prefetch) * kKc, row0);
                 if (lane == 0) {
                     const uint32_t sf = sbase + p.off_stage + (uint32_t)st * p.stage_bytes;
-                    const bool has = w.n_cs > 0;
-                    ptx::mbar_arrive_expect_tx(bar_full + 8 * st, (has ? p.fbox_bytes : 0u) + 256u * kKc * 2u);
-                    if (has) ptx::tma_load_2d(sf, &p.fmap, bar_full + 8 * st, kc * kKc, row0);
-                    if constexpr (CL == 1) {
-                        ptx::tma_load_2d(sf + p.off_a, &p.amap, bar_full + 8 * st, kc * kKc, w.mp * 256);
+                    if (w.n_cs > 0) {
+                        ptx::mbar_arrive_expect_tx(bar_full + 8 * st, p.fbox_bytes);
+                        ptx::tma_load_2d(sf, &p.fmap, bar_full + 8 * st, kc * kKc, row0);
                     } else {
-                        // this CTA's share of the 256-row A tile, multicast to every CTA of the cluster
-                        constexpr int kRows = 256 / CL;
-                        ptx::tma_load_2d_mc(sf + p.off_a + (uint32_t)(rank * kRows * kKc * 2), &p.amap, bar_full + 8 * st,
-                                            kc * kKc, w.mp * 256 + rank * kRows, kMask);
+                        ptx::mbar_arrive(bar_full + 8 * st);   // empty dummy window (cluster padding)
                     }
                     ftrace(p, 0, ntr);
                 }
@@ -198,6 +207,34 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                 if (++st == p.n_stages) {
                     st = 0;
                     ph ^= 1u;
+                }
+            }
+        }
+    } else if (warp == kAProducerWarp) {
+        // ================================================================ A producer
+        int as = 0;
+        uint32_t aph = 0;
+        for (int u = cid; u < p.n_units; u += n_cl) {
+            FUnit w;
+            decode_funit<CL>(p, u, rank, w);
+            for (int kc = w.kc0; kc < w.kc1; ++kc) {
+                ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
+                if (lane == 0) {
+                    const uint32_t sa = sbase + p.off_a + (uint32_t)as * (256u * kKc * 2u);
+                    ptx::mbar_arrive_expect_tx(bar_afull + 8 * as, 256u * kKc * 2u);
+                    if constexpr (CL == 1) {
+                        ptx::tma_load_2d(sa, &p.amap, bar_afull + 8 * as, kc * kKc, w.mp * 256);
+                    } else {
+                        // this CTA's share of the 256-row A tile, multicast to every CTA of the cluster
+                        constexpr int kRows = 256 / CL;
+                        ptx::tma_load_2d_mc(sa + (uint32_t)(rank * kRows * kKc * 2), &p.amap, bar_afull + 8 * as,
+                                            kc * kKc, w.mp * 256 + rank * kRows, kMask);
+                    }
+                }
+                __syncwarp();
+                if (++as == p.n_a) {
+                    as = 0;
+                    aph ^= 1u;
                 }
             }
         }
@@ -253,7 +290,10 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                 }
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(bar_conv + 8 * b);
+                if (lane == 0) {
+                    ptx::mbar_arrive(bar_conv + 8 * b);
+                    ptx::mbar_arrive(bar_empty + 8 * st);   // frame box read (values are in registers)
+                }
                 if (tid == 0) ftrace(p, 2, ntr);
                 ++ntr;
                 if (++st == p.n_stages) {
@@ -270,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         // ================================================================ MMA issuer
         // D: m-tile 0 at TMEM columns [0, N), m-tile 1 at [256, 256 + N); single-buffered (a unit is
         // hundreds of chunks long, the epilogue a few thousand cycles)
-        int st = 0, b = 0, ntr = 0;
+        int st = 0, b = 0, ntr = 0;   // st: A ring slot
         uint32_t ph = 0, bph = 0, dph = 0;
         for (int u = cid; u < p.n_units; u += n_cl) {
             FUnit w;
@@ -281,11 +321,11 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
             ptx::mbar_wait(bar_dempty, dph ^ 1u);
             ptx::tc_fence_after();
             for (int kc = w.kc0; kc < w.kc1; ++kc) {
-                ptx::mbar_wait(bar_full + 8 * st, ph);
+                ptx::mbar_wait(bar_afull + 8 * st, ph);
                 ptx::mbar_wait(bar_conv + 8 * b, bph);
                 ptx::tc_fence_after();
                 if (lane == 0) {
-                    const uint32_t sa = sbase + p.off_stage + (uint32_t)st * p.stage_bytes + p.off_a;
+                    const uint32_t sa = sbase + p.off_a + (uint32_t)st * (256u * kKc * 2u);
                     const uint64_t a0 = ptx::smem_desc_swizzled(sa, 128u, 1024u);
                     const uint64_t a1 = ptx::smem_desc_swizzled(sa + 128u * 128u, 128u, 1024u);
                     const uint64_t bd = ptx::smem_desc_swizzled(sbase + kOffB + (uint32_t)b * p.b_bytes, 128u, 1024u);
@@ -298,16 +338,16 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                             ptx::mma_f16_ss(tmem_base + 256u, a1 + (uint64_t)(ks * 2), bd + (uint64_t)(ks * 2), idesc, acc);
                     }
                     if constexpr (CL == 1)
-                        ptx::tc_commit(bar_empty + 8 * st);
+                        ptx::tc_commit(bar_aempty + 8 * st);
                     else
-                        ptx::tc_commit_mc(bar_empty + 8 * st, kMask);   // frees the stage in every CTA
+                        ptx::tc_commit_mc(bar_aempty + 8 * st, kMask);   // frees the A slot in every CTA
                     ptx::tc_commit(bar_bempty + 8 * b);
                     if (kc == w.kc1 - 1) ptx::tc_commit(bar_dfull);
                     ftrace(p, 3, ntr);
                 }
                 ++ntr;
                 __syncwarp();
-                if (++st == p.n_stages) {
+                if (++st == p.n_a) {
                     st = 0;
                     ph ^= 1u;
                 }
