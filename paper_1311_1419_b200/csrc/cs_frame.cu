@@ -356,6 +356,7 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
         fp.n_stages = (int)std::min<long>(csenc::frm::kMaxStages, (avail - (long)fp.n_a * a_slot) / (long)fp.stage_bytes);
     }
     if (fp.n_stages < 2) return fail(CS_ERR_UNSUPPORTED, "frame measurement: rings do not fit shared memory");
+    if (const int fs = env_int("CSENC_FRAME_FSLOTS", 0)) fp.n_stages = std::max(2, std::min(fp.n_stages, fs));   // knob
     fp.off_a = fp.off_stage + (uint32_t)fp.n_stages * fp.stage_bytes;   // 1024-aligned (slots are)
     const uint32_t smem = 1024 + fp.off_a + (uint32_t)fp.n_a * a_slot;
     fp.prefetch = env_int("CSENC_FRAME_PREFETCH", 0);
