@@ -620,7 +620,7 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-autotune", action="store_true")
-    ap.add_argument("--tune-candidates", type=int, default=6)
+    ap.add_argument("--tune-candidates", type=int, default=12)
     ap.add_argument("--op", choices=["encode", "adjoint", "closed_loop", "frame"], default="encode",
                     help="encode (the north-star hot path, default), adjoint (f3 back-projection) or "
                          "closed_loop (f4: key codec + encode against the decoded keys)")
