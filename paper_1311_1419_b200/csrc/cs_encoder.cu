@@ -370,6 +370,22 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.scales = q.scales;
     kp.arrivals = q.arrivals;
     kp.lookback = std::max(1, std::min(std::min(csenc::kMaxLag, pl.n_dbuf - 1), env_int("CSENC_LOOKBACK", 99)));
+    // multi-piece strips by one 4-D TMA box (H % B == 0 so block rows never run into the next frame;
+    // the box's inner extent W/4 u32 words <= 256; pieces packed back to back in the stage)
+    if (pl.pieces > 1 && !pl.single_piece && g.H % g.B == 0 && g.W % 4 == 0 && g.W / 4 <= 256 &&
+        pl.piece_bytes == (uint32_t)(pl.piece_rows * g.W) && env_int("CSENC_TMA_STRIPS", 1)) {
+        PFN_encodeTiled enc = get_encode_tiled();
+        if (enc) {
+            cuuint64_t dims[4] = {(cuuint64_t)(g.W / 4), (cuuint64_t)g.B, (cuuint64_t)g.nby, (cuuint64_t)n_seq * T};
+            cuuint64_t strides[3] = {(cuuint64_t)g.W, (cuuint64_t)g.B * g.W, (cuuint64_t)g.H * g.W};
+            cuuint32_t box[4] = {(cuuint32_t)(g.W / 4), (cuuint32_t)pl.chunk_rows, (cuuint32_t)pl.T_r, 1u};
+            cuuint32_t estr[4] = {1, 1, 1, 1};
+            CUresult r = enc(&kp.smap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<uint8_t*>(frames), dims, strides,
+                             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            kp.tma_strips = (r == CUDA_SUCCESS && pl.T_r <= 256) ? 1 : 0;
+        }
+    }
     int grid = std::max(1, std::min(e->sms, kp.n_units));
     if (q.gop_rounds) grid = std::max(1, std::min(e->sms / pl.n_tiles * pl.n_tiles, kp.n_units));
     cudaError_t err;

@@ -30,6 +30,7 @@
 // (KM=1), a_full/empty (converters <-> MMA, TMEM A buffers), d_full/empty (MMA <-> epilogue,
 // TMEM accumulators).  Paper passages: Eq.(1) P:83-85, P:87 and Eq.(2)-(3) P:89-91.
 #pragma once
+#include <cuda.h>
 #include <cstdint>
 
 #include "ptx_sm100.cuh"
@@ -95,6 +96,11 @@ static_assert(kRowBarOff + 8 * kRowBufs <= kRowSlotOff, "row barriers overlap th
 static_assert(kRowSlotTileOff + kRowBufs * kRowRegRows * 4 <= 4096, "row slots overflow the staging tile");
 
 struct KParams {
+    // tma_strips != 0 (multi-piece plans, H % B == 0): the T_r pieces of a strip arrive by ONE 4-D TMA
+    // box of smap = frames as u32 words [n_seq*T][nby][B][W/4], box [1][T_r][chunk_rows][W/4] (block
+    // rows past nby zero-filled) instead of T_r bulk copies
+    alignas(64) CUtensorMap smap;
+    int tma_strips;
     const uint8_t* frames;    // device [n_seq][T][H][W]
     const uint8_t* zeros;     // device, >= piece_rows * W zero bytes (rows beyond H)
     float* out;
@@ -199,7 +205,11 @@ __device__ __forceinline__ int key_frame(const KParams& p, const Unit& w) { retu
 // mbarrier transaction count of a slot is a constant.
 template <int B>
 __device__ __forceinline__ void load_strips(const KParams& p, uint32_t dst, const uint8_t* frame, int t, int k,
-                                            uint32_t bar, uint64_t policy) {
+                                            uint32_t bar, uint64_t policy, int fidx = -1) {
+    if (fidx >= 0 && p.tma_strips) {   // all T_r pieces in one box (frame index fidx of `frames`)
+        ptx::tma_load_4d(dst, &p.smap, bar, 0, k * p.chunk_rows, t * p.T_r, fidx, policy);
+        return;
+    }
     for (int pc = 0; pc < p.pieces; ++pc) {
         const int y0 = p.single_piece ? t * p.T_r * B : (t * p.T_r + pc) * B + k * p.chunk_rows;
         const int rows = max(0, min(p.piece_rows, p.H - y0));
@@ -525,7 +535,9 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                     ++phi_loads;
                 }
             }
-            const uint8_t* const raw_key = p.frames + (size_t)key_frame(p, w) * frame_bytes;
+            const int key_idx = key_frame(p, w);
+            const uint8_t* const raw_key = p.frames + (size_t)key_idx * frame_bytes;
+            const int keyf_idx = p.keys ? -1 : key_idx;   // decoded keys live in another buffer: bulk copies
             const uint8_t* const key_f =
                 p.keys ? p.keys + ((size_t)w.s * p.n_gops_T + (size_t)w.g) * frame_bytes : raw_key;
             if constexpr (KM == KEY_REGS) {  // the key strip is the unit's first ring item
@@ -533,7 +545,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                 if (elect_one()) {
                     ptx::mbar_arrive_expect_tx(bar_stage_full + 8 * st, p.set_bytes);
                     load_strips<B>(p, s_stage + (uint32_t)st * p.stage_bytes, key_f, w.t, 0, bar_stage_full + 8 * st,
-                                   pol_key);
+                                   pol_key, keyf_idx);
                 }
                 __syncwarp();
                 if (++st == p.n_stages) {
@@ -546,7 +558,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                     ptx::mbar_arrive_expect_tx(bar_key_full + 8 * kb, (uint32_t)p.n_chunks * p.set_bytes);
                     for (int k = 0; k < p.n_chunks; ++k)
                         load_strips<B>(p, s_key + (uint32_t)kb * p.key_bytes + (uint32_t)k * p.stage_cs_bytes, key_f,
-                                       w.t, k, bar_key_full + 8 * kb, pol_key);
+                                       w.t, k, bar_key_full + 8 * kb, pol_key, keyf_idx);
                 }
                 __syncwarp();
                 kb ^= 1;
@@ -561,10 +573,10 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                     if (elect_one()) {
                         ptx::mbar_arrive_expect_tx(bar_stage_full + 8 * st,
                                                    (KM == KEY_STREAMED ? 2u : 1u) * p.set_bytes);
-                        load_strips<B>(p, dst, cs_f, w.t, k, bar_stage_full + 8 * st, pol_stream);
+                        load_strips<B>(p, dst, cs_f, w.t, k, bar_stage_full + 8 * st, pol_stream, key_idx + 1 + c);
                         if constexpr (KM == KEY_STREAMED)   // chained (Eq. 3 literal): reference = previous frame
                             load_strips<B>(p, dst + p.stage_cs_bytes, p.chained ? cs_f - frame_bytes : key_f, w.t, k,
-                                           bar_stage_full + 8 * st, pol_key);
+                                           bar_stage_full + 8 * st, pol_key, p.chained ? key_idx + c : keyf_idx);
                     }
                     __syncwarp();
                     if (lane == 0) trace_ev(p, EV_P_ISSUED, n_items);
