@@ -73,6 +73,7 @@ typedef struct cs_plan_info {
     int a_bufs;            /* TMEM A-operand ring depth (converters -> MMA) */
     int d_bufs;            /* TMEM accumulator ring depth (MMA -> epilogue) */
     int sms;               /* SMs of the device at create time */
+    int phi_stream;        /* 1: Phi's K-slices ride in the stages (multi-chunk plans), 0: Phi resident in SMEM */
 } cs_plan_info;
 
 /* ---- lifecycle ------------------------------------------------------------------------- */

@@ -33,7 +33,7 @@ class CSError(RuntimeError):
 class PlanInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int) for n in (
         "tile_block_rows", "folds", "lanes", "chunk_rows", "stages", "key_resident", "box_w", "smem_bytes",
-        "tmem_cols", "m_pad", "chains", "prefetch_items", "a_bufs", "d_bufs", "sms")]
+        "tmem_cols", "m_pad", "chains", "prefetch_items", "a_bufs", "d_bufs", "sms", "phi_stream")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -27,7 +27,7 @@ constexpr long kMaxPhiBytes = 160 * 1024;  // Phi is SMEM-resident for the whole
 
 // key_mode: 0 = key strip streamed with every item, 1 = resident in SMEM (double-buffered),
 //           2 = in converter registers (arrives once per unit through a ring slot)
-bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem_limit, Plan& p) {
+bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem_limit, Plan& p, int phi_stream = 0) {
     const bool key_res = key_mode == 1;
     p = Plan();
     const int words = g.B / 2;          // fp16x2 columns per pixel row
@@ -93,7 +93,17 @@ bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem
     }
     p.key_bytes = key_res ? (uint32_t)p.n_chunks * p.stage_cs_bytes : 0;
     p.stage_bytes = (key_res || p.key_regs) ? p.stage_cs_bytes : 2 * p.stage_cs_bytes;
-    const uint32_t phi_bytes = (uint32_t)g.Mpad * (uint32_t)g.N * 2u;
+    uint32_t phi_bytes = (uint32_t)g.Mpad * (uint32_t)g.N * 2u;
+    if (phi_stream) {
+        // Phi's K-slice for the chunk rides in every stage (the canonical layout keeps a chunk's
+        // chunk_k / 8 K-groups contiguous); nothing of Phi stays resident
+        if (p.n_chunks < 2 || p.key_regs) return false;
+        p.phi_stream = 1;
+        p.phi_slice_bytes = phi_bytes / (uint32_t)p.n_chunks;
+        p.stage_phi_off = align_up(p.stage_bytes, 128);
+        p.stage_bytes = align_up(p.stage_phi_off + p.phi_slice_bytes, 128);
+        phi_bytes = 0;
+    }
     p.off_tab = 1024;  // barriers live in the first KB, then the converter offset table (8 KB)
     p.off_epi = 1024 + 8192;  // epilogue staging tiles (4 warps x 4 KB)
     p.off_phi = 1024 + 8192 + 16384;
@@ -115,7 +125,7 @@ bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem
     const int groups_per_wg = (p.F * groups_per_fold + 1) / 2;
     const double px = (double)tile_blocks * p.chunk_k;
     const double item_bytes = (double)p.stage_bytes;
-    const int copies = p.pieces * ((key_res || p.key_regs) ? 1 : 2);
+    const int copies = p.pieces * ((key_res || p.key_regs) ? 1 : 2) + p.phi_stream;
     const double conv = 350.0 * groups_per_wg;
     const double load = item_bytes / 32.0;
     const double mma = (double)(p.chunk_k / 16) * p.F * std::max(48.0, g.Mpad / 2.0);
@@ -139,6 +149,7 @@ std::vector<Plan> plan_candidates(const Geometry& g, int smem_limit) {
     // experiment knobs (tools/sweep.sh): force a tile-row count / chunk size / key residency
     const int f_tr = env_int("CSENC_TILE_ROWS", 0), f_cr = env_int("CSENC_CHUNK_ROWS", 0);
     const int f_kr = env_int("CSENC_KEY_RESIDENT", -1), f_st = env_int("CSENC_STAGES", 0);
+    const int f_ps = env_int("CSENC_PHI_STREAM", -1);
     for (int T_r = 1; T_r <= g.nby; ++T_r) {
         if (T_r * g.nbx > 128 * csenc::kMaxFolds) break;
         if (f_tr && T_r != f_tr) continue;
@@ -146,13 +157,16 @@ std::vector<Plan> plan_candidates(const Geometry& g, int smem_limit) {
             if (f_cr && cr != f_cr) continue;
             for (int kr = 2; kr >= 0; --kr) {
                 if (f_kr >= 0 && kr != f_kr) continue;
-                Plan p;
-                if (!try_plan(g, T_r, cr, kr, smem_limit, p)) continue;
-                if (f_st > 0 && f_st < p.n_stages) {
-                    p.smem_bytes -= (uint32_t)(p.n_stages - f_st) * p.stage_bytes;
-                    p.n_stages = f_st;
+                for (int ps = 0; ps <= 1; ++ps) {
+                    if (f_ps >= 0 && ps != f_ps) continue;
+                    Plan p;
+                    if (!try_plan(g, T_r, cr, kr, smem_limit, p, ps)) continue;
+                    if (f_st > 0 && f_st < p.n_stages) {
+                        p.smem_bytes -= (uint32_t)(p.n_stages - f_st) * p.stage_bytes;
+                        p.n_stages = f_st;
+                    }
+                    all.push_back(p);
                 }
-                all.push_back(p);
             }
         }
     }
@@ -323,6 +337,9 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.out_floats = (long long)n_seq * cs_frames_in_gops(T, g.G, g0, g1) * g.nblk * g.M;
     kp.frames_bytes = (long long)n_seq * T * g.W * g.H;
     kp.stage_cs_bytes = pl.stage_cs_bytes;
+    kp.phi_stream = pl.phi_stream;
+    kp.phi_slice_bytes = pl.phi_slice_bytes;
+    kp.stage_phi_off = pl.stage_phi_off;
     kp.stage_bytes = pl.stage_bytes;
     kp.key_bytes = pl.key_bytes;
 
@@ -620,6 +637,7 @@ static void fill_info(const Plan& p, const Geometry& g, int sms, cs_plan_info* i
     info->tmem_cols = p.tmem_cols;
     info->m_pad = g.Mpad;
     info->chains = 1;
+    info->phi_stream = p.phi_stream;
     info->sms = sms;
 }
 

@@ -48,6 +48,8 @@ struct Plan {
     int pieces = 0, piece_rows = 0, single_piece = 0;
     uint32_t piece_bytes = 0, stage_cs_bytes = 0, stage_bytes = 0, key_bytes = 0;
     int key_resident = 0, key_regs = 0, n_stages = 0, prefetch_items = 0;
+    int phi_stream = 0;                       // Phi K-slices ride in the stages instead of staying resident
+    uint32_t phi_slice_bytes = 0, stage_phi_off = 0;
     uint32_t off_tab = 0, off_epi = 0, off_phi = 0, off_key = 0, off_stage = 0, smem_bytes = 0;
     int a_cols = 0, d_cols = 0, tmem_cols = 0, n_abuf = 2, n_dbuf = 2;
     double score = -1.0;

@@ -101,6 +101,11 @@ struct KParams {
     // rows past nby zero-filled) instead of T_r bulk copies
     alignas(64) CUtensorMap smap;
     int tma_strips;
+    // phi_stream != 0 (multi-chunk plans, KM 0/1): Phi is not resident; each stage carries the K-slice
+    // of Phi its chunk needs (phi_slice_bytes at stage offset stage_phi_off, a contiguous range of the
+    // canonical layout), and the stage is freed only when the converters AND the MMAs are done with it
+    int phi_stream;
+    uint32_t phi_slice_bytes, stage_phi_off;
     const uint8_t* frames;    // device [n_seq][T][H][W]
     const uint8_t* zeros;     // device, >= piece_rows * W zero bytes (rows beyond H)
     float* out;
@@ -430,6 +435,9 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
     const uint32_t tmem_slot = bar_phi + 8;
     const uint32_t bar_phi_empty = bar_phi + 16;   // per-GOP Phi: MMAs on the current Phi done
     const uint32_t s_phi = sbase + p.off_phi;
+    // Phi streaming and 4-D strip boxes only exist for multi-chunk plans, which never hold the key in
+    // registers: compiled out of the KEY_REGS instantiations (their code stays as small as before)
+    const bool phi_stream = KM != KEY_REGS && p.phi_stream;
     const uint32_t s_key = sbase + p.off_key;
     const uint32_t s_stage = sbase + p.off_stage;
     CS_CHECK(p.off_stage + (uint32_t)p.n_stages * p.stage_bytes <= p.smem_bytes);
@@ -440,7 +448,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
     if (threadIdx.x == 0) {
         for (int i = 0; i < p.n_stages; ++i) {
             ptx::mbar_init(bar_stage_full + 8 * i, 1);
-            ptx::mbar_init(bar_stage_empty + 8 * i, kConvWarps);
+            ptx::mbar_init(bar_stage_empty + 8 * i, kConvWarps + (phi_stream ? 1 : 0));
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(bar_key_full + 8 * i, 1);
@@ -504,7 +512,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         const uint64_t pol_stream = ptx::policy_evict_first();
         const uint64_t pol_key = ptx::policy_evict_last();
         const size_t frame_bytes = (size_t)p.W * (size_t)p.H;
-        if (p.n_phis == 0) {
+        if (p.n_phis == 0 && !phi_stream) {
             if (elect_one()) {
                 ptx::mbar_arrive_expect_tx(bar_phi, p.phi_bytes);
                 ptx::bulk_load(s_phi, p.phi, p.phi_bytes, bar_phi);
@@ -521,7 +529,8 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             Unit w;
             if (!decode_unit(p, u, w)) continue;
-            if (p.n_phis > 0) {   // per-GOP Phi: reload when the GOP's matrix differs from the resident one
+            const uint8_t* const phi_src = reinterpret_cast<const uint8_t*>(p.n_phis > 0 ? p.phis + (size_t)(w.g % p.n_phis) * (p.phi_bytes / 2) : p.phi);
+            if (p.n_phis > 0 && !phi_stream) {   // per-GOP Phi: reload when the GOP's matrix differs from the resident one
                 const int gsel = w.g % p.n_phis;
                 if (gsel != phi_cur) {
                     if (phi_loads > 0) ptx::mbar_wait(bar_phi_empty, (phi_loads - 1u) & 1u);
@@ -545,7 +554,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                 if (elect_one()) {
                     ptx::mbar_arrive_expect_tx(bar_stage_full + 8 * st, p.set_bytes);
                     load_strips<B>(p, s_stage + (uint32_t)st * p.stage_bytes, key_f, w.t, 0, bar_stage_full + 8 * st,
-                                   pol_key, keyf_idx);
+                                   pol_key);   // (KEY_REGS plans are single-piece: plain bulk copy)
                 }
                 __syncwarp();
                 if (++st == p.n_stages) {
@@ -572,8 +581,12 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                     const uint32_t dst = s_stage + (uint32_t)st * p.stage_bytes;
                     if (elect_one()) {
                         ptx::mbar_arrive_expect_tx(bar_stage_full + 8 * st,
-                                                   (KM == KEY_STREAMED ? 2u : 1u) * p.set_bytes);
-                        load_strips<B>(p, dst, cs_f, w.t, k, bar_stage_full + 8 * st, pol_stream, key_idx + 1 + c);
+                                                   (KM == KEY_STREAMED ? 2u : 1u) * p.set_bytes + (phi_stream ? p.phi_slice_bytes : 0u));
+                        if (phi_stream)   // this chunk's K-slice of Phi (L2-resident)
+                            ptx::bulk_load(dst + p.stage_phi_off, phi_src + (size_t)k * p.phi_slice_bytes, p.phi_slice_bytes,
+                                           bar_stage_full + 8 * st);
+                        load_strips<B>(p, dst, cs_f, w.t, k, bar_stage_full + 8 * st, pol_stream,
+                                       KM == KEY_REGS ? -1 : key_idx + 1 + c);
                         if constexpr (KM == KEY_STREAMED)   // chained (Eq. 3 literal): reference = previous frame
                             load_strips<B>(p, dst + p.stage_cs_bytes, p.chained ? cs_f - frame_bytes : key_f, w.t, k,
                                            bar_stage_full + 8 * st, pol_key, p.chained ? key_idx + c : keyf_idx);
@@ -621,10 +634,12 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         // ================================================================ MMA issuer
         // The whole warp walks the schedule (warp-uniform control flow keeps every operand in
         // uniform registers); one elected lane issues the tcgen05 instructions.
-        if (p.n_phis == 0) {
+        if (p.n_phis == 0 && !phi_stream) {
             ptx::mbar_wait(bar_phi, 0);
             ptx::tc_fence_after();
         }
+        int pst = 0;   // phi_stream: stage of the current chunk (one stage per chunk: KM 0/1)
+        uint32_t pph = 0;
         int phi_cur = -1;
         uint32_t phi_waits = 0;
         int ab = 0, db = 0;
@@ -640,7 +655,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             Unit w;
             if (!decode_unit(p, u, w)) continue;
-            if (p.n_phis > 0) {
+            if (p.n_phis > 0 && !phi_stream) {
                 const int gsel = w.g % p.n_phis;
                 if (gsel != phi_cur) {
                     // release the resident Phi once every MMA issued so far has completed, then wait
@@ -662,6 +677,10 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                 uint64_t dk = desc0;
                 for (int k = 0; k < p.n_chunks; ++k, dk += desc_chunk) {
                     ptx::mbar_wait(bar_a_full + 8 * ab, aph);
+                    if (phi_stream) {   // the chunk's Phi slice rides in its stage (landed: the converters saw it)
+                        ptx::mbar_wait(bar_stage_full + 8 * pst, pph);
+                        dk = ptx::smem_desc_noswizzle(s_stage + (uint32_t)pst * p.stage_bytes + p.stage_phi_off, p.lbo, p.sbo);
+                    }
                     ptx::tc_fence_after();
                     if (lane == 0) trace_ev(p, EV_M_AFULL, n_items);
                     const uint32_t a_tm = tmem_base + a_col0 + (uint32_t)ab * (uint32_t)p.a_cols;
@@ -681,8 +700,13 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                             }
                         }
                         ptx::tc_commit(bar_a_empty + 8 * ab);
+                        if (phi_stream) ptx::tc_commit(bar_stage_empty + 8 * pst);   // slice read: stage may go
                     }
                     __syncwarp();
+                    if (phi_stream && ++pst == p.n_stages) {
+                        pst = 0;
+                        pph ^= 1u;
+                    }
                     if (lane == 0) trace_ev(p, EV_M_ISSUED, n_items);
                     ++n_items;
                     if (++ab == p.n_abuf) {

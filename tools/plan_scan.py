@@ -43,5 +43,5 @@ for M in Ms:
     for ms, i, pl in res[:top]:
         print(f"{wl} M={M} cand {i:3d} {ms * 1e3:8.1f} us {n_cs * cfg.W * cfg.H / ms / 1e6:7.0f} Gpx/s",
               {k: pl[k] for k in ("tile_block_rows", "folds", "lanes", "chunk_rows", "stages", "key_resident",
-                                  "a_bufs", "d_bufs")})
+                                  "a_bufs", "d_bufs", "phi_stream")})
     print(f"{wl} M={M}: {len(res)} candidates; planner's rank of the best: {res[0][1]}", flush=True)

@@ -6,5 +6,5 @@ for cfg in "$@"; do
   env $cfg timeout 120 python bench.py --workload $WL --steps 30 --warmup 5 --no-e2e --no-cpu-baseline --no-autotune 2>/dev/null | python -c "
 import json,sys
 d=json.loads(sys.stdin.read().strip().splitlines()[-1])
-print('$WL $cfg', {k:(round(v['gpix_s']),round(v['frac_of_peak'],3), {q: v['plan'].get(q) for q in ('tile_block_rows','chunk_rows','key_resident','stages','a_bufs','d_bufs')}) for k,v in d['per_M'].items()})" 2>/dev/null || echo "$WL $cfg FAILED"
+print('$WL $cfg', {k:(round(v['gpix_s']),round(v['frac_of_peak'],3), {q: v['plan'].get(q) for q in ('tile_block_rows','chunk_rows','key_resident','stages','a_bufs','d_bufs','phi_stream')}) for k,v in d['per_M'].items()})" 2>/dev/null || echo "$WL $cfg FAILED"
 done
