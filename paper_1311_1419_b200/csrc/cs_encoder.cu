@@ -13,6 +13,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "cs_internal.h"
@@ -97,7 +98,7 @@ bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem
     if (phi_stream) {
         // Phi's K-slice for the chunk rides in every stage (the canonical layout keeps a chunk's
         // chunk_k / 8 K-groups contiguous); nothing of Phi stays resident
-        if (p.n_chunks < 2 || p.key_regs) return false;
+        if (p.n_chunks < 2 || p.key_regs || key_res) return false;   // KEY_STREAMED plans only
         p.phi_stream = 1;
         p.phi_slice_bytes = phi_bytes / (uint32_t)p.n_chunks;
         p.stage_phi_off = align_up(p.stage_bytes, 128);
@@ -389,7 +390,10 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.lookback = std::max(1, std::min(std::min(csenc::kMaxLag, pl.n_dbuf - 1), env_int("CSENC_LOOKBACK", 99)));
     // multi-piece strips by one 4-D TMA box (H % B == 0 so block rows never run into the next frame;
     // the box's inner extent W/4 u32 words <= 256; pieces packed back to back in the stage)
-    if (pl.pieces > 1 && !pl.single_piece && g.H % g.B == 0 && g.W % 4 == 0 && g.W / 4 <= 256 &&
+    csenc::KParamsTS kpt;
+    std::memset(&kpt, 0, sizeof(kpt));
+    static_cast<KParams&>(kpt) = kp;
+    if (!pl.key_regs && !pl.key_resident && pl.pieces > 1 && !pl.single_piece && g.H % g.B == 0 && g.W % 4 == 0 && g.W / 4 <= 256 &&
         pl.piece_bytes == (uint32_t)(pl.piece_rows * g.W) && env_int("CSENC_TMA_STRIPS", 1)) {
         PFN_encodeTiled enc = get_encode_tiled();
         if (enc) {
@@ -397,24 +401,32 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
             cuuint64_t strides[3] = {(cuuint64_t)g.W, (cuuint64_t)g.B * g.W, (cuuint64_t)g.H * g.W};
             cuuint32_t box[4] = {(cuuint32_t)(g.W / 4), (cuuint32_t)pl.chunk_rows, (cuuint32_t)pl.T_r, 1u};
             cuuint32_t estr[4] = {1, 1, 1, 1};
-            CUresult r = enc(&kp.smap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<uint8_t*>(frames), dims, strides,
+            CUresult r = enc(&kpt.smap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<uint8_t*>(frames), dims, strides,
                              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            kp.tma_strips = (r == CUDA_SUCCESS && pl.T_r <= 256) ? 1 : 0;
+            kpt.tma_strips = (r == CUDA_SUCCESS && pl.T_r <= 256) ? 1 : 0;
         }
     }
     int grid = std::max(1, std::min(e->sms, kp.n_units));
     if (q.gop_rounds) grid = std::max(1, std::min(e->sms / pl.n_tiles * pl.n_tiles, kp.n_units));
     cudaError_t err;
     const int km = pl.key_regs ? csenc::KEY_REGS : (pl.key_resident ? csenc::KEY_RESIDENT : csenc::KEY_STREAMED);
+    // KEY_STREAMED kernels take KParamsTS (with the strip tensor map), the others KParams
     auto go = [&](auto kern) {
-        if (q.gop_rounds) {   // the look-back needs every CTA resident: cooperative launch guarantees it
-            void* args[] = {&kp};
-            cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(csenc::threads_for<csenc::EPI_Q16F>()), args,
-                                        pl.smem_bytes, stream);
-        } else {
-            kern<<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(kp);
-        }
+        auto run = [&](auto& prm) {
+            if (q.gop_rounds) {   // the look-back needs every CTA resident: cooperative launch guarantees it
+                void* args[] = {&prm};
+                cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(csenc::threads_for<csenc::EPI_Q16F>()),
+                                            args, pl.smem_bytes, stream);
+            } else {
+                kern<<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(prm);
+            }
+        };
+        if constexpr (std::is_invocable_v<decltype(kern), const csenc::KParamsTS&> &&
+                      !std::is_invocable_v<decltype(kern), const csenc::KParams&>)
+            run(kpt);
+        else
+            run(kp);
     };
     int epi = q.qmode == csenc::Q_FRAME1 ? csenc::EPI_Q16F : (q.qmode ? csenc::EPI_Q16 : csenc::EPI_F32);
     if (q.qmode == csenc::Q_ROW)

@@ -31,6 +31,7 @@
 // TMEM accumulators).  Paper passages: Eq.(1) P:83-85, P:87 and Eq.(2)-(3) P:89-91.
 #pragma once
 #include <cuda.h>
+#include <type_traits>
 #include <cstdint>
 
 #include "ptx_sm100.cuh"
@@ -96,10 +97,8 @@ static_assert(kRowBarOff + 8 * kRowBufs <= kRowSlotOff, "row barriers overlap th
 static_assert(kRowSlotTileOff + kRowBufs * kRowRegRows * 4 <= 4096, "row slots overflow the staging tile");
 
 struct KParams {
-    // tma_strips != 0 (multi-piece plans, H % B == 0): the T_r pieces of a strip arrive by ONE 4-D TMA
-    // box of smap = frames as u32 words [n_seq*T][nby][B][W/4], box [1][T_r][chunk_rows][W/4] (block
-    // rows past nby zero-filled) instead of T_r bulk copies
-    alignas(64) CUtensorMap smap;
+    // tma_strips != 0 (KEY_STREAMED multi-piece plans, H % B == 0): the T_r pieces of a strip arrive by
+    // ONE 4-D TMA box of KParamsTS::smap instead of T_r bulk copies
     int tma_strips;
     // phi_stream != 0 (multi-chunk plans, KM 0/1): Phi is not resident; each stage carries the K-slice
     // of Phi its chunk needs (phi_slice_bytes at stage offset stage_phi_off, a contiguous range of the
@@ -162,6 +161,15 @@ struct KParams {
     int lookback;             // Q_FRAME1: lag in items (1 .. min(n_dbuf - 1, kMaxLag))
 };
 
+// KEY_STREAMED kernels' parameters: + the strip tensor map (frames as u32 words [n_seq*T][nby][B][W/4],
+// box [1][T_r][chunk_rows][W/4], block rows past nby zero-filled).  Only these kernels carry it:
+// a CUtensorMap in the parameters of the other kernels measurably slowed them (C4 M = 64: -2%).
+struct KParamsTS : KParams {
+    alignas(64) CUtensorMap smap;
+};
+template <int KM>
+using KParamsFor = typename std::conditional<KM == KEY_STREAMED, KParamsTS, KParams>::type;
+
 // trace events
 enum : int {
     EV_P_EMPTY = 0,   // producer: stage slot free
@@ -210,9 +218,10 @@ __device__ __forceinline__ int key_frame(const KParams& p, const Unit& w) { retu
 // mbarrier transaction count of a slot is a constant.
 template <int B>
 __device__ __forceinline__ void load_strips(const KParams& p, uint32_t dst, const uint8_t* frame, int t, int k,
-                                            uint32_t bar, uint64_t policy, int fidx = -1) {
-    if (fidx >= 0 && p.tma_strips) {   // all T_r pieces in one box (frame index fidx of `frames`)
-        ptx::tma_load_4d(dst, &p.smap, bar, 0, k * p.chunk_rows, t * p.T_r, fidx, policy);
+                                            uint32_t bar, uint64_t policy, int fidx = -1,
+                                            const CUtensorMap* smap = nullptr) {
+    if (smap != nullptr && fidx >= 0 && p.tma_strips) {   // all T_r pieces in one box (frame fidx of `frames`)
+        ptx::tma_load_4d(dst, smap, bar, 0, k * p.chunk_rows, t * p.T_r, fidx, policy);
         return;
     }
     for (int pc = 0; pc < p.pieces; ++pc) {
@@ -410,7 +419,7 @@ __device__ __forceinline__ float q16_scale(uint32_t amax_bits) {
 __device__ __forceinline__ float q16_inv(float scale) { return __frcp_rn(scale); }
 
 template <int B, int KM, int EPI>
-__global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const __grid_constant__ KParams p) {
+__global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const __grid_constant__ KParamsFor<KM> p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t sbase = (ptx::smem_addr(smem_raw) + 1023u) & ~1023u;
     const int warp = threadIdx.x >> 5;
@@ -437,7 +446,9 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
     const uint32_t s_phi = sbase + p.off_phi;
     // Phi streaming and 4-D strip boxes only exist for multi-chunk plans, which never hold the key in
     // registers: compiled out of the KEY_REGS instantiations (their code stays as small as before)
-    const bool phi_stream = KM != KEY_REGS && p.phi_stream;
+    const bool phi_stream = KM == KEY_STREAMED && p.phi_stream;
+    const CUtensorMap* smap = nullptr;
+    if constexpr (KM == KEY_STREAMED) smap = &p.smap;
     const uint32_t s_key = sbase + p.off_key;
     const uint32_t s_stage = sbase + p.off_stage;
     CS_CHECK(p.off_stage + (uint32_t)p.n_stages * p.stage_bytes <= p.smem_bytes);
@@ -567,7 +578,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                     ptx::mbar_arrive_expect_tx(bar_key_full + 8 * kb, (uint32_t)p.n_chunks * p.set_bytes);
                     for (int k = 0; k < p.n_chunks; ++k)
                         load_strips<B>(p, s_key + (uint32_t)kb * p.key_bytes + (uint32_t)k * p.stage_cs_bytes, key_f,
-                                       w.t, k, bar_key_full + 8 * kb, pol_key, keyf_idx);
+                                       w.t, k, bar_key_full + 8 * kb, pol_key);
                 }
                 __syncwarp();
                 kb ^= 1;
@@ -585,11 +596,10 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                         if (phi_stream)   // this chunk's K-slice of Phi (L2-resident)
                             ptx::bulk_load(dst + p.stage_phi_off, phi_src + (size_t)k * p.phi_slice_bytes, p.phi_slice_bytes,
                                            bar_stage_full + 8 * st);
-                        load_strips<B>(p, dst, cs_f, w.t, k, bar_stage_full + 8 * st, pol_stream,
-                                       KM == KEY_REGS ? -1 : key_idx + 1 + c);
+                        load_strips<B>(p, dst, cs_f, w.t, k, bar_stage_full + 8 * st, pol_stream, key_idx + 1 + c, smap);
                         if constexpr (KM == KEY_STREAMED)   // chained (Eq. 3 literal): reference = previous frame
                             load_strips<B>(p, dst + p.stage_cs_bytes, p.chained ? cs_f - frame_bytes : key_f, w.t, k,
-                                           bar_stage_full + 8 * st, pol_key, p.chained ? key_idx + c : keyf_idx);
+                                           bar_stage_full + 8 * st, pol_key, p.chained ? key_idx + c : keyf_idx, smap);
                     }
                     __syncwarp();
                     if (lane == 0) trace_ev(p, EV_P_ISSUED, n_items);
