@@ -118,8 +118,9 @@ int cs_encoder_plan(const cs_encoder* enc, cs_plan_info* info);
  * CS_TRACE_EVENTS * cap uint64): trace_dev[event * cap + i] = i-th occurrence of the event.
  * Events: 0 producer slot free, 1 producer TMA issued, 2 converter data landed, 3 converter A
  * buffer free, 4 converter A written, 5 MMA A ready, 6 MMA issued+committed, 7 epilogue
- * accumulator ready, 8 epilogue done, 9 converter tcgen05.st issued.  cap = 0 disables (default).  Not thread-safe with
- * concurrent encodes of the same encoder. */
+ * accumulator ready, 8 epilogue done, 9 converter tcgen05.st issued, 10 / 11 (q16 row-scale register
+ * path) epilogue row maxima published / all four warps' maxima present.  cap = 0 disables (default).
+ * Not thread-safe with concurrent encodes of the same encoder. */
 #define CS_TRACE_EVENTS 12
 int cs_encoder_set_trace(cs_encoder* enc, unsigned long long* trace_dev, int cap);
 
