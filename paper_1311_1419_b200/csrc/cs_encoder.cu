@@ -429,6 +429,7 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
             run(kp);
     };
     int epi = q.qmode == csenc::Q_FRAME1 ? csenc::EPI_Q16F : (q.qmode ? csenc::EPI_Q16 : csenc::EPI_F32);
+    if (q.qmode == csenc::Q_STOREMAX) epi = csenc::EPI_F32A;
     if (q.qmode == csenc::Q_ROW)
         epi = (pl.F != 1 || g.Mpad != g.M || pl.T_r > csenc::kRowRegRows || g.Mpad > 64) ? csenc::EPI_Q16R
               : g.Mpad <= 32 ? csenc::EPI_Q16RR : csenc::EPI_Q16RR64;
@@ -438,7 +439,8 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     case (B_ * 4 + K_) * 8 + csenc::EPI_Q16F: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16F>); break; \
     case (B_ * 4 + K_) * 8 + csenc::EPI_Q16R: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16R>); break; \
     case (B_ * 4 + K_) * 8 + csenc::EPI_Q16RR: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16RR>); break; \
-    case (B_ * 4 + K_) * 8 + csenc::EPI_Q16RR64: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16RR64>); break;
+    case (B_ * 4 + K_) * 8 + csenc::EPI_Q16RR64: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16RR64>); break; \
+    case (B_ * 4 + K_) * 8 + csenc::EPI_F32A: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_F32A>); break;
     switch ((g.B * 4 + km) * 8 + epi) {
         CSENC_CASE(8, csenc::KEY_STREAMED) CSENC_CASE(8, csenc::KEY_RESIDENT) CSENC_CASE(8, csenc::KEY_REGS)
         CSENC_CASE(16, csenc::KEY_STREAMED) CSENC_CASE(16, csenc::KEY_RESIDENT) CSENC_CASE(16, csenc::KEY_REGS)
@@ -472,6 +474,9 @@ cudaError_t set_smem_attr_all(int bytes) {
     if (r != cudaSuccess) e = r;                                                                          \
     r = cudaFuncSetAttribute(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16RR64>,                       \
                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);                         \
+    if (r != cudaSuccess) e = r;                                                                          \
+    r = cudaFuncSetAttribute(csenc::cs_measure_kernel<B_, K_, csenc::EPI_F32A>,                          \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);                         \
     if (r != cudaSuccess) e = r;
     CSENC_ATTR(8, csenc::KEY_STREAMED) CSENC_ATTR(8, csenc::KEY_RESIDENT) CSENC_ATTR(8, csenc::KEY_REGS)
     CSENC_ATTR(16, csenc::KEY_STREAMED) CSENC_ATTR(16, csenc::KEY_RESIDENT) CSENC_ATTR(16, csenc::KEY_REGS)
@@ -498,6 +503,50 @@ std::vector<uint16_t> arrange_phi(const Geometry& g, uint32_t lbo, uint32_t sbo,
             arranged[byte / 2] = phi_fp16[(size_t)n * g.N + j];
         }
     return arranged;
+}
+
+}  // namespace
+
+cudaError_t csenc::host::scratch_alloc(cs_encoder* e, void** ptr, size_t bytes, cudaStream_t st) {
+    {
+        std::lock_guard<std::mutex> lk(e->pool_mu);
+        if (!e->pool) {
+            cudaMemPoolProps props;
+            std::memset(&props, 0, sizeof(props));
+            props.allocType = cudaMemAllocationTypePinned;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = e->device;
+            cudaError_t err = cudaMemPoolCreate(&e->pool, &props);
+            if (err != cudaSuccess) {
+                e->pool = nullptr;
+                return err;
+            }
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(e->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    }
+    return cudaMallocFromPoolAsync(ptr, bytes, e->pool, st);
+}
+
+namespace {
+
+// f1, per-frame scale from stored y (8 M < N): codes = rint(y * inv), inv = 1 / (amax / 32767) of the
+// frame -- the same expressions as the K1 epilogue (q16_bits / q16_scale / q16_inv), so the codes are
+// bitwise those of the two-pass path.  8 measurements per thread and step (two 16-B loads, one 16-B
+// store); per_frame (= nblk * M) is a multiple of 8.
+__global__ void q16_requant_kernel(const float4* __restrict__ y, const uint32_t* __restrict__ amax,
+                                   uint4* __restrict__ codes, long long n8, long long per8) {
+    const long long step = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += step) {
+        const float inv = csenc::q16_inv(csenc::q16_scale(__ldg(amax + i / per8)));
+        const float4 a = y[2 * i], b = y[2 * i + 1];
+        uint4 w;
+        w.x = csenc::q16_pack(__float_as_uint(a.x), __float_as_uint(a.y), inv);
+        w.y = csenc::q16_pack(__float_as_uint(a.z), __float_as_uint(a.w), inv);
+        w.z = csenc::q16_pack(__float_as_uint(b.x), __float_as_uint(b.y), inv);
+        w.w = csenc::q16_pack(__float_as_uint(b.z), __float_as_uint(b.w), inv);
+        codes[i] = w;
+    }
 }
 
 // f1, per-frame scale: amax bits (pass 1) -> fp32 scales in place, after pass 2 has read them.
@@ -630,6 +679,7 @@ int cs_encoder_destroy(cs_encoder* e) {
     for (auto& s : e->hs)
         if (s) cudaStreamDestroy(s);
     for (auto& ev : e->hev) cudaEventDestroy(ev);
+    if (e->pool) cudaMemPoolDestroy(e->pool);
     delete e;
     return CS_OK;
 }
@@ -863,7 +913,7 @@ int cs_encode_batch_q16(cs_encoder* e, const uint8_t* frames, int n_seq, int T, 
         // per-frame scale in ONE pass: frame-major units, decoupled look-back on per-frame maxima
         // (workspace: |y| maxima and arrival counters, stream-ordered, zeroed)
         uint32_t* ws = nullptr;
-        cudaError_t err = cudaMallocAsync((void**)&ws, (size_t)n_cs * 8, st);
+        cudaError_t err = scratch_alloc(e, (void**)&ws, (size_t)n_cs * 8, st);
         if (err != cudaSuccess) return fail(CS_ERR_OOM, std::string("q16 workspace: ") + cudaGetErrorString(err));
         err = cudaMemsetAsync(ws, 0, (size_t)n_cs * 8, st);
         int rc = err == cudaSuccess ? CS_OK : cuda_fail(err, "cudaMemsetAsync");
@@ -879,11 +929,39 @@ int cs_encode_batch_q16(cs_encoder* e, const uint8_t* frames, int n_seq, int T, 
         cudaFreeAsync(ws, st);
         return rc;
     }
-    // per-frame scale in two passes: zero the |y| maxima, absmax pass, codes pass,
-    // finalize
+    // per-frame scale: zero the |y| maxima, then either
+    //  (a) 8 M < N: one measurement pass storing fp32 y in a stream-ordered workspace + the maxima,
+    //      and a re-quantisation pass over y (8 B per measurement moved instead of re-reading the
+    //      frames, N / M B per measurement), or
+    //  (b) an absmax pass and a codes pass, both measuring (no y round trip);
+    // then finalize (maxima -> scales in place).
     q.amax = reinterpret_cast<uint32_t*>(scales);
     cudaError_t err = cudaMemsetAsync(scales, 0, (size_t)n_cs * sizeof(float), st);
     if (err != cudaSuccess) return cuda_fail(err, "cudaMemsetAsync");
+    const long long per_frame = (long long)g.nblk * g.M;
+    if (8 * g.M < g.N && per_frame % 8 == 0 && env_int("CSENC_Q16_STORE", 1)) {
+        float* ybuf = nullptr;
+        err = scratch_alloc(e, (void**)&ybuf, (size_t)(n_cs * per_frame) * sizeof(float), st);
+        if (err == cudaSuccess) {
+            q.qmode = csenc::Q_STOREMAX;
+            int rc = launch(e, frames, n_seq, T, 0, n_gops, ybuf, st, q);
+            if (rc == CS_OK) {
+                const long long n8 = n_cs * per_frame / 8;
+                const unsigned blocks = (unsigned)std::min<long long>((n8 + 255) / 256, (long long)e->sms * 16);
+                q16_requant_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(ybuf), q.amax,
+                                                          reinterpret_cast<uint4*>(codes), n8, per_frame / 8);
+                err = cudaGetLastError();
+                if (err == cudaSuccess) {
+                    q16_finalize_kernel<<<(unsigned)((n_cs + 255) / 256), 256, 0, st>>>(q.amax, n_cs);
+                    err = cudaGetLastError();
+                }
+                rc = err == cudaSuccess ? CS_OK : cuda_fail(err, "re-quantisation launch");
+            }
+            cudaFreeAsync(ybuf, st);
+            return rc;
+        }
+        cudaGetLastError();   // no workspace: fall back to measuring twice
+    }
     q.qmode = csenc::Q_ABSMAX;
     int rc = launch(e, frames, n_seq, T, 0, n_gops, nullptr, st, q);
     if (rc != CS_OK) return rc;

@@ -90,6 +90,11 @@ struct cs_encoder {
     unsigned long long* trace = nullptr;  // device buffer (debug timeline), caller-owned
     int trace_cap = 0;
     std::vector<cudaEvent_t> hev;
+    // stream-ordered scratch (q16 workspaces): the encoder's own memory pool, created on first use,
+    // that keeps its memory between calls (release threshold = max) so repeated calls do not map
+    // and unmap device memory
+    cudaMemPool_t pool = nullptr;
+    std::mutex pool_mu;
     // f3 adjoint (K3): Phi^T chunks (tf32, no-swizzle K-major), plan; phiT_dev == nullptr when M % 4 != 0
     void* phiT_dev = nullptr;
     int adj_Kc = 0, adj_n_kc = 0, adj_Nc = 0, adj_n_nc = 0, adj_stages = 0;
@@ -102,6 +107,8 @@ namespace csenc {
 namespace host {
 // f3 (cs_adjoint.cu): Phi^T chunks and plan at create; per-kernel SMEM attribute
 int prepare_adjoint(cs_encoder* e, const uint16_t* phi_fp16);
+// stream-ordered scratch from the encoder's pool (created on first use); free with cudaFreeAsync
+cudaError_t scratch_alloc(cs_encoder* e, void** ptr, size_t bytes, cudaStream_t st);
 cudaError_t adjoint_set_smem_attr(int bytes);
 }  // namespace host
 }  // namespace csenc

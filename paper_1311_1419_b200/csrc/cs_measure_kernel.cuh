@@ -68,6 +68,9 @@ enum Epilogue : int {
     EPI_Q16R = 3,   // Q_ROW, general (two TMEM passes, named barrier)
     EPI_Q16RR = 4,  // Q_ROW, register path: one fold, M = 16 or 32, <= kRowRegRows block rows
     EPI_Q16RR64 = 5,  // the same for M = 48 or 64
+    EPI_F32A = 6,   // fp32 measurements + per-CS-frame |y| maximum (atomicMax into amax): the first
+                    // pass of the per-frame scale when storing y and re-quantising it is cheaper than
+                    // measuring twice (8 M < N)
 };
 // EPI_Q16 sub-modes (KParams::qmode)
 enum QMode : int {
@@ -75,6 +78,7 @@ enum QMode : int {
     Q_FRAME = 2,      // pass 2: codes with scale = amax[cs] / 32767 (1 if 0)
     Q_ROW = 3,        // single pass: one scale per (CS frame, block row), reduced in SMEM
     Q_FRAME1 = 4,     // single pass, per-frame scale: decoupled look-back over GOP-aligned rounds
+    Q_STOREMAX = 5,   // EPI_F32A: fp32 y to a workspace + atomicMax of |y| bits into amax[cs]
 };
 constexpr int kMaxLag = 7;                       // Q_FRAME1: items held in TMEM before quantising (<= ring-1);
                                                  // kMaxLag + 1 must be a power of two (pending ring)
@@ -892,7 +896,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                 if (kb == 0) kph ^= 1u;
             }
         }
-    } else if (EPI != EPI_F32 && warp >= kEpiWarp0 && warp < kEpiWarp0 + 4 && !dbg_load_only) {
+    } else if (EPI != EPI_F32 && EPI != EPI_F32A && warp >= kEpiWarp0 && warp < kEpiWarp0 + 4 && !dbg_load_only) {
         // ================================================================ epilogue, 16-bit codes (f1)
         // Per item: (Q_ABSMAX) warp max of |y| -> one atomicMax per warp into amax[cs];
         // (Q_FRAME) codes with the frame's scale; (Q_ROW) pass A: per-block-row max reduced across
@@ -1319,7 +1323,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                 }
             }
         }
-    } else if (EPI == EPI_F32 && warp >= kEpiWarp0 && warp < kEpiWarp0 + 4 && !dbg_load_only) {
+    } else if ((EPI == EPI_F32 || EPI == EPI_F32A) && warp >= kEpiWarp0 && warp < kEpiWarp0 + 4 && !dbg_load_only) {
         // ================================================================ epilogue (a6)
         // Output rows (blocks) are M*4 bytes apart.  For M == 4 a thread's row is one 16-byte
         // vector and the warp's 32 rows are contiguous: store straight from registers.  For other
@@ -1351,6 +1355,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                 const uint32_t d_tm = tmem_base + lane_bits + d_col0 + (uint32_t)db * (uint32_t)p.d_cols;
                 CS_CHECK(d_col0 + (uint32_t)(db + 1) * (uint32_t)p.d_cols <= kTmemCols);
                 CS_CHECK((cs_global + 1) * p.nblk * (long long)p.M <= p.out_floats);
+                float amx = 0.0f;   // EPI_F32A: |y| maximum of this lane's blocks
                 for (int f = 0; f < p.F; ++f) {
                     const int row0 = f * p.L + ew * p.Lq;            // tile block of this warp's lane 0
                     const int b = row0 + (int)lane;
@@ -1361,6 +1366,10 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                         ptx::tmem_ld_32x32b_x16(d_tm + (uint32_t)(f * p.Mpad), v);
                         ptx::tc_wait_ld();
                         if (valid && !skip) ptx::stg128(out_cs + (long long)b * 4, v[0], v[1], v[2], v[3]);
+                        if constexpr (EPI == EPI_F32A)
+                            if (valid)
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) amx = fmaxf(amx, fabsf(__uint_as_float(v[q])));
                         continue;
                     }
                     for (int j0 = 0; j0 < p.Mpad; j0 += 32) {
@@ -1373,6 +1382,11 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                                                     *reinterpret_cast<uint32_t(*)[16]>(v));
                         }
                         ptx::tc_wait_ld();
+                        if constexpr (EPI == EPI_F32A)   // padded columns (j0 + q >= M) hold 0: Phi's pad rows are 0
+                            if (valid)
+#pragma unroll
+                                for (int q = 0; q < 32; ++q)
+                                    if (q < cw) amx = fmaxf(amx, fabsf(__uint_as_float(v[q])));
                         if (mode == 2) {
                             if (valid) {
                                 float* dst = out_cs + (long long)b * p.M + j0;
@@ -1388,6 +1402,10 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                         else
                             stage_store<16>(v, stage_tile, lane, dst_row0, p.M, j0, rows_valid, skip);
                     }
+                }
+                if constexpr (EPI == EPI_F32A) {
+                    const uint32_t mx = __reduce_max_sync(0xFFFFFFFFu, __float_as_uint(amx));
+                    if (lane == 0 && mx != 0) atomicMax(p.amax + cs_global, mx);
                 }
                 ptx::tc_fence_before();
                 __syncwarp();

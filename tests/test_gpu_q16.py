@@ -254,3 +254,24 @@ def test_q16_frame_single_pass_equals_two_pass(name):
         assert torch.equal(c1, c2) and torch.equal(s1, s2)
         y, S = oracle.encode(frames, phi, cfg.G, cfg.B)
         check_q16(c1.cpu().numpy(), s1.cpu().numpy(), y, S, enc.nby, enc.nbx, P.Encoder.Q16_FRAME)
+
+
+@pytest.mark.parametrize("name,M", [("C4", 16), ("C5", 4), ("C3", 64)])
+def test_q16_frame_store_path_equals_two_pass(name, M, monkeypatch):
+    """CS_Q16_FRAME with 8 M < N stores y and re-quantises it; the two-pass path (CSENC_Q16_STORE=0)
+    measures twice.  Same codes and scales, bit for bit."""
+    base = synth.CONFIGS[name]
+    cfg = base.with_(T=min(base.T, 2 * base.G + 3), S=min(base.S, 2))
+    frames = synth.gen_video(cfg)
+    fd = torch.from_numpy(frames).cuda()
+    phi = synth.phi_from_seed(synth.phi_seed(), M, cfg.B ** 2)
+    enc = P.Encoder(cfg.W, cfg.H, cfg.G, cfg.B, M, phi)
+    assert 8 * M < cfg.B ** 2
+    monkeypatch.setenv("CSENC_Q16_STORE", "1")
+    c1, s1 = run_q16(enc, fd, P.Encoder.Q16_FRAME)
+    monkeypatch.setenv("CSENC_Q16_STORE", "0")
+    c0, s0 = run_q16(enc, fd, P.Encoder.Q16_FRAME)
+    torch.cuda.synchronize()
+    assert torch.equal(c0, c1) and torch.equal(s0, s1)
+    y, S = oracle.encode(frames, phi, cfg.G, cfg.B)
+    check_q16(c1.cpu().numpy(), s1.cpu().numpy(), y, S, enc.nby, enc.nbx, P.Encoder.Q16_FRAME)
