@@ -151,8 +151,8 @@ int cs_encode_batch_gops(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, 
  * scale) (IEEE fp32 division, round half to even, clamped to +-32767); dequantize = codes *
  * scale.  Container payload per CS frame: f32 scale + M*nblk int16 codes.
  *   CS_Q16_FRAME: one scale per CS frame, exactly as SPEC states.  The frame maximum is a
- *     grid-wide dependency.  When 8*M < B*B (storing fp32 y and reading it back moves fewer bytes
- *     than reading the frames again) one measurement pass writes y to a stream-ordered workspace
+ *     grid-wide dependency.  When 8*M <= B*B (storing fp32 y and reading it back moves no more
+ *     bytes than reading the frames again) one measurement pass writes y to a stream-ordered workspace
  *     (cudaMallocAsync / cudaFreeAsync on `stream`, n_cs*nblk*M floats) together with the frame
  *     maxima and a re-quantisation kernel makes the codes; otherwise the measurement runs twice: an
  *     absmax pass (no stores, one atomicMax per warp and frame) and a codes pass.  Then a tiny

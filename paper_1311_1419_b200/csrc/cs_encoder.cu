@@ -939,7 +939,7 @@ int cs_encode_batch_q16(cs_encoder* e, const uint8_t* frames, int n_seq, int T, 
     cudaError_t err = cudaMemsetAsync(scales, 0, (size_t)n_cs * sizeof(float), st);
     if (err != cudaSuccess) return cuda_fail(err, "cudaMemsetAsync");
     const long long per_frame = (long long)g.nblk * g.M;
-    if (8 * g.M < g.N && per_frame % 8 == 0 && env_int("CSENC_Q16_STORE", 1)) {
+    if (8 * g.M <= g.N && per_frame % 8 == 0 && env_int("CSENC_Q16_STORE", 1)) {
         float* ybuf = nullptr;
         err = scratch_alloc(e, (void**)&ybuf, (size_t)(n_cs * per_frame) * sizeof(float), st);
         if (err == cudaSuccess) {

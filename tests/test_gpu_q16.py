@@ -256,9 +256,9 @@ def test_q16_frame_single_pass_equals_two_pass(name):
         check_q16(c1.cpu().numpy(), s1.cpu().numpy(), y, S, enc.nby, enc.nbx, P.Encoder.Q16_FRAME)
 
 
-@pytest.mark.parametrize("name,M", [("C4", 16), ("C5", 4), ("C3", 64)])
+@pytest.mark.parametrize("name,M", [("C4", 16), ("C4", 32), ("C5", 4), ("C3", 64)])
 def test_q16_frame_store_path_equals_two_pass(name, M, monkeypatch):
-    """CS_Q16_FRAME with 8 M < N stores y and re-quantises it; the two-pass path (CSENC_Q16_STORE=0)
+    """CS_Q16_FRAME with 8 M <= N stores y and re-quantises it; the two-pass path (CSENC_Q16_STORE=0)
     measures twice.  Same codes and scales, bit for bit."""
     base = synth.CONFIGS[name]
     cfg = base.with_(T=min(base.T, 2 * base.G + 3), S=min(base.S, 2))
@@ -266,7 +266,7 @@ def test_q16_frame_store_path_equals_two_pass(name, M, monkeypatch):
     fd = torch.from_numpy(frames).cuda()
     phi = synth.phi_from_seed(synth.phi_seed(), M, cfg.B ** 2)
     enc = P.Encoder(cfg.W, cfg.H, cfg.G, cfg.B, M, phi)
-    assert 8 * M < cfg.B ** 2
+    assert 8 * M <= cfg.B ** 2
     monkeypatch.setenv("CSENC_Q16_STORE", "1")
     c1, s1 = run_q16(enc, fd, P.Encoder.Q16_FRAME)
     monkeypatch.setenv("CSENC_Q16_STORE", "0")
