@@ -153,7 +153,8 @@ int cs_encode_batch_gops(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, 
  *   CS_Q16_FRAME: one scale per CS frame, exactly as SPEC states.  The frame maximum is a
  *     grid-wide dependency.  When 8*M <= B*B (storing fp32 y and reading it back moves no more
  *     bytes than reading the frames again) one measurement pass writes y to a stream-ordered workspace
- *     (cudaMallocAsync / cudaFreeAsync on `stream`, n_cs*nblk*M floats) together with the frame
+ *     (stream-ordered, from the encoder's own memory pool, n_cs*nblk*M floats;
+ *     the pool keeps its memory for later calls until cs_encoder_destroy) together with the frame
  *     maxima and a re-quantisation kernel makes the codes; otherwise the measurement runs twice: an
  *     absmax pass (no stores, one atomicMax per warp and frame) and a codes pass.  Then a tiny
  *     finalize kernel (memset + 3 launches either way).  Both give the same codes, bit for bit.
