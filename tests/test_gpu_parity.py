@@ -189,6 +189,9 @@ def test_real_subnormals_in_phi_parity():
     (2048, 8, 8, 64, 2, 3),       # 256 blocks per row -> folds
     (128, 200, 16, 48, 5, 12),    # several tile rows, short last GOP
     (64, 64, 32, 80, 2, 4),       # largest B=32 M
+    (64, 48, 16, 256, 3, 5),      # M = N = 256: the largest M (UMMA N limit), lossless mode
+    (16, 300, 8, 4, 4, 9),        # one block column, tall frame, many tile rows
+    (640, 96, 32, 64, 4, 9),      # C3-like rows with H % B == 0: 4-D strip boxes / Phi streaming plans
 ])
 def test_edge_shapes(W, H, B, M, G, T):
     rng = np.random.default_rng(W * 7 + H)
