@@ -20,3 +20,4 @@ run_op q16frame cs_measure 24 2 --output q16frame
 run_op adjoint cs_adjoint 12 4 --op adjoint
 run_op closed_loop key_codec 4 1 --op closed_loop
 run_op frame frame_measure 3 1 --op frame
+run_op adjoint_c5 cs_adjoint 3 1 --op adjoint --workload C5
