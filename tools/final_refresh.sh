@@ -13,9 +13,9 @@ run C1 --workload C1
 run C2 --workload C2
 run C3 --workload C3
 run C5 --workload C5
-run C4_q16row --output q16row --tune-file $OUT/plans.json
-run C4_q16frame --output q16frame --tune-file $OUT/plans.json
-run C4_q16frame1 --output q16frame1 --tune-file $OUT/plans.json
+run C4_q16row --output q16row
+run C4_q16frame --output q16frame
+run C4_q16frame1 --output q16frame1
 run C4_adjoint --op adjoint
 run C5_adjoint --op adjoint --workload C5
 run C4_closed_loop --op closed_loop --tune-file $OUT/plans.json
@@ -27,3 +27,4 @@ timeout 300 $CMD > $OUT/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launch.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:cs_measure -s 12 -c 4 -o $OUT/prof $CMD > $OUT/ncu_full.log 2>&1
 echo "ncu rc=$?" >> $OUT/ncu_full.log
+[ "${NEXT:-0}" = "1" ] && ONLY="q16row q16frame" bash tools/prof_next.sh $TAG-next
