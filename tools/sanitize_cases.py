@@ -38,6 +38,14 @@ for W, H, T, G, B, M in cases:
         out = enc.encode_batch(fd)
         torch.cuda.synchronize()
         report(f"{tag} plan {i} key {enc.plan()['key_resident']}", oracle.check_tolerance(out.cpu().numpy(), y, S)[0])
+    # Phi-streaming plans (and with them the 4-D strip boxes when H % B == 0): the first two
+    streaming = [i for i in range(enc.num_candidates()) if enc.set_candidate(i)["phi_stream"]][:2]
+    for i in streaming:
+        enc.set_candidate(i)
+        out = enc.encode_batch(fd)
+        torch.cuda.synchronize()
+        report(f"{tag} phi-stream plan {i}", oracle.check_tolerance(out.cpu().numpy(), y, S)[0])
+    enc.set_candidate(0)
     enc.set_candidate(0)
     # f1: q16 modes (codes within +-1 of the oracle's quantisation of the exact y)
     oc, _ = oracle.quantize_frames(y)
