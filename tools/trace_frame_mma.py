@@ -1,3 +1,5 @@
+"""MMA-warp wait breakdown of the frame-level GEMM (needs a build whose trace events 0/1 are recorded
+after the A-tile and residual-operand waits in the MMA loop; see DESIGN.md sec.7 f2)."""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch, synth, paper_1311_1419_b200 as P
