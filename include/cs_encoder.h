@@ -122,6 +122,9 @@ int cs_encoder_plan(const cs_encoder* enc, cs_plan_info* info);
  * path) epilogue row maxima published / all four warps' maxima present.  cap = 0 disables (default).
  * Not thread-safe with concurrent encodes of the same encoder. */
 #define CS_TRACE_EVENTS 12
+/* Profiling ranges: with CSENC_NVTX=1 in the environment (read once per process), every encode /
+ * adjoint / key-codec / frame-encode entry point opens an NVTX range named after itself (ncu --nvtx,
+ * nsys); header-only nvtx3, a no-op when no tool is attached. */
 int cs_encoder_set_trace(cs_encoder* enc, unsigned long long* trace_dev, int cap);
 
 /* ---- encode (device buffers; asynchronous) ---------------------------------------------- */

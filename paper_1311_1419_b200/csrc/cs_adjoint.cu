@@ -132,6 +132,7 @@ using namespace csenc::host;
 extern "C" {
 
 int cs_adjoint(cs_encoder* e, const float* meas, int64_t n_frames, float* x, cs_stream_t stream) {
+    csenc::host::NvtxScope nvtx_scope("cs_adjoint");
     if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
     if (n_frames < 0) return fail(CS_ERR_ARG, "n_frames must be >= 0");
     if (n_frames == 0) return CS_OK;

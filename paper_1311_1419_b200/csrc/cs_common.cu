@@ -31,6 +31,11 @@ float half_bits_to_float(uint16_t h) {
     return s ? -v : v;
 }
 
+bool nvtx_enabled() {
+    static const bool on = env_int("CSENC_NVTX", 0) != 0;
+    return on;
+}
+
 int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
     return v ? std::atoi(v) : dflt;

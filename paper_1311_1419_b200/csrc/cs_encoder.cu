@@ -809,12 +809,14 @@ int cs_encode_batch_gops(cs_encoder* e, const uint8_t* frames, int n_seq, int T,
 }
 
 int cs_encode_batch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, float* out, cs_stream_t stream) {
+    csenc::host::NvtxScope nvtx_scope("cs_encode_batch");
     if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
     if (T < 0) return fail(CS_ERR_ARG, "T must be >= 0");
     return cs_encode_batch_gops(e, frames, n_seq, T, 0, cdiv(T, e->geo.G), out, stream);
 }
 
 int cs_encode_gop(cs_encoder* e, const uint8_t* frames, int n_frames, float* out, cs_stream_t stream) {
+    csenc::host::NvtxScope nvtx_scope("cs_encode_gop");
     if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
     if (n_frames < 1 || n_frames > e->geo.G) return fail(CS_ERR_ARG, "n_frames must be in [1, gop]");
     return cs_encode_batch_gops(e, frames, 1, n_frames, 0, 1, out, stream);
@@ -885,6 +887,7 @@ int64_t cs_q16_scale_count(const cs_encoder* e, int n_seq, int T, int granularit
 
 int cs_encode_batch_q16(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int granularity, int16_t* codes,
                         float* scales, cs_stream_t stream) {
+    csenc::host::NvtxScope nvtx_scope("cs_encode_batch_q16");
     if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
     if (n_seq < 0 || T < 0) return fail(CS_ERR_ARG, "n_seq and T must be >= 0");
     if (granularity != CS_Q16_FRAME && granularity != CS_Q16_ROW && granularity != CS_Q16_FRAME_1PASS)
@@ -1099,6 +1102,7 @@ int cs_encode_batch_host_multi(cs_encoder* const* encs, int n_enc, const uint8_t
 }
 
 int cs_encode_batch_host(cs_encoder* e, const uint8_t* frames_host, int n_seq, int T, float* out_host) {
+    csenc::host::NvtxScope nvtx_scope("cs_encode_batch_host");
     return cs_encode_batch_host_multi(&e, 1, frames_host, n_seq, T, &out_host);
 }
 

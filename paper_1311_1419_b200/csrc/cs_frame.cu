@@ -251,6 +251,7 @@ int encode_2sm(cs_frame_encoder* f, const uint8_t* frames, int n_seq, int T, flo
 extern "C" {
 
 int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq, int T, float* y, cs_stream_t stream) {
+    csenc::host::NvtxScope nvtx_scope("cs_frame_encode_batch");
     if (!f) return fail(CS_ERR_ARG, "encoder is NULL");
     if (n_seq < 0 || T < 0) return fail(CS_ERR_ARG, "n_seq and T must be >= 0");
     const long long cs_s = cs_frames_per_stream(T, f->G);

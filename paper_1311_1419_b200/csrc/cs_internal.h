@@ -5,6 +5,7 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdint>
@@ -26,6 +27,19 @@ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 float half_bits_to_float(uint16_t h);
 int env_int(const char* name, int dflt);   // tuning / debug knobs (CSENC_*)
+
+// NVTX range around an ABI call (profiling: ncu --nvtx / nsys), when CSENC_NVTX=1 (read once);
+// nvtx3 is header-only: no extra link dependency, a no-op without an attached tool
+bool nvtx_enabled();
+struct NvtxScope {
+    bool on;
+    explicit NvtxScope(const char* name) : on(nvtx_enabled()) {
+        if (on) nvtxRangePushA(name);
+    }
+    ~NvtxScope() {
+        if (on) nvtxRangePop();
+    }
+};
 
 // GOP accounting (a1)
 inline long long cs_frames_per_stream(int T, int G) { return (long long)T - cdiv(T, G); }

@@ -34,6 +34,7 @@ int64_t cs_key_coef_count(const cs_encoder* e, int n_seq, int T) {
 
 int cs_key_codec(cs_encoder* e, const uint8_t* frames, int n_seq, int T, const int32_t* qsteps, int16_t* coef,
                  uint8_t* keys, cs_stream_t stream) {
+    csenc::host::NvtxScope nvtx_scope("cs_key_codec");
     if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
     if (n_seq < 0 || T < 0) return fail(CS_ERR_ARG, "n_seq and T must be >= 0");
     if (n_seq == 0 || T == 0) return CS_OK;
