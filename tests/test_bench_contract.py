@@ -56,3 +56,14 @@ def test_device_arm_contract():
     assert d["gpu_launches"] == 3 * 4
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("args,bound", [(("--op", "adjoint"), "hbm"), (("--op", "closed_loop"), "hbm"),
+                                        (("--output", "q16row"), "hbm"), (("--op", "frame"), "tensor")])
+def test_device_arm_variants(args, bound):
+    d = run_bench(*args, "--steps", "1", "--warmup", "3", "--no-e2e", "--no-cpu-baseline", "--tune-candidates", "2")
+    for k in BASE_KEYS:
+        assert k in d, k
+    r = d["roofline"]
+    assert r["bound"] == bound and 0 < r["frac"] < 1.5 and d["gpu_launches"] > 0

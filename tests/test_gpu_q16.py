@@ -103,6 +103,9 @@ CASES = [
     ("b16_m32", 400, 150, 4, 2, 16, 32),
     ("b16_m48", 176, 60, 4, 3, 16, 48),
     ("b8_m16", 128, 56, 5, 3, 8, 16),
+    # per-frame store path not applicable (nblk * M not a multiple of 8): two passes
+    ("b8_m3", 48, 40, 5, 4, 8, 3),
+    ("b8_m5", 48, 24, 5, 4, 8, 5),
 ]
 
 
