@@ -237,7 +237,10 @@ def run_ours(args, cfg, Ms):
             best, best_ms = 0, float("inf")
             for k in range(min(args.tune_candidates, e.num_candidates())):
                 e.set_candidate(k)
-                e.encode_batch_q16(frames, gran, qouts[i][0], qouts[i][1], stream)   # warm-up
+                try:
+                    e.encode_batch_q16(frames, gran, qouts[i][0], qouts[i][1], stream)   # warm-up
+                except P.CSError:   # e.g. row scales need <= 40 block rows per tile: skip this plan
+                    continue
                 t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 t0.record(stream)
                 for _ in range(2):
