@@ -151,8 +151,10 @@ int cs_encode_batch_gops(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, 
 /* ---- 16-bit measurement quantisation ---------------------------- */
 
 /* SPEC.md:154-162 quantize: scale = max|y_i| / 32767 (1 if all y_i == 0), codes = round(y_i /
- * scale) (IEEE fp32 division, round half to even, clamped to +-32767); dequantize = codes *
- * scale.  Container payload per CS frame: f32 scale + M*nblk int16 codes.
+ * scale), round half to even, clamped to +-32767; dequantize = codes * scale.  The kernel takes
+ * the decision in fp32 on its own fp32 y: scale = fl32(amax / 32767), inv = fl32(1 / scale), code =
+ * round-half-even of the fp32 FFMA y * inv (R18), so a code can differ by one from the
+ * exact round(y / scale) only where y / scale lies within ~32767 * 2^-23 of a half-integer.  Container payload per CS frame: f32 scale + M*nblk int16 codes.
  *   CS_Q16_FRAME: one scale per CS frame, exactly as SPEC states.  The frame maximum is a
  *     grid-wide dependency.  When 8*M <= B*B (storing fp32 y and reading it back moves no more
  *     bytes than reading the frames again) one measurement pass writes y to a stream-ordered workspace

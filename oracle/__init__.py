@@ -30,8 +30,8 @@ Paper passages followed (PAPER.md line numbers, section):
   a6 output layout   -- y[s][g][c][by][bx][m], block-major (BASELINE.json:5 item 4)
   a7 CR accounting   -- "original bits / (key bits + measurement bits)"
                         (BASELINE.json:5); Table I closed form P:113-126
-  f1 quantisation    -- SPEC.md:154-162 (scale = max|y|/32767, codes = round(y/scale)),
-                        f32 scale SPEC.md:410; decision precision DESIGN.md R17-R18
+  f1 quantisation    -- SPEC.md:154-162 (scale = max|y|/32767, codes = round(y/scale)) on the
+                        exact y, f32 scale SPEC.md:410, ties to even (R17-R18)
   f2 frame-level A   -- Eq.(1) P:83-85 with one dense A in R^{m x n}, n = W*H
   f3 adjoint         -- SPEC.md:145-153 (A^T v), TVAL3 start point x = A^T y SPEC.md:235;
                         per block x_b = Phi^T y_b reassembled into the frame (inverse of a2)
@@ -179,11 +179,13 @@ def measure_entries(frames: np.ndarray, phi_bits: np.ndarray, G: int, B: int, cs
 def quantize(y, bits: int = 16):
     """SPEC.md:154-162 quantize: scale = max|y_i| / 32767 (scale = 1 if y is all zero),
     codes = round(y_i / scale), dequantize = codes * scale.  The container stores the scale as f32
-    (SPEC.md:410), so scale is rounded to fp32; round = round half to even (SPEC leaves the tie rule
-    open -- DESIGN.md reading R17).  The rounding decision is taken in the kernel's precision
-    (R18): y rounded to fp32, divided by the scale as a multiplication with the fp32
-    reciprocal inv = fl32(1 / scale), the exact product rounded half-to-even (an fp32 x fp32 product
-    is exact in fp64, so np.rint of it is that rounding).  Returns (int16 codes, float32 scale)."""
+    (SPEC.md:410), so scale is rounded to fp32 (R17); round = round half to even (SPEC
+    leaves the tie rule open, R17).  y is the exact measurement (fp64, as encode() returns it) and
+    the rounding of y / scale is decided EXACTLY (R18): q0 = rint of the fp64 quotient, then the
+    exact remainder d = y - q0 * scale (q0 * scale has <= 16 + 24 significant bits and d is a
+    multiple of min(ulp(y), ulp(scale)) below scale in magnitude, so both are exact in fp64) moves q0
+    by one where the quotient's rounding crossed a half-integer, and an exact tie (|d| = scale/2)
+    goes to the even neighbour.  Returns (int16 codes, float32 scale)."""
     if bits != 16:
         raise ValueError("16-bit quantisation only")
     y = np.asarray(y, dtype=np.float64)
@@ -192,8 +194,13 @@ def quantize(y, bits: int = 16):
     qmax = (1 << (bits - 1)) - 1
     amax = float(np.max(np.abs(y))) if y.size else 0.0
     scale = np.float32(amax / qmax) if amax > 0 else np.float32(1.0)
-    inv = np.float32(1.0) / scale                       # fp32 IEEE division
-    q = np.rint(y.astype(np.float32).astype(np.float64) * float(inv))
+    s = float(scale)
+    q = np.rint(y / s)
+    d = y - q * s                                        # exact remainder of y / scale at q
+    q = np.where(d > 0.5 * s, q + 1, np.where(d < -0.5 * s, q - 1, q))
+    d = y - q * s
+    tie = np.abs(d) == 0.5 * s
+    q = np.where(tie & (np.mod(q, 2) != 0), q + np.sign(d), q)   # half to even
     codes = np.clip(q, -qmax, qmax).astype(np.int16)
     return codes, scale
 

@@ -31,6 +31,16 @@ REL = 1e-5
 QMAX = 32767
 
 
+def kernel_fp32_decision(y, scale):
+    """EMULATION of the kernel's rounding decision (R18), kept here in the test, not in
+    the oracle: code = round-half-even of fl32(y) * fl32(1 / scale) (one FFMA against 1.5 * 2^23 in
+    the kernel; an fp32 x fp32 product is exact in fp64, so np.rint of it is that rounding).  Used
+    only to check the kernel bitwise against ITS OWN fp32 output; against the exact oracle the tie
+    band of check_group applies."""
+    inv = (np.float32(1.0) / np.asarray(scale, dtype=np.float32)).astype(np.float64)
+    return np.clip(np.rint(np.asarray(y, dtype=np.float32).astype(np.float64) * inv), -QMAX, QMAX).astype(np.int16)
+
+
 def check_group(codes, scale, y, S):
     """codes int [n], scale float32, exact y / S fp64 [n] of one scale group."""
     codes = np.asarray(codes, dtype=np.int64)
@@ -80,10 +90,9 @@ def fp32_consistency(enc, fd, codes_f, scales_f, codes_r, scales_r):
     torch.cuda.synchronize()
     y32 = y32.cpu().numpy().astype(np.float64)
     sf, sr = scales_f.cpu().numpy(), scales_r.cpu().numpy()
-    inv_f = (np.float32(1.0) / sf).astype(np.float64)
-    assert np.array_equal(np.rint(y32 * inv_f[:, None, None]).astype(np.int16), codes_f.cpu().numpy())
-    inv_r = np.repeat((np.float32(1.0) / sr).astype(np.float64), enc.nbx, axis=1)[:, :, None]
-    assert np.array_equal(np.rint(y32 * inv_r).astype(np.int16), codes_r.cpu().numpy())
+    assert np.array_equal(kernel_fp32_decision(y32, sf[:, None, None]), codes_f.cpu().numpy())
+    sr_blk = np.repeat(sr, enc.nbx, axis=1)[:, :enc.nblk, None]
+    assert np.array_equal(kernel_fp32_decision(y32, sr_blk), codes_r.cpu().numpy())
     assert np.array_equal(sf, sr.max(axis=1))
 
 
