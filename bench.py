@@ -9,9 +9,10 @@ one per measurement matrix), inputs resident in HBM.  value = CS pixels encoded 
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C4]
 
-Multi-GPU (torchrun): every rank encodes its own independent sequence (weak scaling; GOPs are
-independent, P:87 / SPEC.md:406) -- no data-path collective; a barrier and a MAX all-reduce of
-the device time are the only communication.
+Multi-GPU: `--gpus N` (N > 1) re-runs itself under torch.distributed.run with N ranks (or run it under
+torchrun directly); every rank encodes its own independent sequence (weak scaling; GOPs are
+independent, P:87 / SPEC.md:406) -- no data-path collective; a barrier and a MAX all-reduce of the
+device time are the only communication.
 
 --impl reference times the fp64 CPU oracle (oracle/, the slow correctness reference) on a
 bounded sample of the same workload; on N>1 only rank 0 runs it.
@@ -185,6 +186,71 @@ def timed_steps(args, launch, n_launch, stream, dev, world, flush=None):
     return ms_total, launch_ms, clk
 
 
+def l2_clean_times(launch, n_launch, stream, dev, reps):
+    """Per-launch device time with L2 holding only CLEAN lines before each launch: a read-only pass
+    over a buffer 4x the L2 (a reduction) evicts whatever the previous launch left -- including its
+    dirty output tail, whose write-back would otherwise be charged to the next launch -- without
+    leaving dirty lines itself.  Outside the timed region; for the per-M attribution only."""
+    import torch
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    buf = torch.ones(4 * l2 // 4, dtype=torch.int32, device=dev)
+    sink = torch.empty((), dtype=torch.int64, device=dev)
+    out = []
+    for i in range(n_launch):
+        evs = []
+        for _ in range(reps):
+            torch.sum(buf, out=sink)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            launch(i)
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize(dev)
+        out.append(sum(a.elapsed_time(b) for a, b in evs) / reps)
+    del buf
+    return out
+
+
+def timed_output_parity(cfg, Ms, phis, frames_h, results, gran, n_samples=400, seed=0):
+    """Oracle check of the outputs the timed steps wrote (every step rewrites the same outputs, so the
+    buffers after timing are the timed results): n_samples (CS frame, block) entries of the rank's
+    first stream per M, each recomputed one by one from the definition (oracle.measure_entries).
+    fp32: |y_gpu - y| <= 1e-5 * S (S = 0 -> exactly 0).  q16: the dequantised code is within half a
+    quantisation step (plus the tolerance band) of the exact y."""
+    import oracle
+    rng = np.random.default_rng(seed)
+    nbx, nby = -(-cfg.W // cfg.B), -(-cfg.H // cfg.B)
+    nblk = nbx * nby
+    n_cs_s = cfg.T - -(-cfg.T // cfg.G)
+    worst, n_bad, n = 0.0, 0, 0
+    for M, phi, res in zip(Ms, phis, results):
+        ci = rng.integers(0, n_cs_s, size=n_samples)
+        bi = rng.integers(0, nblk, size=n_samples)
+        bi[: min(n_samples, 8)] = nblk - 1 - np.arange(min(n_samples, 8))   # always include the ragged last blocks
+        y, S = oracle.measure_entries(frames_h[0], phi, cfg.G, cfg.B, ci, bi)
+        if gran is None:
+            g = res.view(-1, nblk, M)[ci, bi].double().cpu().numpy()
+            d = np.abs(g - y)
+            bad = (d > 1e-5 * S) | ((S == 0) & (g != 0))
+            with np.errstate(divide="ignore", invalid="ignore"):
+                rel = np.where(S > 0, d / np.where(S > 0, S, 1.0), 0.0)
+        else:
+            codes, scales = res
+            c = codes.view(-1, nblk, M)[ci, bi].double().cpu().numpy()
+            sc = scales.view(-1, nby)[ci, bi // nbx] if gran == 1 else scales.view(-1)[ci]
+            sc = sc.double().cpu().numpy()[:, None]
+            d = np.abs(c * sc - y)
+            lim = sc * (0.5 + 2.0 ** -21) + 1e-5 * S + 2.0 ** -22 * np.abs(y)
+            bad = d > lim
+            rel = d / lim
+        n_bad += int(bad.sum())
+        n += y.size
+        worst = max(worst, float(rel.max()))
+    key = "max_rel" if gran is None else "max_err_over_bound"
+    return {"n": n, "n_bad": n_bad, key: worst, "ok": n_bad == 0,
+            "how": f"{n_samples} sampled (CS frame, block) entries x M of the timed outputs vs oracle.measure_entries"}
+
+
 def run_ours(args, cfg, Ms):
     import torch
     import torch.distributed as dist
@@ -234,7 +300,7 @@ def run_ours(args, cfg, Ms):
         elif not args.no_autotune:
             # q16 outputs: time the planner's top plans on the q16 call itself (the epilogue differs,
             # so the fp32-tuned plan is not necessarily the fastest); codes are bitwise plan-independent
-            best, best_ms = 0, float("inf")
+            best, best_ms = None, float("inf")
             for k in range(min(args.tune_candidates, e.num_candidates())):
                 e.set_candidate(k)
                 try:
@@ -249,6 +315,8 @@ def run_ours(args, cfg, Ms):
                 t1.synchronize()
                 if t0.elapsed_time(t1) < best_ms:
                     best, best_ms = k, t0.elapsed_time(t1)
+            if best is None:
+                raise SystemExit(f"--output {args.output}: no candidate plan of M={Ms[i]} supports this output")
             e.set_candidate(best)
             tuned[key] = best
     if args.tune_file and rank == 0:
@@ -280,6 +348,10 @@ def run_ours(args, cfg, Ms):
     flush = torch.empty(4 * l2_bytes, dtype=torch.uint8, device=dev) if small else None
     ms_total, launch_ms, clk = timed_steps(args, launch, len(Ms) + (1 if closed else 0), stream, dev, world, flush)
     K = args.steps
+    # per-launch attribution with a clean L2 before every launch (outside the timed region)
+    clean_ms = l2_clean_times(launch, len(Ms) + (1 if closed else 0), stream, dev, max(3, min(K, 10)))
+    if closed:
+        clean_ms = clean_ms[1:]
     key_ms = None
     if closed:
         key_ms = sum(launch_ms[0]) / K
@@ -287,31 +359,44 @@ def run_ours(args, cfg, Ms):
 
     # ---- end to end through the public host-buffer C-ABI call (copies inside the timed region)
     e2e = None
-    if gran is not None or closed:
+    if closed:
         e2e = {"value": None, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-               "how": "not measured: the host-buffer C-ABI call (cs_encode_batch_host) is the open-loop fp32 path"}
+               "how": "not measured: the closed loop has a device-buffer C-ABI call only"}
     elif not args.no_e2e:
         pin_in = torch.from_numpy(frames_h).pin_memory()
-        pin_out = [torch.empty(o.shape, dtype=torch.float32).pin_memory() for o in outs]
-        P.encode_batch_host_multi(encs, pin_in, pin_out)   # warm-up (workspace allocation)
+        if gran is None:
+            pin_out = [torch.empty(e.out_shape(n_seq, cfg.T), dtype=torch.float32).pin_memory() for e in encs]
+
+            def host_call():   # one public call per step: every M over the same host frames
+                P.encode_batch_host_multi(encs, pin_in, pin_out)
+            d2h = sum(o.numel() * 4 for o in pin_out)
+            how = "cs_encode_batch_host_multi"
+        else:
+            pin_out = [(torch.empty(e.out_shape(n_seq, cfg.T), dtype=torch.int16).pin_memory(),
+                        torch.empty(e.q16_scale_shape(n_seq, cfg.T, gran), dtype=torch.float32).pin_memory())
+                       for e in encs]
+
+            def host_call():
+                P.encode_batch_host_multi_q16(encs, pin_in, gran, pin_out)
+            d2h = sum(c.numel() * 2 + sc.numel() * 4 for c, sc in pin_out)
+            how = "cs_encode_batch_host_multi_q16 (int16 codes + fp32 scales copied back)"
+        host_call()   # warm-up (workspace allocation)
         e2e_steps = max(1, min(args.e2e_steps, K))
         if world > 1:
             dist.barrier()
         w0 = time.perf_counter()
-        for _ in range(e2e_steps):   # one public call per step: every M over the same host frames
-            P.encode_batch_host_multi(encs, pin_in, pin_out)
+        for _ in range(e2e_steps):
+            host_call()
         w = (time.perf_counter() - w0) / e2e_steps
         if world > 1:
             tt = torch.tensor([w], device=dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             w = float(tt.item())
         h2d = frames_h.nbytes                       # frames cross PCIe once per step
-        d2h = sum(o.numel() * 4 for o in outs)
         e2e = {"value": world * len(Ms) * cs_pixels(cfg, n_seq) / w / 1e9, "unit": "Gpixel/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": w * 1e3,
-               "how": "cs_encode_batch_host_multi (all M encoders over the same pinned host frames: frames "
-                      "copied in once, H2D + encodes + D2H pipelined in stream groups), wall clock around the "
-                      "synchronous C-ABI call"}
+               "how": how + " (all M encoders over the same pinned host frames: frames copied in once, H2D + "
+                            "encodes + D2H pipelined in stream groups), wall clock around the synchronous C-ABI call"}
 
     if rank != 0:
         if world > 1:
@@ -325,7 +410,8 @@ def run_ours(args, cfg, Ms):
         med = statistics.median(launch_ms[i])
         avg = sum(launch_ms[i]) / K
         b = alg_bytes(cfg, M, n_seq, args.output)
-        per_m[str(M)] = {"ms_median": med, "ms_mean": avg,
+        per_m[str(M)] = {"ms_median": med, "ms_mean": avg, "ms_mean_l2clean": clean_ms[i],
+                         "frac_of_peak_l2clean": alg_bytes(cfg, M, n_seq, args.output) / (clean_ms[i] * 1e-3) / 1e9 / peak,
                          "gpix_s": cs_pixels(cfg, n_seq) / (avg * 1e-3) / 1e9,
                          "alg_gbs": b / (avg * 1e-3) / 1e9, "frac_of_peak": b / (avg * 1e-3) / 1e9 / peak,
                          "alg_bytes": b, "plan": encs[i].plan()}
@@ -365,6 +451,12 @@ def run_ours(args, cfg, Ms):
         "clocks": clk.summary(),
         "e2e": e2e,
     }
+    # oracle leg (rank 0; outside the timed region): parity of the timed outputs, CPU baseline at N=1
+    if closed or args.gop_phis:
+        line["parity"] = {"ok": None, "how": "not checked here (tests/test_gpu_keys.py covers this variant)"}
+    else:
+        phis = [synth.phi_from_seed(synth.phi_seed(), M, cfg.B ** 2) for M in Ms]
+        line["parity"] = timed_output_parity(cfg, Ms, phis, frames_h, outs if gran is None else qouts, gran)
     if not args.no_cpu_baseline and world == 1:   # (rank 0 at N=1 only)
         line["cpu_baseline"] = cpu_baseline(cfg, Ms, budget_s=args.cpu_budget, output=args.output)
     print(json.dumps(line))
@@ -627,7 +719,45 @@ def run_reference(args, cfg, Ms):
     return line
 
 
+def self_launch(args, argv):
+    """--gpus N > 1 without a torchrun environment: re-run this script under torch.distributed.run with
+    N ranks on this node (one process per GPU, rendezvous on 127.0.0.1); rank 0 prints the line."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", str(max(1, (os.cpu_count() or 1) // args.gpus)))
+    return subprocess.call(cmd, env=env)
+
+
+def launcher_check(args):
+    """--launcher-check: the multi-rank plumbing without a GPU (gloo): every rank joins, the max over
+    ranks of a per-rank 'time' is taken as the timed region does, rank 0 prints n_gpus."""
+    import torch
+    import torch.distributed as dist
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.tensor([1.0 + rank])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    else:
+        ms = 1.0
+    if rank == 0:
+        print(json.dumps({"launcher_check": True, "n_gpus": world, "max_ms_over_ranks": ms,
+                          "streams": [rank * synth.CONFIGS[args.workload].S for rank in range(world)]}))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
@@ -649,7 +779,12 @@ def main(argv=None):
     ap.add_argument("--output", choices=list(OUTPUTS), default="f32",
                     help="f32 measurements (headline) or 16-bit codes (f1): per-frame or per-row scales")
     ap.add_argument("--tune-file", default=None, help="json of chosen plan indices (read if present, else written)")
+    ap.add_argument("--launcher-check", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:   # not under torchrun: launch the N ranks ourselves
+        return self_launch(args, argv)
+    if args.launcher_check:
+        return launcher_check(args)
     if args.warmup < 3 and args.impl == "ours":
         ap.error("--warmup must be >= 3")
     cfg = synth.CONFIGS[args.workload]
@@ -664,4 +799,5 @@ def main(argv=None):
 
 
 if __name__ == "__main__":
-    main()
+    rc = main()
+    sys.exit(rc if isinstance(rc, int) else 0)

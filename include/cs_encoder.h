@@ -34,6 +34,11 @@
  * the caller's next synchronisation.  The encoder is immutable after create
  * (except its internal caches, guarded by a mutex), so concurrent encodes on
  * different streams are safe.
+ * Devices: an encoder lives on the device that was current at create.  Every
+ * device-buffer call (encode, q16, adjoint, key codec, set_gop_phis, autotune)
+ * must be made with that device current, else it returns CS_ERR_ARG without
+ * launching; the host-buffer calls switch to it for their duration and restore
+ * the caller's current device.
  */
 #ifndef CS_ENCODER_H
 #define CS_ENCODER_H
@@ -171,8 +176,9 @@ int cs_encode_batch_gops(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, 
  *     is gated by the slowest CTA of its frame); kept as an option.
  *     CS_ERR_UNSUPPORTED when no plan fits (D ring >= 2 accumulators, tiles per frame <= SMs).
  *   CS_Q16_ROW: one scale per (CS frame, block row of B pixel rows): a single fused pass (the
- *     maximum is reduced on chip).  A documented deviation (R19), available when the
- *     plan's tile has <= 40 block rows (CS_ERR_UNSUPPORTED otherwise). */
+ *     maximum is reduced on chip).  A documented deviation (R19).  Needs tiles of
+ *     <= 40 block rows: when the encoder's current plan has taller tiles the call runs the best
+ *     candidate plan that qualifies (CS_ERR_UNSUPPORTED only if none does). */
 #define CS_Q16_FRAME 0
 #define CS_Q16_ROW 1
 #define CS_Q16_FRAME_1PASS 2
@@ -231,7 +237,9 @@ int cs_frame_encode_batch(cs_frame_encoder* enc, const uint8_t* frames_dev, int 
  * Tensor cores (kind::tf32) with y split into two tf32 terms: |error| <~ 1e-6 * sum_m |Phi_mj y_m|.
  * One asynchronous launch on `stream`; no allocation.  Errors: CS_ERR_ARG (NULL / misaligned /
  * n_frames < 0), CS_ERR_UNSUPPORTED (M % 4 != 0: measurement rows must be 16-byte multiples;
- * more than 2^31 blocks in one call), CS_ERR_CUDA. */
+ * more than 2^31 blocks in one call; per-GOP matrices set by cs_encoder_set_gop_phis -- the
+ * adjoint uses the Phi given at create, restore it with cs_encoder_set_gop_phis(enc, 0, NULL)),
+ * CS_ERR_CUDA. */
 int cs_adjoint(cs_encoder* enc, const float* meas_dev, int64_t n_frames, float* x_dev, cs_stream_t stream);
 
 /* ---- closed-loop key frame --------------------------------------- */
@@ -300,6 +308,18 @@ int cs_encode_batch_host(cs_encoder* enc, const uint8_t* frames_host, int n_seq,
  * first encoder's frame workspace and streams; locks every encoder's workspace. */
 int cs_encode_batch_host_multi(cs_encoder* const* encs, int n_enc, const uint8_t* frames_host, int n_seq, int T,
                                float* const* meas_host);
+
+/* 16-bit form of the host calls (f1; SPEC.md:154-162 and the container's "f32 scale + m x i16 codes",
+ * SPEC.md:410): the same pipeline with cs_encode_batch_q16 per group, codes_host = HOST int16 (the
+ * measurement layout, cs_measurement_count entries) and scales_host = HOST fp32 (cs_q16_scale_count
+ * entries), so the device->host copy moves 2 bytes per measurement instead of 4.  Groups are whole
+ * streams (n_seq > 1) or whole GOPs, and every scale (per CS frame or per CS-frame block row) lies
+ * inside one group, so the result equals cs_encode_batch_q16 on the whole batch, bit for bit.
+ * Errors as cs_encode_batch_q16 and cs_encode_batch_host_multi. */
+int cs_encode_batch_host_q16(cs_encoder* enc, const uint8_t* frames_host, int n_seq, int T, int granularity,
+                             int16_t* codes_host, float* scales_host);
+int cs_encode_batch_host_multi_q16(cs_encoder* const* encs, int n_enc, const uint8_t* frames_host, int n_seq, int T,
+                                   int granularity, int16_t* const* codes_host, float* const* scales_host);
 
 /* ---- accounting (host only) ------------------------------------------------------------- */
 

@@ -17,7 +17,7 @@ import numpy as np
 
 from ._build import LIB, build as build_library
 
-__all__ = ["Encoder", "CSError", "total_cr", "compression_ratio_cfg", "measurement_count_cfg", "plan_cfg",
+__all__ = ["Encoder", "FrameEncoder", "encode_batch_host_multi", "encode_batch_host_multi_q16", "CSError", "total_cr", "compression_ratio_cfg", "measurement_count_cfg", "plan_cfg",
            "validate_config", "lib", "LIB", "build_library", "version"]
 
 CS_OK, CS_ERR_ARG, CS_ERR_UNSUPPORTED, CS_ERR_PHI, CS_ERR_CUDA, CS_ERR_OOM = range(6)
@@ -65,6 +65,8 @@ def lib() -> ctypes.CDLL:
             "cs_encode_batch_gops": (c_int, [vp, vp, c_int, c_int, c_int, c_int, vp, vp]),
             "cs_encode_batch_host": (c_int, [vp, vp, c_int, c_int, vp]),
             "cs_encode_batch_host_multi": (c_int, [vp, c_int, vp, c_int, c_int, vp]),
+            "cs_encode_batch_host_q16": (c_int, [vp, vp, c_int, c_int, c_int, vp, vp]),
+            "cs_encode_batch_host_multi_q16": (c_int, [vp, c_int, vp, c_int, c_int, c_int, vp, vp]),
             "cs_encode_batch_q16": (c_int, [vp, vp, c_int, c_int, c_int, vp, vp, vp]),
             "cs_q16_scale_count": (c_i64, [vp, c_int, c_int, c_int]),
             "cs_adjoint": (c_int, [vp, vp, c_i64, vp, vp]),
@@ -149,13 +151,63 @@ def _ptr(t) -> int:
     return int(t.data_ptr())
 
 
-def _stream_handle(stream) -> int:
+def _stream_handle(stream, device=None) -> int:
+    """cudaStream_t of `stream` (torch stream, raw handle or None = the current stream of `device`)."""
     if stream is None:
         import torch
-        return int(torch.cuda.current_stream().cuda_stream)
+        return int(torch.cuda.current_stream(device).cuda_stream)
     if isinstance(stream, int):
         return stream
     return int(stream.cuda_stream)
+
+
+def _dev_tensor(t, dtype, name, device=None, min_numel=None, shape=None):
+    """ValueError unless t is a contiguous CUDA tensor of `dtype` (on `device`, with >= min_numel
+    elements / exactly `shape`): the C ABI takes raw pointers and no lengths."""
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if min_numel is not None and t.numel() < min_numel:
+        raise ValueError(f"{name} has {t.numel()} elements, needs >= {min_numel}")
+    return t
+
+
+def _host_buffer(a, dtype, name, min_numel=None, shape=None):
+    """(pointer, array) of a contiguous HOST numpy array or CPU tensor of `dtype`; ValueError otherwise."""
+    try:
+        import torch
+    except ImportError:   # pragma: no cover
+        torch = None
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.dtype(dtype):
+            raise ValueError(f"{name} must be {np.dtype(dtype)}, got {a.dtype}")
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"{name} must be C-contiguous")
+        ptr, n, shp = a.ctypes.data, a.size, a.shape
+    elif torch is not None and isinstance(a, torch.Tensor):
+        if a.is_cuda:
+            raise ValueError(f"{name} must be host memory")
+        want = {np.uint8: torch.uint8, np.float32: torch.float32, np.int16: torch.int16}[dtype]
+        if a.dtype != want:
+            raise ValueError(f"{name} must be {want}, got {a.dtype}")
+        if not a.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        ptr, n, shp = _ptr(a), a.numel(), tuple(a.shape)
+    else:
+        raise ValueError(f"{name} must be a numpy array or a CPU tensor")
+    if shape is not None and tuple(shp) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(shp)}")
+    if min_numel is not None and n < min_numel:
+        raise ValueError(f"{name} has {n} elements, needs >= {min_numel}")
+    return ptr
 
 
 class Encoder:
@@ -171,6 +223,8 @@ class Encoder:
         h = ctypes.c_void_p()
         _check(lib().cs_encoder_create(W, H, gop, B, M, phi.ctypes.data, ctypes.byref(h)))
         self._h = h
+        import torch
+        self.device = torch.device("cuda", torch.cuda.current_device())   # the encoder lives here (create)
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
@@ -213,29 +267,48 @@ class Encoder:
         n_cs = n_seq * (T - -(-T // self.G))
         return (n_cs, self.nblk, self.M)
 
+    # -- argument checks shared by every wrapper (the C ABI takes pointers and no lengths)
+    def _frames(self, frames, name="frames"):
+        """(n_seq, T) of a contiguous CUDA uint8 [n_seq][T][H][W] tensor on the encoder's device."""
+        import torch
+        _dev_tensor(frames, torch.uint8, name, device=self.device)
+        if frames.dim() != 4 or tuple(frames.shape[2:]) != (self.H, self.W):
+            raise ValueError(f"{name} must be [n_seq][T][{self.H}][{self.W}], got {tuple(frames.shape)}")
+        return int(frames.shape[0]), int(frames.shape[1])
+
+    def _out(self, out, shape, dtype, name="out"):
+        import torch
+        if out is None:
+            return torch.empty(shape, dtype=dtype, device=self.device)
+        n = 1
+        for d in shape:
+            n *= d
+        return _dev_tensor(out, dtype, name, device=self.device, min_numel=n)
+
+    def _call(self, fn, *args, stream=None):
+        """Run a C-ABI launch with the encoder's device current, on `stream` (default: that device's
+        current stream)."""
+        import torch
+        with torch.cuda.device(self.device):
+            _check(fn(*args, _stream_handle(stream, self.device)))
+
     # -- encode (device tensors)
     def encode_batch(self, frames, out=None, stream=None):
         """frames: CUDA uint8 [n_seq][T][H][W] (contiguous); returns CUDA float32 [n_cs][nblk][M]."""
         import torch
-        assert frames.is_cuda and frames.dtype == torch.uint8 and frames.is_contiguous()
-        n_seq, T, H, W = frames.shape
-        assert (H, W) == (self.H, self.W)
-        if out is None:
-            out = torch.empty(self.out_shape(n_seq, T), dtype=torch.float32, device=frames.device)
-        assert out.is_cuda and out.dtype == torch.float32 and out.is_contiguous()
-        assert out.numel() >= self.measurement_count(n_seq, T)
-        _check(lib().cs_encode_batch(self._h, _ptr(frames), n_seq, T, _ptr(out), _stream_handle(stream)))
+        n_seq, T = self._frames(frames)
+        out = self._out(out, self.out_shape(n_seq, T), torch.float32)
+        self._call(lib().cs_encode_batch, self._h, _ptr(frames), n_seq, T, _ptr(out), stream=stream)
         return out
 
     def autotune(self, frames, out=None, max_candidates: int = 6, reps: int = 3, stream=None) -> dict:
         """Time the planner's top plans on these buffers and keep the fastest (outputs are bitwise
         identical across plans).  Returns the chosen plan."""
         import torch
-        n_seq, T = frames.shape[:2]
-        if out is None:
-            out = torch.empty(self.out_shape(n_seq, T), dtype=torch.float32, device=frames.device)
-        _check(lib().cs_encoder_autotune(self._h, _ptr(frames), n_seq, T, _ptr(out), max_candidates, reps,
-                                         _stream_handle(stream)))
+        n_seq, T = self._frames(frames)
+        out = self._out(out, self.out_shape(n_seq, T), torch.float32)
+        self._call(lib().cs_encoder_autotune, self._h, _ptr(frames), n_seq, T, _ptr(out), max_candidates, reps,
+                   stream=stream)
         return self.plan()
 
     def num_candidates(self) -> int:
@@ -248,19 +321,31 @@ class Encoder:
         _check(lib().cs_encoder_set_candidate(self._h, index))
         return self.plan()
 
+    def gop_range_count(self, n_seq: int, T: int, gop_begin: int, gop_end: int) -> int:
+        """Measurements cs_encode_batch_gops writes for GOPs [gop_begin, gop_end) of every stream."""
+        n_cs = sum(max(0, min(self.G, T - g * self.G) - 1) for g in range(gop_begin, gop_end))
+        return n_seq * n_cs * self.nblk * self.M
+
     def encode_batch_gops(self, frames, gop_begin: int, gop_end: int, out, stream=None):
-        n_seq, T = frames.shape[:2]
-        _check(lib().cs_encode_batch_gops(self._h, _ptr(frames), n_seq, T, gop_begin, gop_end, _ptr(out),
-                                          _stream_handle(stream)))
+        import torch
+        n_seq, T = self._frames(frames)
+        if not (0 <= gop_begin <= gop_end <= self.n_gops(T)):
+            raise ValueError("GOP range out of bounds")
+        _dev_tensor(out, torch.float32, "out", device=self.device,
+                    min_numel=self.gop_range_count(n_seq, T, gop_begin, gop_end))
+        self._call(lib().cs_encode_batch_gops, self._h, _ptr(frames), n_seq, T, gop_begin, gop_end, _ptr(out),
+                   stream=stream)
         return out
 
     def encode_gop(self, frames, out=None, stream=None):
         """frames: CUDA uint8 [n][H][W], 1 <= n <= gop, frame 0 = key; returns [n-1][nblk][M]."""
         import torch
-        n = frames.shape[0]
-        if out is None:
-            out = torch.empty((max(n - 1, 0), self.nblk, self.M), dtype=torch.float32, device=frames.device)
-        _check(lib().cs_encode_gop(self._h, _ptr(frames), n, _ptr(out), _stream_handle(stream)))
+        _dev_tensor(frames, torch.uint8, "frames", device=self.device)
+        if frames.dim() != 3 or tuple(frames.shape[1:]) != (self.H, self.W):
+            raise ValueError(f"frames must be [n][{self.H}][{self.W}], got {tuple(frames.shape)}")
+        n = int(frames.shape[0])
+        out = self._out(out, (max(n - 1, 0), self.nblk, self.M), torch.float32)
+        self._call(lib().cs_encode_gop, self._h, _ptr(frames), n, _ptr(out), stream=stream)
         return out
 
     # -- 16-bit quantisation (f1; SPEC.md:154-162)
@@ -274,20 +359,11 @@ class Encoder:
         """frames: CUDA uint8 [n_seq][T][H][W]; returns (codes int16 [n_cs][nblk][M], scales fp32
         [n_cs] (Q16_FRAME, SPEC's per-frame scale) or [n_cs][nby] (Q16_ROW, per block row))."""
         import torch
-        assert frames.is_cuda and frames.dtype == torch.uint8 and frames.is_contiguous()
-        n_seq, T, H, W = frames.shape
-        assert (H, W) == (self.H, self.W)
-        if codes is None:
-            codes = torch.empty(self.out_shape(n_seq, T), dtype=torch.int16, device=frames.device)
-        if scales is None:
-            scales = torch.empty(self.q16_scale_shape(n_seq, T, granularity), dtype=torch.float32,
-                                 device=frames.device)
-        assert codes.is_cuda and codes.dtype == torch.int16 and codes.is_contiguous()
-        assert scales.is_cuda and scales.dtype == torch.float32 and scales.is_contiguous()
-        assert codes.numel() >= self.measurement_count(n_seq, T)
-        assert scales.numel() >= lib().cs_q16_scale_count(self._h, n_seq, T, granularity)
-        _check(lib().cs_encode_batch_q16(self._h, _ptr(frames), n_seq, T, granularity, _ptr(codes), _ptr(scales),
-                                         _stream_handle(stream)))
+        n_seq, T = self._frames(frames)
+        codes = self._out(codes, self.out_shape(n_seq, T), torch.int16, "codes")
+        scales = self._out(scales, self.q16_scale_shape(n_seq, T, granularity), torch.float32, "scales")
+        self._call(lib().cs_encode_batch_q16, self._h, _ptr(frames), n_seq, T, granularity, _ptr(codes),
+                   _ptr(scales), stream=stream)
         return codes, scales
 
     # -- closed-loop key frame (f4; Eq. 2-3, SPEC.md:282-308)
@@ -298,49 +374,46 @@ class Encoder:
         """frames: CUDA uint8 [n_seq][T][H][W]; qsteps: int [8][8] (see key_qsteps).  Returns
         (decoded keys uint8 [n_seq][ceil(T/G)][H][W], coefficients int16 [...][nby8][nbx8][8][8] or None)."""
         import torch
-        assert frames.is_cuda and frames.dtype == torch.uint8 and frames.is_contiguous()
-        n_seq, T = frames.shape[:2]
+        n_seq, T = self._frames(frames)
         ng = self.n_gops(T)
-        if keys is None:
-            keys = torch.empty((n_seq, ng, self.H, self.W), dtype=torch.uint8, device=frames.device)
-        if coef is None and want_coef:
-            coef = torch.empty((n_seq, ng, -(-self.H // 8), -(-self.W // 8), 8, 8), dtype=torch.int16,
-                               device=frames.device)
+        keys = self._out(keys, (n_seq, ng, self.H, self.W), torch.uint8, "keys")
+        if coef is not None or want_coef:
+            coef = self._out(coef, (n_seq, ng, -(-self.H // 8), -(-self.W // 8), 8, 8), torch.int16, "coef")
         q = np.ascontiguousarray(qsteps, dtype=np.int32).ravel()
-        assert q.size == 64
-        _check(lib().cs_key_codec(self._h, _ptr(frames), n_seq, T, q.ctypes.data,
-                                  _ptr(coef) if coef is not None else None, _ptr(keys), _stream_handle(stream)))
+        if q.size != 64:
+            raise ValueError("qsteps must have 64 entries")
+        self._call(lib().cs_key_codec, self._h, _ptr(frames), n_seq, T, q.ctypes.data,
+                   _ptr(coef) if coef is not None else None, _ptr(keys), stream=stream)
         return keys, coef
 
     def encode_batch_keys(self, frames, keys, out=None, stream=None):
         """cs_encode_batch with residuals against keys [n_seq][ceil(T/G)][H][W] (decoded key frames)."""
         import torch
-        n_seq, T = frames.shape[:2]
-        assert keys.is_cuda and keys.dtype == torch.uint8 and keys.is_contiguous()
-        assert keys.shape == (n_seq, self.n_gops(T), self.H, self.W)
-        if out is None:
-            out = torch.empty(self.out_shape(n_seq, T), dtype=torch.float32, device=frames.device)
-        _check(lib().cs_encode_batch_keys(self._h, _ptr(frames), n_seq, T, _ptr(keys), _ptr(out),
-                                          _stream_handle(stream)))
+        n_seq, T = self._frames(frames)
+        _dev_tensor(keys, torch.uint8, "keys", device=self.device, shape=(n_seq, self.n_gops(T), self.H, self.W))
+        out = self._out(out, self.out_shape(n_seq, T), torch.float32)
+        self._call(lib().cs_encode_batch_keys, self._h, _ptr(frames), n_seq, T, _ptr(keys), _ptr(out), stream=stream)
         return out
 
     def set_gop_phis(self, phis=None):
         """Per-GOP matrices: phis uint16 [n][M][B*B]; GOP g uses phis[g % n].  None or
         an empty list restores the single Phi."""
-        if phis is None or len(phis) == 0:
-            _check(lib().cs_encoder_set_gop_phis(self._h, 0, None))
-            return
-        a = np.ascontiguousarray(np.stack([np.asarray(x, dtype=np.uint16) for x in phis]))
-        assert a.shape[1:] == (self.M, self.B * self.B)
-        _check(lib().cs_encoder_set_gop_phis(self._h, a.shape[0], a.ctypes.data))
+        import torch
+        with torch.cuda.device(self.device):
+            if phis is None or len(phis) == 0:
+                _check(lib().cs_encoder_set_gop_phis(self._h, 0, None))
+                return
+            a = np.ascontiguousarray(np.stack([np.asarray(x, dtype=np.uint16) for x in phis]))
+            if a.shape[1:] != (self.M, self.B * self.B):
+                raise ValueError(f"phis must be [n][{self.M}][{self.B * self.B}], got {a.shape}")
+            _check(lib().cs_encoder_set_gop_phis(self._h, a.shape[0], a.ctypes.data))
 
     def encode_batch_chained(self, frames, out=None, stream=None):
         """Eq. 3 literal variant: residual of every CS frame against the previous raw frame."""
         import torch
-        n_seq, T = frames.shape[:2]
-        if out is None:
-            out = torch.empty(self.out_shape(n_seq, T), dtype=torch.float32, device=frames.device)
-        _check(lib().cs_encode_batch_chained(self._h, _ptr(frames), n_seq, T, _ptr(out), _stream_handle(stream)))
+        n_seq, T = self._frames(frames)
+        out = self._out(out, self.out_shape(n_seq, T), torch.float32)
+        self._call(lib().cs_encode_batch_chained, self._h, _ptr(frames), n_seq, T, _ptr(out), stream=stream)
         return out
 
     def encode_batch_closed_loop(self, frames, qsteps, out=None, stream=None):
@@ -353,39 +426,89 @@ class Encoder:
         """meas: CUDA float32 [n][nblk][M] (contiguous); returns CUDA float32 [n][H][W] = Phi^T y per
         block laid back into the frame."""
         import torch
-        assert meas.is_cuda and meas.dtype == torch.float32 and meas.is_contiguous()
+        _dev_tensor(meas, torch.float32, "meas", device=self.device)
         n = meas.numel() // (self.nblk * self.M)
-        assert meas.numel() == n * self.nblk * self.M
-        if out is None:
-            out = torch.empty((n, self.H, self.W), dtype=torch.float32, device=meas.device)
-        assert out.is_cuda and out.dtype == torch.float32 and out.is_contiguous() and out.numel() >= n * self.H * self.W
-        _check(lib().cs_adjoint(self._h, _ptr(meas), n, _ptr(out), _stream_handle(stream)))
+        if meas.numel() != n * self.nblk * self.M:
+            raise ValueError(f"meas must hold whole frames of {self.nblk * self.M} measurements")
+        out = self._out(out, (n, self.H, self.W), torch.float32)
+        self._call(lib().cs_adjoint, self._h, _ptr(meas), n, _ptr(out), stream=stream)
         return out
 
     # -- encode (host buffers)
+    def _host_frames(self, frames):
+        if frames.ndim != 4 or tuple(frames.shape[2:]) != (self.H, self.W):
+            raise ValueError(f"frames must be [n_seq][T][{self.H}][{self.W}], got {tuple(frames.shape)}")
+        return int(frames.shape[0]), int(frames.shape[1]), _host_buffer(frames, np.uint8, "frames")
+
     def encode_batch_host(self, frames, out=None):
         """frames: host uint8 [n_seq][T][H][W] (numpy or CPU tensor, pinned for full bandwidth);
         copies in, encodes, copies out; returns host float32 [n_cs][nblk][M]."""
-        n_seq, T = frames.shape[:2]
+        n_seq, T, fp = self._host_frames(frames)
         if out is None:
             out = np.empty(self.out_shape(n_seq, T), dtype=np.float32)
-        fp = frames.ctypes.data if isinstance(frames, np.ndarray) else _ptr(frames)
-        op = out.ctypes.data if isinstance(out, np.ndarray) else _ptr(out)
+        op = _host_buffer(out, np.float32, "out", min_numel=self.measurement_count(n_seq, T))
         _check(lib().cs_encode_batch_host(self._h, fp, n_seq, T, op))
         return out
+
+    def encode_batch_host_q16(self, frames, granularity: int = 0, codes=None, scales=None):
+        """Host-buffer form of encode_batch_q16 (f1): frames in, int16 codes + fp32 scales out; the
+        device->host copy moves 2 B per measurement instead of 4."""
+        n_seq, T, fp = self._host_frames(frames)
+        if codes is None:
+            codes = np.empty(self.out_shape(n_seq, T), dtype=np.int16)
+        if scales is None:
+            scales = np.empty(self.q16_scale_shape(n_seq, T, granularity), dtype=np.float32)
+        cp = _host_buffer(codes, np.int16, "codes", min_numel=self.measurement_count(n_seq, T))
+        sp = _host_buffer(scales, np.float32, "scales",
+                          min_numel=lib().cs_q16_scale_count(self._h, n_seq, T, granularity))
+        _check(lib().cs_encode_batch_host_q16(self._h, fp, n_seq, T, granularity, cp, sp))
+        return codes, scales
+
+
+def _multi_args(encoders, frames):
+    if not encoders:
+        raise ValueError("need at least one encoder")
+    e0 = encoders[0]
+    for e in encoders:
+        if (e.W, e.H, e.G) != (e0.W, e0.H, e0.G):
+            raise ValueError("encoders must share W, H and gop")
+    return e0._host_frames(frames)
 
 
 def encode_batch_host_multi(encoders, frames, outs=None):
     """Several encoders (same W, H, gop) over the same HOST frames [n_seq][T][H][W]: each frame group
     crosses PCIe once.  frames: numpy or (pinned) CPU tensor; returns the list of host outputs."""
-    n_seq, T = frames.shape[:2]
+    n_seq, T, fp = _multi_args(encoders, frames)
     if outs is None:
         outs = [np.empty(e.out_shape(n_seq, T), dtype=np.float32) for e in encoders]
+    if len(outs) != len(encoders):
+        raise ValueError("one output per encoder")
     hs = (ctypes.c_void_p * len(encoders))(*[e._h.value for e in encoders])
-    ps = (ctypes.c_void_p * len(outs))(*[o.ctypes.data if isinstance(o, np.ndarray) else _ptr(o) for o in outs])
-    fp = frames.ctypes.data if isinstance(frames, np.ndarray) else _ptr(frames)
+    ps = (ctypes.c_void_p * len(outs))(*[_host_buffer(o, np.float32, "out", min_numel=e.measurement_count(n_seq, T))
+                                         for e, o in zip(encoders, outs)])
     _check(lib().cs_encode_batch_host_multi(ctypes.cast(hs, ctypes.c_void_p), len(encoders), fp, n_seq, T,
                                             ctypes.cast(ps, ctypes.c_void_p)))
+    return outs
+
+
+def encode_batch_host_multi_q16(encoders, frames, granularity: int = 0, outs=None):
+    """cs_encode_batch_host_multi_q16: every encoder's int16 codes + fp32 scales of the same HOST frames.
+    Returns the list of (codes, scales) host pairs."""
+    n_seq, T, fp = _multi_args(encoders, frames)
+    if outs is None:
+        outs = [(np.empty(e.out_shape(n_seq, T), dtype=np.int16),
+                 np.empty(e.q16_scale_shape(n_seq, T, granularity), dtype=np.float32)) for e in encoders]
+    if len(outs) != len(encoders):
+        raise ValueError("one (codes, scales) pair per encoder")
+    hs = (ctypes.c_void_p * len(encoders))(*[e._h.value for e in encoders])
+    cps = (ctypes.c_void_p * len(outs))(*[_host_buffer(c, np.int16, "codes", min_numel=e.measurement_count(n_seq, T))
+                                          for e, (c, _) in zip(encoders, outs)])
+    sps = (ctypes.c_void_p * len(outs))(*[_host_buffer(sc, np.float32, "scales",
+                                                       min_numel=lib().cs_q16_scale_count(e._h, n_seq, T, granularity))
+                                          for e, (_, sc) in zip(encoders, outs)])
+    _check(lib().cs_encode_batch_host_multi_q16(ctypes.cast(hs, ctypes.c_void_p), len(encoders), fp, n_seq, T,
+                                                granularity, ctypes.cast(cps, ctypes.c_void_p),
+                                                ctypes.cast(sps, ctypes.c_void_p)))
     return outs
 
 
@@ -401,6 +524,8 @@ class FrameEncoder:
         h = ctypes.c_void_p()
         _check(lib().cs_frame_encoder_create(W, H, gop, m, A.ctypes.data, ctypes.byref(h)))
         self._h = h
+        import torch
+        self.device = torch.device("cuda", torch.cuda.current_device())
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
@@ -423,12 +548,15 @@ class FrameEncoder:
     def encode_batch(self, frames, out=None, stream=None):
         """frames: CUDA uint8 [n_seq][T][H][W]; returns CUDA float32 [n_cs][m]."""
         import torch
-        assert frames.is_cuda and frames.dtype == torch.uint8 and frames.is_contiguous()
-        n_seq, T, H, W = frames.shape
-        assert (H, W) == (self.H, self.W)
+        _dev_tensor(frames, torch.uint8, "frames", device=self.device)
+        if frames.dim() != 4 or tuple(frames.shape[2:]) != (self.H, self.W):
+            raise ValueError(f"frames must be [n_seq][T][{self.H}][{self.W}], got {tuple(frames.shape)}")
+        n_seq, T = int(frames.shape[0]), int(frames.shape[1])
         if out is None:
-            out = torch.empty(self.out_shape(n_seq, T), dtype=torch.float32, device=frames.device)
-        assert out.is_cuda and out.dtype == torch.float32 and out.is_contiguous()
-        assert out.numel() >= lib().cs_frame_measurement_count(self._h, n_seq, T)
-        _check(lib().cs_frame_encode_batch(self._h, _ptr(frames), n_seq, T, _ptr(out), _stream_handle(stream)))
+            out = torch.empty(self.out_shape(n_seq, T), dtype=torch.float32, device=self.device)
+        _dev_tensor(out, torch.float32, "out", device=self.device,
+                    min_numel=lib().cs_frame_measurement_count(self._h, n_seq, T))
+        with torch.cuda.device(self.device):
+            _check(lib().cs_frame_encode_batch(self._h, _ptr(frames), n_seq, T, _ptr(out),
+                                               _stream_handle(stream, self.device)))
         return out

@@ -25,16 +25,26 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Compile every translation unit (in parallel) and link libcsenc.so."""
     if out is None and not force and not _stale():
         return LIB
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
     target = out or LIB
     os.makedirs(LIB_DIR, exist_ok=True)
-    cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-I", os.path.join(ROOT, "include"), "-o", target + ".tmp"] + [f"-D{d}" for d in defines]
+    flags = [*ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
+    flags += [f"-D{d}" for d in defines]
     if verbose:
-        cmd += ["-Xptxas", "-v"]
-    cmd += [os.path.join(CSRC, f) for f in SOURCES]
-    subprocess.check_call(cmd)
+        flags += ["-Xptxas", "-v"]
+    with tempfile.TemporaryDirectory(prefix="csenc_build_") as tmp:
+        objs = [os.path.join(tmp, f.replace(".cu", ".o")) for f in SOURCES]
+
+        def compile_one(i):
+            subprocess.check_call([NVCC, *flags, "-c", os.path.join(CSRC, SOURCES[i]), "-o", objs[i]])
+
+        with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+            list(ex.map(compile_one, range(len(SOURCES))))
+        subprocess.check_call([NVCC, *ARCH, "-shared", "-o", target + ".tmp", *objs])
     os.replace(target + ".tmp", target)
     return target
 

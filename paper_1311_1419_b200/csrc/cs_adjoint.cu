@@ -139,6 +139,10 @@ int cs_adjoint(cs_encoder* e, const float* meas, int64_t n_frames, float* x, cs_
     if (!meas || !x) return fail(CS_ERR_ARG, "NULL buffer");
     if (!aligned16(meas) || !aligned16(x)) return fail(CS_ERR_ARG, "buffers must be 16-byte aligned");
     if (!e->phiT_dev) return fail(CS_ERR_UNSUPPORTED, "adjoint needs M % 4 == 0 (16-byte measurement rows)");
+    if (e->n_phis > 0)
+        return fail(CS_ERR_UNSUPPORTED, "adjoint: per-GOP matrices are set (cs_encoder_set_gop_phis); Phi^T is that of the "
+                                        "single Phi given at create -- restore it with cs_encoder_set_gop_phis(e, 0, NULL)");
+    if (int rc = check_device(e->device)) return rc;
     const Geometry& g = e->geo;
     if (n_frames * (long long)g.nblk >= 0x7FFFFFFFLL || n_frames * (long long)g.nby * cdiv(g.nbx, 128) >= 0x7FFFFFFFLL)
         return fail(CS_ERR_UNSUPPORTED, "too many frames for one call");

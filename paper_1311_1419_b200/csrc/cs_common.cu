@@ -36,6 +36,16 @@ bool nvtx_enabled() {
     return on;
 }
 
+int check_device(int device) {
+    int cur = -1;
+    const cudaError_t err = cudaGetDevice(&cur);
+    if (err != cudaSuccess) return cuda_fail(err, "cudaGetDevice");
+    if (cur != device)
+        return fail(CS_ERR_ARG, "the current device (" + std::to_string(cur) + ") is not the device the encoder was created on (" +
+                                    std::to_string(device) + "): call cudaSetDevice first");
+    return CS_OK;
+}
+
 int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
     return v ? std::atoi(v) : dflt;

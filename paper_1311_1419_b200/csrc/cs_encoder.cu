@@ -610,6 +610,13 @@ int cs_encoder_create(int W, int H, int gop, int B, int M, const uint16_t* phi_f
             e->chained_plan = (int)i;
             break;
         }
+    // f1 row scales: the best plan whose tiles have <= kRowSlots block rows (used when the current
+    // plan -- model choice, autotuned or set -- has more)
+    for (size_t i = 0; i < e->candidates.size(); ++i)
+        if (e->candidates[i].T_r <= csenc::kRowSlots) {
+            e->row_plan = (int)i;
+            break;
+        }
     // f1 single pass: the best plan with a D ring deep enough for the look-back whose tiles fit one
     // round (n_tiles <= SMs)
     for (size_t i = 0; i < e->candidates.size(); ++i) {
@@ -725,6 +732,7 @@ int cs_encoder_autotune(cs_encoder* e, const uint8_t* frames, int n_seq, int T, 
                         int reps, cs_stream_t stream) {
     if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
     if (max_candidates < 1 || reps < 1) return fail(CS_ERR_ARG, "max_candidates and reps must be >= 1");
+    if (int rc = check_device(e->device)) return rc;
     if (cs_frames_per_stream(T, e->geo.G) * n_seq == 0) return CS_OK;
     cudaStream_t s = (cudaStream_t)stream;
     cudaEvent_t e0, e1;
@@ -805,6 +813,7 @@ int cs_encode_batch_gops(cs_encoder* e, const uint8_t* frames, int n_seq, int T,
     if (!frames || !out) return fail(CS_ERR_ARG, "NULL buffer");
     if (!aligned16(frames) || !aligned16(out)) return fail(CS_ERR_ARG, "buffers must be 16-byte aligned");
     if ((long long)n_seq * T > 0x7FFFFFFFLL) return fail(CS_ERR_UNSUPPORTED, "too many frames");
+    if (int rc = check_device(e->device)) return rc;
     return launch(e, frames, n_seq, T, g0, g1, out, (cudaStream_t)stream);
 }
 
@@ -827,6 +836,7 @@ int cs_encoder_set_gop_phis(cs_encoder* e, int n_phi, const uint16_t* phis) {
     if (n_phi < 0 || (n_phi > 0 && !phis)) return fail(CS_ERR_ARG, "n_phi must be >= 0 and phis non-NULL");
     const Geometry& g = e->geo;
     const size_t per = (size_t)g.M * g.N;
+    if (int rc = check_device(e->device)) return rc;
     for (int i = 0; i < n_phi; ++i) {
         const int rc = validate(g.W, g.H, g.G, g.B, g.M, phis + (size_t)i * per);
         if (rc != CS_OK) return rc;
@@ -858,6 +868,7 @@ int cs_encode_batch_chained(cs_encoder* e, const uint8_t* frames, int n_seq, int
     if (!aligned16(frames) || !aligned16(out)) return fail(CS_ERR_ARG, "buffers must be 16-byte aligned");
     if ((long long)n_seq * T > 0x7FFFFFFFLL) return fail(CS_ERR_UNSUPPORTED, "too many frames");
     if (e->chained_plan < 0) return fail(CS_ERR_UNSUPPORTED, "no streamed-key plan fits this configuration");
+    if (int rc = check_device(e->device)) return rc;
     QArgs q;
     q.chained = 1;
     q.plan = &e->candidates[(size_t)e->chained_plan];
@@ -872,6 +883,7 @@ int cs_encode_batch_keys(cs_encoder* e, const uint8_t* frames, int n_seq, int T,
     if (!frames || !keys || !out) return fail(CS_ERR_ARG, "NULL buffer");
     if (!aligned16(frames) || !aligned16(keys) || !aligned16(out)) return fail(CS_ERR_ARG, "buffers must be 16-byte aligned");
     if ((long long)n_seq * T > 0x7FFFFFFFLL) return fail(CS_ERR_UNSUPPORTED, "too many frames");
+    if (int rc = check_device(e->device)) return rc;
     QArgs q;
     q.keys = keys;
     return launch(e, frames, n_seq, T, 0, cdiv(T, e->geo.G), out, (cudaStream_t)stream, q);
@@ -899,13 +911,17 @@ int cs_encode_batch_q16(cs_encoder* e, const uint8_t* frames, int n_seq, int T, 
     if (!aligned16(frames) || !aligned16(codes) || (reinterpret_cast<uintptr_t>(scales) & 3u))
         return fail(CS_ERR_ARG, "frames/codes must be 16-byte aligned, scales 4-byte aligned");
     if ((long long)n_seq * T > 0x7FFFFFFFLL) return fail(CS_ERR_UNSUPPORTED, "too many frames");
+    if (int rc = check_device(e->device)) return rc;
     const int n_gops = cdiv(T, g.G);
     const cudaStream_t st = (cudaStream_t)stream;
     QArgs q;
     q.codes = codes;
     if (granularity == CS_Q16_ROW) {
-        if (e->plan.T_r > csenc::kRowSlots)
-            return fail(CS_ERR_UNSUPPORTED, "row-scale quantisation needs a plan with <= 40 block rows per tile");
+        if (e->plan.T_r > csenc::kRowSlots) {   // the current plan's tiles are too tall: the best one that fits
+            if (e->row_plan < 0)
+                return fail(CS_ERR_UNSUPPORTED, "row-scale quantisation: no plan with <= 40 block rows per tile fits");
+            q.plan = &e->candidates[(size_t)e->row_plan];
+        }
         q.qmode = csenc::Q_ROW;
         q.scales = scales;
         return launch(e, frames, n_seq, T, 0, n_gops, nullptr, st, q);
@@ -976,8 +992,18 @@ int cs_encode_batch_q16(cs_encoder* e, const uint8_t* frames, int n_seq, int T, 
     return err == cudaSuccess ? CS_OK : cuda_fail(err, "finalize launch");
 }
 
-int cs_encode_batch_host_multi(cs_encoder* const* encs, int n_enc, const uint8_t* frames_host, int n_seq, int T,
-                               float* const* outs_host) {
+}  // extern "C"
+
+namespace {
+
+// Host-buffer pipeline shared by the fp32 and q16 host calls.  granularity < 0: fp32 measurements into
+// outs_host[k] (float); otherwise int16 codes into outs_host[k] and fp32 scales into scales_host[k].
+// Groups are chunks of streams (n_seq > 1) or of whole GOPs of the single stream; a GOP range of one
+// stream is itself a stream of whole GOPs starting at a key frame, so every group is one ordinary
+// device-buffer call on a sub-batch.  Copy-in of group i+1 overlaps the encodes of group i and the
+// copy-outs of group i-1; each frame group crosses PCIe once whatever the number of encoders.
+int host_pipeline(cs_encoder* const* encs, int n_enc, const uint8_t* frames_host, int n_seq, int T, int granularity,
+                  void* const* outs_host, float* const* scales_host) {
     if (!encs || n_enc < 1) return fail(CS_ERR_ARG, "encoders: need at least one");
     for (int k = 0; k < n_enc; ++k) {
         if (!encs[k]) return fail(CS_ERR_ARG, "encoder is NULL");
@@ -989,15 +1015,23 @@ int cs_encode_batch_host_multi(cs_encoder* const* encs, int n_enc, const uint8_t
             return fail(CS_ERR_ARG, "encoders must share W, H, gop and device");
     }
     if (n_seq < 0 || T < 0) return fail(CS_ERR_ARG, "n_seq and T must be >= 0");
+    const bool q16 = granularity >= 0;
+    if (q16 && granularity != CS_Q16_FRAME && granularity != CS_Q16_ROW && granularity != CS_Q16_FRAME_1PASS)
+        return fail(CS_ERR_ARG, "bad granularity");
     cs_encoder* const e = encs[0];   // frames workspace, streams and events
     const Geometry& g = e->geo;
     const long long cs_s = cs_frames_per_stream(T, g.G);
     if (n_seq == 0 || T == 0 || cs_s == 0) return CS_OK;
-    if (!frames_host || !outs_host) return fail(CS_ERR_ARG, "NULL buffer");
+    if (!frames_host || !outs_host || (q16 && !scales_host)) return fail(CS_ERR_ARG, "NULL buffer");
     for (int k = 0; k < n_enc; ++k)
-        if (!outs_host[k]) return fail(CS_ERR_ARG, "NULL output buffer");
+        if (!outs_host[k] || (q16 && !scales_host[k])) return fail(CS_ERR_ARG, "NULL output buffer");
+    if ((long long)n_seq * T > 0x7FFFFFFFLL) return fail(CS_ERR_UNSUPPORTED, "too many frames");
+    DeviceGuard dev_guard(e->device);   // synchronous host call: run on the encoders' device
+    if (!dev_guard.ok) return fail(CS_ERR_CUDA, "cannot switch to the encoder's device");
     const size_t frame_bytes = (size_t)g.W * g.H;
     const size_t in_bytes = (size_t)n_seq * T * frame_bytes;
+    const size_t n_cs = (size_t)n_seq * cs_s;
+    const size_t elem = q16 ? sizeof(int16_t) : sizeof(float);
     // workspaces are per encoder: lock them in address order (no deadlock between concurrent callers)
     std::vector<cs_encoder*> order(encs, encs + n_enc);
     std::sort(order.begin(), order.end());
@@ -1012,9 +1046,14 @@ int cs_encode_batch_host_multi(cs_encoder* const* encs, int n_enc, const uint8_t
             return fail(CS_ERR_OOM, std::string("workspace: ") + cudaGetErrorString(err));
         e->ws_frames_bytes = in_bytes;
     }
+    // per encoder: [measurements or codes][scales] (scales at a 256-byte aligned offset)
+    std::vector<size_t> sc_off(n_enc, 0), sc_per_cs(n_enc, 0);
     for (int k = 0; k < n_enc; ++k) {
         cs_encoder* x = encs[k];
-        const size_t out_bytes = (size_t)n_seq * cs_s * x->geo.nblk * x->geo.M * sizeof(float);
+        const size_t meas_bytes = n_cs * (size_t)x->geo.nblk * x->geo.M * elem;
+        sc_per_cs[k] = !q16 ? 0 : (granularity == CS_Q16_ROW ? (size_t)x->geo.nby : 1);
+        sc_off[k] = (meas_bytes + 255) / 256 * 256;
+        const size_t out_bytes = sc_off[k] + n_cs * sc_per_cs[k] * sizeof(float);
         if (x->ws_out_bytes < out_bytes) {
             if (x->ws_out) cudaFree(x->ws_out);
             x->ws_out = nullptr;
@@ -1027,9 +1066,6 @@ int cs_encode_batch_host_multi(cs_encoder* const* encs, int n_enc, const uint8_t
     for (auto& st : e->hs)
         if (!st && (err = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess)
             return cuda_fail(err, "cudaStreamCreate");
-    // Groups: chunks of streams (n_seq > 1) or of GOPs (n_seq == 1).  Copy-in of group i+1 overlaps
-    // the encodes of group i and the copy-outs of group i-1; each frame group crosses PCIe once
-    // whatever the number of encoders.
     struct Grp {
         int s0, s1, g0, g1;
     };
@@ -1053,13 +1089,24 @@ int cs_encode_batch_host_multi(cs_encoder* const* encs, int n_enc, const uint8_t
     int rc = CS_OK;
     for (size_t i = 0; i < groups.size() && rc == CS_OK; ++i) {
         const Grp& gr = groups[i];
-        size_t f0, f1;  // frame range (global, [s][t] order) of this group
+        // the group as a sub-batch: streams [s0, s1) x all T frames, or frames [g0*G, min(g1*G, T)) of
+        // the single stream (whole GOPs from a key frame)
+        size_t f0, f1, c0, c1;   // frame range (global [s][t] order) and CS-frame range of the group
+        int sub_seq, sub_T;
         if (n_seq > 1) {
             f0 = (size_t)gr.s0 * T;
             f1 = (size_t)gr.s1 * T;
+            c0 = (size_t)gr.s0 * cs_s;
+            c1 = (size_t)gr.s1 * cs_s;
+            sub_seq = gr.s1 - gr.s0;
+            sub_T = T;
         } else {
             f0 = (size_t)gr.g0 * g.G;
             f1 = std::min((size_t)gr.g1 * g.G, (size_t)T);
+            c0 = (size_t)cs_frames_in_gops(T, g.G, 0, gr.g0);
+            c1 = (size_t)cs_frames_in_gops(T, g.G, 0, gr.g1);
+            sub_seq = 1;
+            sub_T = (int)(f1 - f0);
         }
         err = cudaMemcpyAsync(e->ws_frames + f0 * frame_bytes, frames_host + f0 * frame_bytes,
                               (f1 - f0) * frame_bytes, cudaMemcpyHostToDevice, s_in);
@@ -1070,27 +1117,25 @@ int cs_encode_batch_host_multi(cs_encoder* const* encs, int n_enc, const uint8_t
         cudaEvent_t* ev = &e->hev[i * (size_t)(1 + n_enc)];
         cudaEventRecord(ev[0], s_in);
         cudaStreamWaitEvent(s_run, ev[0], 0);
+        if (c1 == c0) continue;
         for (int k = 0; k < n_enc && rc == CS_OK; ++k) {
             cs_encoder* x = encs[k];
-            const size_t cs_meas = (size_t)x->geo.nblk * x->geo.M;   // floats per CS frame
-            size_t o0, o1;  // output float range
-            if (n_seq > 1) {
-                o0 = (size_t)gr.s0 * cs_s * cs_meas;
-                o1 = (size_t)gr.s1 * cs_s * cs_meas;
-                rc = cs_encode_batch(x, e->ws_frames + f0 * frame_bytes, gr.s1 - gr.s0, T, x->ws_out + o0, s_run);
-            } else {
-                o0 = (size_t)cs_frames_in_gops(T, g.G, 0, gr.g0) * cs_meas;
-                o1 = (size_t)cs_frames_in_gops(T, g.G, 0, gr.g1) * cs_meas;
-                rc = cs_encode_batch_gops(x, e->ws_frames, 1, T, gr.g0, gr.g1, x->ws_out + o0, s_run);
-            }
+            const size_t per_cs = (size_t)x->geo.nblk * x->geo.M;   // measurements per CS frame
+            uint8_t* const ws = reinterpret_cast<uint8_t*>(x->ws_out);
+            uint8_t* const meas_dev = ws + c0 * per_cs * elem;
+            float* const sc_dev = reinterpret_cast<float*>(ws + sc_off[k]) + c0 * sc_per_cs[k];
+            const uint8_t* const fr = e->ws_frames + f0 * frame_bytes;
+            rc = q16 ? cs_encode_batch_q16(x, fr, sub_seq, sub_T, granularity, reinterpret_cast<int16_t*>(meas_dev), sc_dev, s_run)
+                     : cs_encode_batch(x, fr, sub_seq, sub_T, reinterpret_cast<float*>(meas_dev), s_run);
             if (rc != CS_OK) break;
             cudaEventRecord(ev[1 + k], s_run);
             cudaStreamWaitEvent(s_out, ev[1 + k], 0);
-            if (o1 > o0) {
-                err = cudaMemcpyAsync(outs_host[k] + o0, x->ws_out + o0, (o1 - o0) * sizeof(float),
+            err = cudaMemcpyAsync(reinterpret_cast<uint8_t*>(outs_host[k]) + c0 * per_cs * elem, meas_dev,
+                                  (c1 - c0) * per_cs * elem, cudaMemcpyDeviceToHost, s_out);
+            if (err == cudaSuccess && q16)
+                err = cudaMemcpyAsync(scales_host[k] + c0 * sc_per_cs[k], sc_dev, (c1 - c0) * sc_per_cs[k] * sizeof(float),
                                       cudaMemcpyDeviceToHost, s_out);
-                if (err != cudaSuccess) rc = cuda_fail(err, "D2H");
-            }
+            if (err != cudaSuccess) rc = cuda_fail(err, "D2H");
         }
     }
     cudaError_t e1 = cudaStreamSynchronize(s_in), e2 = cudaStreamSynchronize(s_run), e3 = cudaStreamSynchronize(s_out);
@@ -1101,9 +1146,36 @@ int cs_encode_batch_host_multi(cs_encoder* const* encs, int n_enc, const uint8_t
     return CS_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+int cs_encode_batch_host_multi(cs_encoder* const* encs, int n_enc, const uint8_t* frames_host, int n_seq, int T,
+                               float* const* outs_host) {
+    csenc::host::NvtxScope nvtx_scope("cs_encode_batch_host_multi");
+    std::vector<void*> outs(outs_host ? n_enc : 0);
+    for (size_t k = 0; k < outs.size(); ++k) outs[k] = outs_host[k];
+    return host_pipeline(encs, n_enc, frames_host, n_seq, T, -1, outs_host ? outs.data() : nullptr, nullptr);
+}
+
 int cs_encode_batch_host(cs_encoder* e, const uint8_t* frames_host, int n_seq, int T, float* out_host) {
     csenc::host::NvtxScope nvtx_scope("cs_encode_batch_host");
     return cs_encode_batch_host_multi(&e, 1, frames_host, n_seq, T, &out_host);
+}
+
+int cs_encode_batch_host_multi_q16(cs_encoder* const* encs, int n_enc, const uint8_t* frames_host, int n_seq, int T,
+                                   int granularity, int16_t* const* codes_host, float* const* scales_host) {
+    csenc::host::NvtxScope nvtx_scope("cs_encode_batch_host_multi_q16");
+    if (granularity < 0) return fail(CS_ERR_ARG, "bad granularity");
+    std::vector<void*> outs(codes_host && n_enc > 0 ? n_enc : 0);
+    for (size_t k = 0; k < outs.size(); ++k) outs[k] = codes_host[k];
+    return host_pipeline(encs, n_enc, frames_host, n_seq, T, granularity, codes_host ? outs.data() : nullptr,
+                         scales_host);
+}
+
+int cs_encode_batch_host_q16(cs_encoder* e, const uint8_t* frames_host, int n_seq, int T, int granularity,
+                             int16_t* codes_host, float* scales_host) {
+    return cs_encode_batch_host_multi_q16(&e, 1, frames_host, n_seq, T, granularity, &codes_host, &scales_host);
 }
 
 }  // extern "C"

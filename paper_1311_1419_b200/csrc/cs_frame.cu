@@ -259,6 +259,7 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     if (!frames || !y) return fail(CS_ERR_ARG, "NULL buffer");
     if (!aligned16(frames) || !aligned16(y)) return fail(CS_ERR_ARG, "buffers must be 16-byte aligned");
     if ((long long)n_seq * T > 0x7FFFFFFFLL) return fail(CS_ERR_UNSUPPORTED, "too many frames");
+    if (int rc = check_device(f->device)) return rc;
     const cudaStream_t st = (cudaStream_t)stream;
     if (env_int("CSENC_FRAME_2SM", 0) == 1) {   // K4b: CTA pairs, 2-SM MMA (opt-in: measured slower, DESIGN 6d)
         const int rc = encode_2sm(f, frames, n_seq, T, y, st);

@@ -28,6 +28,22 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 float half_bits_to_float(uint16_t h);
 int env_int(const char* name, int dflt);   // tuning / debug knobs (CSENC_*)
 
+// Device-buffer calls launch on the calling thread's current device: it must be the device the
+// object was created on (Phi, workspaces and kernel attributes live there).  CS_ERR_ARG otherwise.
+int check_device(int device);
+// Host-buffer calls (synchronous) switch to the object's device for their duration and restore the
+// caller's current device afterwards.
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = false;
+    explicit DeviceGuard(int device) {
+        if (cudaGetDevice(&prev) == cudaSuccess) ok = prev == device || cudaSetDevice(device) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        if (ok && prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 // NVTX range around an ABI call (profiling: ncu --nvtx / nsys), when CSENC_NVTX=1 (read once);
 // nvtx3 is header-only: no extra link dependency, a no-op without an attached tool
 bool nvtx_enabled();
@@ -89,11 +105,12 @@ struct cs_encoder {
     std::mutex ws_mu;  // host-path workspace
     // host-path workspace
     uint8_t* ws_frames = nullptr;
-    float* ws_out = nullptr;
+    void* ws_out = nullptr;           // measurements (fp32 or int16 codes) + scales
     size_t ws_frames_bytes = 0, ws_out_bytes = 0;
     cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
     std::vector<csenc::host::Plan> candidates;  // planner's ranked plans (autotune)
     int chained_plan = -1;         // best KEY_STREAMED candidate (previous-frame reference), -1 = none
+    int row_plan = -1;             // best candidate with <= kRowSlots block rows per tile (CS_Q16_ROW), -1 = none
     int frame1_plan = -1;          // f1 single-pass plan: D ring >= 2 (look-back lag >= 1), tiles <= SMs; -1 = none
     csenc::host::Plan frame1{};                 // that candidate with the D ring as deep as TMEM allows (<= 8)
     void* phis_dev = nullptr;      // per-GOP Phi copies (arranged like phi_dev), n_phis of phi_bytes

@@ -41,6 +41,7 @@ int cs_key_codec(cs_encoder* e, const uint8_t* frames, int n_seq, int T, const i
     if (!frames || !keys || !qsteps) return fail(CS_ERR_ARG, "NULL buffer");
     if (!aligned16(frames) || !aligned16(keys) || (coef && !aligned16(coef)))
         return fail(CS_ERR_ARG, "buffers must be 16-byte aligned");
+    if (int rc = check_device(e->device)) return rc;
     const Geometry& g = e->geo;
     csenc::kc::KCParams kp;
     std::memset(&kp, 0, sizeof(kp));

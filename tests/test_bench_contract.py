@@ -56,6 +56,26 @@ def test_device_arm_contract():
     assert d["gpu_launches"] == 3 * 4
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0
+    assert d["parity"]["ok"] is True and d["parity"]["n"] == 4 * 400
+    for m in d["per_M"].values():
+        assert m["ms_mean_l2clean"] > 0
+
+
+def test_self_launch_n_ranks():
+    """--gpus N without torchrun re-runs bench.py under torch.distributed.run with N ranks; the
+    launcher check (gloo, no GPU) proves every rank joined and rank 0 reports n_gpus == N."""
+    d = run_bench("--gpus", "2", "--launcher-check", timeout=300)
+    assert d["n_gpus"] == 2 and d["max_ms_over_ranks"] == 2.0 and d["streams"] == [0, 1]
+
+
+@pytest.mark.gpu
+def test_multi_gpu_bench():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    d = run_bench("--gpus", "2", "--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu-baseline", "--M", "16",
+                  "--tune-candidates", "2")
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["parity"]["ok"] is True
 
 
 @pytest.mark.gpu
@@ -67,3 +87,17 @@ def test_device_arm_variants(args, bound):
         assert k in d, k
     r = d["roofline"]
     assert r["bound"] == bound and 0 < r["frac"] < 1.5 and d["gpu_launches"] > 0
+    if "parity" in d and d["parity"]["ok"] is not None:
+        assert d["parity"]["ok"] is True, d["parity"]
+
+
+@pytest.mark.gpu
+def test_device_arm_q16_e2e():
+    """--output q16row: the host-buffer e2e goes through cs_encode_batch_host_multi_q16 and copies
+    back int16 codes + per-row fp32 scales."""
+    d = run_bench("--output", "q16row", "--steps", "2", "--warmup", "3", "--e2e-steps", "1", "--no-cpu-baseline",
+                  "--tune-candidates", "2")
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] == 240 * 1920 * 1080
+    assert e["d2h_bytes_per_step"] == 2 * 210 * 8160 * (16 + 32 + 64 + 128) + 4 * 4 * 210 * 68
+    assert d["parity"]["ok"] is True

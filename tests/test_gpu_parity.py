@@ -327,7 +327,7 @@ def test_host_multi_encoder_path():
         torch.cuda.synchronize()
         assert np.array_equal(o, ref.cpu().numpy())
     other = P.Encoder(cfg.W, cfg.H, cfg.G + 1, 16, 16, synth.phi_from_seed(1, 16, 256))
-    with pytest.raises(P.CSError):
+    with pytest.raises(ValueError):
         P.encode_batch_host_multi([encs[0], other], frames)
     with pytest.raises(P.CSError):
         P.encode_batch_host_multi([encs[0], encs[0]], frames)
