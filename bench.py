@@ -194,12 +194,11 @@ def l2_clean_times(launch, n_launch, stream, dev, reps):
     import torch
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     buf = torch.ones(4 * l2 // 4, dtype=torch.int32, device=dev)
-    sink = torch.empty((), dtype=torch.int64, device=dev)
     out = []
     for i in range(n_launch):
         evs = []
         for _ in range(reps):
-            torch.sum(buf, out=sink)
+            buf.sum()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             launch(i)
@@ -247,7 +246,7 @@ def timed_output_parity(cfg, Ms, phis, frames_h, results, gran, n_samples=400, s
         n += y.size
         worst = max(worst, float(rel.max()))
     key = "max_rel" if gran is None else "max_err_over_bound"
-    return {"n": n, "n_bad": n_bad, key: worst, "ok": n_bad == 0,
+    return {"entries": n_samples * len(Ms), "values": n, "n_bad": n_bad, key: worst, "ok": n_bad == 0,
             "how": f"{n_samples} sampled (CS frame, block) entries x M of the timed outputs vs oracle.measure_entries"}
 
 

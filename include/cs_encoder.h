@@ -89,12 +89,11 @@ typedef struct cs_plan_info {
  *   phi_fp16: HOST pointer, M*B*B IEEE fp16 bit patterns, row-major [M][B*B]; copied.
  *   *out    : receives the encoder; left NULL on failure.
  * Validation: W,H >= 1; gop >= 1; B in {8,16,32} (else CS_ERR_UNSUPPORTED);
- * 1 <= M <= min(B*B, 256); W % 16 == 0 (TMA row pitch) else CS_ERR_UNSUPPORTED; Phi is kept
- * in shared memory, so Mpad*B*B*2 <= 160 KB (Mpad = M rounded up to 16; B = 32 => M <= 80) else
- * CS_ERR_UNSUPPORTED;
- * Phi entries finite with |Phi| <= 2048 else CS_ERR_PHI.  Argument validation
+ * 1 <= M <= min(B*B, 256); W % 16 == 0 (TMA row pitch) else CS_ERR_UNSUPPORTED; Phi entries finite with |Phi| <= 2048 else CS_ERR_PHI.  Argument validation
  * happens before any CUDA call.  Allocates the device copy of Phi on the current
- * device. */
+ * device.  Phi stays resident in shared memory when it fits beside the ring (Mpad*B*B*2 bytes,
+ * Mpad = M rounded up to 16); otherwise (B = 32 with large M) the planner streams its K-slices with
+ * the frame strips; CS_ERR_UNSUPPORTED only if no tiling fits at all. */
 int cs_encoder_create(int W, int H, int gop, int B, int M, const uint16_t* phi_fp16, cs_encoder** out);
 
 /* Free the encoder and its device memory.  NULL-safe.  The caller must have

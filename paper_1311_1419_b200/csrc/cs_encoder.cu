@@ -24,8 +24,6 @@ using csenc::KParams;
 namespace csenc {
 namespace host {
 
-constexpr long kMaxPhiBytes = 160 * 1024;  // Phi is SMEM-resident for the whole kernel
-
 // key_mode: 0 = key strip streamed with every item, 1 = resident in SMEM (double-buffered),
 //           2 = in converter registers (arrives once per unit through a ring slot)
 bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem_limit, Plan& p, int phi_stream = 0) {
@@ -238,11 +236,6 @@ int validate(int W, int H, int gop, int B, int M, const uint16_t* phi) {
     if (M > B * B) return fail(CS_ERR_ARG, "M must be <= N = B*B");
     if (M > 256) return fail(CS_ERR_UNSUPPORTED, "M must be <= 256 (UMMA N limit)");
     if (W % 16 != 0) return fail(CS_ERR_UNSUPPORTED, "W must be a multiple of 16 (16-byte aligned bulk-copy rows)");
-    {
-        const long mpad = std::max(16, (M + 15) / 16 * 16);
-        if (mpad * B * B * 2 > kMaxPhiBytes)
-            return fail(CS_ERR_UNSUPPORTED, "Phi (Mpad*B*B fp16) must fit in 160 KB of shared memory (B=32: M <= 80)");
-    }
     if ((long long)W * H > (1LL << 31)) return fail(CS_ERR_UNSUPPORTED, "frame too large");
     if (phi) {
         for (long i = 0; i < (long)M * B * B; ++i) {

@@ -44,7 +44,8 @@ def test_version_and_error_string():
     ((176, 144, 4, 16, 257), P.CS_ERR_ARG),          # M > N
     ((176, 144, 4, 16, 0), P.CS_ERR_ARG),
     ((180, 144, 4, 16, 64), P.CS_ERR_UNSUPPORTED),   # W % 16
-    ((640, 480, 16, 32, 96), P.CS_ERR_UNSUPPORTED),  # Phi > 160 KB of SMEM
+    ((640, 480, 16, 32, 96), P.CS_OK),               # Phi > 160 KB: streamed in K-slices
+    ((640, 480, 16, 32, 256), P.CS_OK),
     ((640, 480, 16, 32, 80), P.CS_OK),
     ((16, 16, 1, 16, 256), P.CS_OK),                 # lossless M = N
 ])
@@ -96,7 +97,8 @@ def test_plans_fit_b200_limits():
             assert p["folds"] * p["lanes"] >= p["tile_block_rows"] * -(-cfg.W // cfg.B)
             assert p["lanes"] <= 128
     for args in [(16, 1, 2, 16, 16), (48, 40, 3, 32, 5), (2048, 8, 2, 8, 64), (3840, 2160, 8, 16, 128),
-                 (64, 64, 2, 32, 80), (16, 16, 2, 16, 256), (3840, 2160, 8, 8, 4)]:
+                 (64, 64, 2, 32, 80), (16, 16, 2, 16, 256), (3840, 2160, 8, 8, 4), (640, 480, 16, 32, 96),
+                 (640, 480, 16, 32, 128), (640, 480, 16, 32, 256), (96, 64, 3, 32, 256), (1920, 1080, 8, 32, 192)]:
         p = P.plan_cfg(*args)
         assert p["smem_bytes"] <= 232448 and p["tmem_cols"] <= 512
 

@@ -56,7 +56,7 @@ def test_device_arm_contract():
     assert d["gpu_launches"] == 3 * 4
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0
-    assert d["parity"]["ok"] is True and d["parity"]["n"] == 4 * 400
+    assert d["parity"]["ok"] is True and d["parity"]["entries"] == 4 * 400
     for m in d["per_M"].values():
         assert m["ms_mean_l2clean"] > 0
 

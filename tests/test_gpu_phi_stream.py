@@ -75,3 +75,40 @@ def test_phi_stream_gop_phis_and_q16():
     torch.cuda.synchronize()
     assert torch.equal(c0, c1) and torch.equal(s0, s1)
     assert np.isfinite(s0.cpu().numpy()).all()
+
+
+@pytest.mark.parametrize("W,H,T,G,M", [(640, 480, 5, 4, 96), (640, 100, 6, 3, 128), (160, 72, 7, 4, 256),
+                                       (96, 40, 3, 3, 200)])
+def test_b32_large_m(W, H, T, G, M):
+    """B = 32 with M up to 256 (M <= min(N, 256)): Phi (up to 512 KB) no longer fits
+    shared memory, so every plan streams its K-slices; parity with the oracle for fp32 (every candidate
+    plan bitwise equal), the 16-bit row / frame codes and the adjoint."""
+    cfg = synth.CONFIGS["C3"].with_(W=W, H=H, T=T, G=G, Ms=(M,), S=2)
+    frames = synth.gen_video(cfg)
+    fd = torch.from_numpy(frames).cuda()
+    phi = synth.phi_from_seed(synth.phi_seed() + M, M, 1024)
+    enc = P.Encoder(W, H, G, 32, M, phi)
+    assert enc.plan()["phi_stream"] == 1
+    out = enc.encode_batch(fd)
+    torch.cuda.synchronize()
+    y, S = oracle.encode(frames, phi, G, 32)
+    ok, stats = oracle.check_tolerance(out.cpu().numpy(), y, S)
+    assert ok, stats
+    for i in range(min(6, enc.num_candidates())):
+        enc.set_candidate(i)
+        assert torch.equal(enc.encode_batch(fd), out), enc.plan()
+    enc.set_candidate(0)
+    for gran in (P.Encoder.Q16_FRAME, P.Encoder.Q16_ROW):
+        codes, scales = enc.encode_batch_q16(fd, gran)
+        torch.cuda.synchronize()
+        c = codes.cpu().numpy().astype(np.float64)
+        sc = scales.cpu().numpy().astype(np.float64)
+        sc = np.repeat(sc, enc.nbx, axis=1)[:, :, None] if gran == P.Encoder.Q16_ROW else sc[:, None, None]
+        assert np.all(np.abs(c * sc - y) <= sc * (0.5 + 2.0 ** -21) + 1e-5 * S + 2.0 ** -22 * np.abs(y))
+    if M % 4 == 0:
+        x = enc.adjoint(out)
+        torch.cuda.synchronize()
+        yv = out.cpu().numpy().astype(np.float64)
+        xo = oracle.adjoint(yv, phi, W, H, 32)
+        Sx = oracle.adjoint_tolerance_scale(yv, phi, W, H, 32)
+        assert np.all(np.abs(x.cpu().numpy() - xo) <= 1e-5 * Sx)
