@@ -32,7 +32,10 @@ float half_bits_to_float(uint16_t h) {
 }
 
 bool nvtx_enabled() {
-    static const bool on = env_int("CSENC_NVTX", 0) != 0;
+    static const bool on = [] {
+        const char* v = std::getenv("CSENC_NVTX");
+        return v != nullptr && std::atoi(v) != 0;
+    }();
     return on;
 }
 
@@ -47,8 +50,13 @@ int check_device(int device) {
 }
 
 int env_int(const char* name, int dflt) {
+#if CSENC_TUNING
     const char* v = std::getenv(name);
     return v ? std::atoi(v) : dflt;
+#else
+    (void)name;   // product build: every tuning / debug knob keeps its default
+    return dflt;
+#endif
 }
 
 PFN_encodeTiled get_encode_tiled() {

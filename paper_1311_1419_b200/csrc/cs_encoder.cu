@@ -25,14 +25,22 @@ namespace csenc {
 namespace host {
 
 // key_mode: 0 = key strip streamed with every item, 1 = resident in SMEM (double-buffered),
-//           2 = in converter registers (arrives once per unit through a ring slot)
-bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem_limit, Plan& p, int phi_stream = 0) {
+//           2 = in converter registers (arrives once per unit through a ring slot),
+//           3 = chunk-outer order (KEY_CHUNK): per K-chunk the key chunk arrives once through a ring
+//               slot into converter registers and every CS frame of the unit follows against it, each
+//               into its own TMEM accumulator (unit frames <= n_dbuf); Phi resident, or (phi_stream)
+//               its K-slice loaded once per chunk into a double-buffered region.
+// a_pref (key_mode 3 only): TMEM A-operand buffers; the rest of TMEM goes to accumulators.
+bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem_limit, Plan& p, int phi_stream = 0,
+              int a_pref = 2) {
     const bool key_res = key_mode == 1;
+    const bool key_chunk = key_mode == 3;
     p = Plan();
     const int words = g.B / 2;          // fp16x2 columns per pixel row
     const int rows_per_st = 32 / words;
     if (g.B % chunk_rows != 0 || chunk_rows % rows_per_st != 0) return false;
     if ((chunk_rows * g.B) % 16 != 0) return false;
+    if (key_chunk && g.B != 32) return false;   // instantiated for B = 32 (the config it exists for: C3)
     const int tile_blocks = T_r * g.nbx;
     p.T_r = T_r;
     p.F = cdiv(tile_blocks, 128);
@@ -43,12 +51,18 @@ bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem
     p.n_chunks = g.B / chunk_rows;
     p.chunk_k = chunk_rows * g.B;
     p.a_cols = p.F * p.chunk_k / 2;
+    p.d_cols = p.F * g.Mpad;
     // TMEM rings: A buffers (converter -> MMA) and accumulators (MMA -> epilogue).  Deeper rings
     // decouple the converter and epilogue latencies (measured: with 2+2 a slow converter OR a
     // slow epilogue stalls the chain).  Prefer (3+, 3+), then (2, 2).  (Dependent MMAs into one
     // accumulator issue back to back -- tools/mma_microbench*.cu -- so no split-K chains.)
-    {
-        const int dc = p.F * g.Mpad;
+    // KEY_CHUNK: a_pref A buffers and as many accumulators as fit (they bound the unit's frames).
+    if (key_chunk) {
+        p.n_abuf = a_pref;
+        p.n_dbuf = std::min(csenc::kMaxTmemBufs, ((int)csenc::kTmemCols - a_pref * p.a_cols) / p.d_cols);
+        if (p.n_dbuf < 2) return false;
+    } else {
+        const int dc = p.d_cols;
         const int cands[][2] = {{4, 4}, {4, 3}, {3, 4}, {3, 3}, {4, 2}, {3, 2}, {2, 3}, {2, 2}, {2, 1}, {1, 1}};
         p.n_abuf = 0;
         for (auto& c : cands)
@@ -58,6 +72,7 @@ bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem
                 break;
             }
         if (p.n_abuf == 0) return false;
+#if CSENC_TUNING
         if (const char* e = std::getenv("CSENC_TMEM_BUFS")) {  // experiment knob "A,D"
             int a = 0, d = 0;
             if (std::sscanf(e, "%d,%d", &a, &d) == 2 && a >= 1 && d >= 1 && a <= 4 && d <= 4 &&
@@ -66,8 +81,8 @@ bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem
                 p.n_dbuf = d;
             }
         }
+#endif
     }
-    p.d_cols = p.F * g.Mpad;
     p.tmem_cols = p.n_abuf * p.a_cols + p.n_dbuf * p.d_cols;
     if (p.tmem_cols > (int)csenc::kTmemCols) return false;
     const double ring_q = std::min(p.n_abuf, 3) * std::min(p.n_dbuf, 3) / 9.0;  // prefer 3+3
@@ -85,22 +100,29 @@ bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem
     p.stage_cs_bytes = (uint32_t)p.pieces * p.piece_bytes;
     p.key_resident = key_res ? 1 : 0;
     p.key_regs = key_mode == 2 ? 1 : 0;
-    if (p.key_regs) {
+    p.key_chunk = key_chunk ? 1 : 0;
+    const int groups_per_fold = chunk_rows / rows_per_st;
+    if (p.key_regs || key_chunk) {
         // each converter warpgroup holds <= 2 row groups (16 u8 words each) of the key
-        const int groups_per_fold = chunk_rows / rows_per_st;
-        if (g.B == 32 || p.n_chunks != 1 || p.F * groups_per_fold > 4) return false;
+        if (p.F * groups_per_fold > 4) return false;
+        if (p.key_regs && (g.B == 32 || p.n_chunks != 1)) return false;
     }
     p.key_bytes = key_res ? (uint32_t)p.n_chunks * p.stage_cs_bytes : 0;
-    p.stage_bytes = (key_res || p.key_regs) ? p.stage_cs_bytes : 2 * p.stage_cs_bytes;
+    p.stage_bytes = (key_res || p.key_regs || key_chunk) ? p.stage_cs_bytes : 2 * p.stage_cs_bytes;
     uint32_t phi_bytes = (uint32_t)g.Mpad * (uint32_t)g.N * 2u;
     if (phi_stream) {
-        // Phi's K-slice for the chunk rides in every stage (the canonical layout keeps a chunk's
-        // chunk_k / 8 K-groups contiguous); nothing of Phi stays resident
-        if (p.n_chunks < 2 || p.key_regs || key_res) return false;   // KEY_STREAMED plans only
+        if (p.n_chunks < 2 || p.key_regs || key_res) return false;
         p.phi_stream = 1;
         p.phi_slice_bytes = phi_bytes / (uint32_t)p.n_chunks;
-        p.stage_phi_off = align_up(p.stage_bytes, 128);
-        p.stage_bytes = align_up(p.stage_phi_off + p.phi_slice_bytes, 128);
+        if (key_chunk) {
+            // the chunk's K-slice of Phi: once per (unit, chunk) into a double-buffered region (at off_key)
+            p.key_bytes = align_up(p.phi_slice_bytes, 1024);
+        } else {
+            // Phi's K-slice for the chunk rides in every stage (the canonical layout keeps a chunk's
+            // chunk_k / 8 K-groups contiguous); nothing of Phi stays resident
+            p.stage_phi_off = align_up(p.stage_bytes, 128);
+            p.stage_bytes = align_up(p.stage_phi_off + p.phi_slice_bytes, 128);
+        }
         phi_bytes = 0;
     }
     p.off_tab = 1024;  // barriers live in the first KB, then the converter offset table (8 KB)
@@ -111,25 +133,30 @@ bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem
     const long avail = (long)smem_limit - 1024 /*alignment slack*/ - (long)p.off_stage;
     if (avail < (long)p.stage_bytes * 2) return false;
     p.n_stages = (int)std::min<long>(csenc::kMaxStages, avail / p.stage_bytes);
+    if (key_chunk && p.n_stages < 3) return false;   // key item + at least two frames in flight
     p.smem_bytes = p.off_stage + (uint32_t)p.n_stages * p.stage_bytes + 1024;
-    // L2 prefetch of future strips: measured no benefit once the SMEM ring holds >= ~100 KB
-    // (tools/sweep.sh); kept as a knob (CSENC_PREFETCH), off by default.
-    p.prefetch_items = 0;  // (knob removed from the kernel; kept in the plan info as 0)
+    p.prefetch_items = 0;  // (L2 prefetch of future strips measured no benefit; kept in the plan info as 0)
     // Score = modelled pixels per cycle of one SM, calibrated on B200 measurements
     // (tools/trace_timeline.py, tools/sweep*.sh): an item costs a fixed ~700
     // cycles of pipeline handoffs plus ~150 per bulk copy, overlapped with the slowest of
     //   converters ~350 cycles per row group per warpgroup, loads at ~32 B/cycle,
     //   MMA issue ~48 cycles per tcgen05.mma.
-    const int groups_per_fold = chunk_rows / rows_per_st;
     const int groups_per_wg = (p.F * groups_per_fold + 1) / 2;
     const double px = (double)tile_blocks * p.chunk_k;
     const double item_bytes = (double)p.stage_bytes;
-    const int copies = p.pieces * ((key_res || p.key_regs) ? 1 : 2) + p.phi_stream;
+    const bool box = p.pieces > 1 && !p.key_regs && !key_res && g.H % g.B == 0;   // 4-D TMA strips
+    const int strip_copies = box ? 1 : p.pieces;
+    const int copies = strip_copies * ((key_res || p.key_regs || key_chunk) ? 1 : 2) + (key_chunk ? 0 : p.phi_stream);
     const double conv = 350.0 * groups_per_wg;
     const double load = item_bytes / 32.0;
     const double mma = (double)(p.chunk_k / 16) * p.F * std::max(48.0, g.Mpad / 2.0);
     const double cycles = 700.0 + 150.0 * copies + std::max({conv, load, mma});
     double s = px / cycles;
+    if (key_chunk) {   // one key item per chunk, amortised over the unit's frames (<= n_dbuf of G-1)
+        const double U = std::max(1, std::min(p.n_dbuf, g.G - 1));
+        const double key_item = 700.0 + 150.0 * strip_copies + (double)p.stage_cs_bytes / 32.0;
+        s = px * U / (U * cycles + key_item);
+    }
     // Measured (tools/sweep10.sh): with >= 3 ring slots the double-buffered SMEM key is ~5% faster
     // than the register key (whose load sits in the ring at every unit start); the register key
     // wins when a resident key would leave < 3 slots (C5).
@@ -137,7 +164,7 @@ bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem
     if (p.key_regs) s *= (g.B == 8) ? 1.05 : 0.9;
     if (p.n_stages < 3) s *= 0.85;
     if (p.n_dbuf < 2) s *= 0.8;
-    s *= 0.85 + 0.15 * ring_q;
+    if (!key_chunk) s *= 0.85 + 0.15 * ring_q;
     p.score = s;
     return true;
 }
@@ -154,17 +181,19 @@ std::vector<Plan> plan_candidates(const Geometry& g, int smem_limit) {
         if (f_tr && T_r != f_tr) continue;
         for (int cr = g.B; cr >= 1; --cr) {
             if (f_cr && cr != f_cr) continue;
-            for (int kr = 2; kr >= 0; --kr) {
+            for (int kr = 3; kr >= 0; --kr) {
                 if (f_kr >= 0 && kr != f_kr) continue;
                 for (int ps = 0; ps <= 1; ++ps) {
                     if (f_ps >= 0 && ps != f_ps) continue;
-                    Plan p;
-                    if (!try_plan(g, T_r, cr, kr, smem_limit, p, ps)) continue;
-                    if (f_st > 0 && f_st < p.n_stages) {
-                        p.smem_bytes -= (uint32_t)(p.n_stages - f_st) * p.stage_bytes;
-                        p.n_stages = f_st;
+                    for (int ap = 2; ap <= (kr == 3 ? 3 : 2); ++ap) {
+                        Plan p;
+                        if (!try_plan(g, T_r, cr, kr, smem_limit, p, ps, ap)) continue;
+                        if (f_st > 0 && f_st < p.n_stages) {
+                            p.smem_bytes -= (uint32_t)(p.n_stages - f_st) * p.stage_bytes;
+                            p.n_stages = f_st;
+                        }
+                        all.push_back(p);
                     }
-                    all.push_back(p);
                 }
             }
         }
@@ -180,31 +209,6 @@ bool make_plan(const Geometry& g, int smem_limit, Plan& best) {
     return true;
 }
 
-[[maybe_unused]] bool make_plan_scan(const Geometry& g, int smem_limit, Plan& best) {
-    best = Plan();
-    // experiment knobs (tools/sweep.sh): force a tile-row count / chunk size / key residency
-    const int f_tr = env_int("CSENC_TILE_ROWS", 0), f_cr = env_int("CSENC_CHUNK_ROWS", 0);
-    const int f_kr = env_int("CSENC_KEY_RESIDENT", -1), f_st = env_int("CSENC_STAGES", 0);
-    for (int T_r = 1; T_r <= g.nby; ++T_r) {
-        if (T_r * g.nbx > 128 * csenc::kMaxFolds) break;
-        if (f_tr && T_r != f_tr) continue;
-        for (int cr = g.B; cr >= 1; --cr) {
-            if (f_cr && cr != f_cr) continue;
-            for (int kr = 2; kr >= 0; --kr) {
-                if (f_kr >= 0 && kr != f_kr) continue;
-                Plan p;
-                if (!try_plan(g, T_r, cr, kr, smem_limit, p)) continue;
-                if (f_st > 0 && f_st < p.n_stages) {
-                    p.smem_bytes -= (uint32_t)(p.n_stages - f_st) * p.stage_bytes;
-                    p.n_stages = f_st;
-                }
-                if (p.score > best.score + 1e-9) best = p;
-            }
-        }
-    }
-    return best.score > 0;
-}
-
 struct WorkSplit {
     int n_splits, cs_per_unit, n_units;
 };
@@ -214,10 +218,12 @@ WorkSplit choose_split(const Geometry& g, const Plan& p, int n_seq, int n_gops_s
     WorkSplit best{1, std::max(1, g.G - 1), (int)base};
     if (g.G <= 1) return best;
     double best_cost = 1e300;
-    const double key_cost = (p.key_resident || p.key_regs) ? 1.0 : 0.0;
+    const double key_cost = (p.key_resident || p.key_regs || p.key_chunk) ? 1.0 : 0.0;
+    if (p.key_chunk) best = WorkSplit{cdiv(g.G - 1, p.n_dbuf), p.n_dbuf, (int)(base * cdiv(g.G - 1, p.n_dbuf))};
     for (int ns = 1; ns <= g.G - 1; ++ns) {
         int cpu = cdiv(g.G - 1, ns);
         if (ns > 1 && cdiv(g.G - 1, cpu) != ns) continue;  // identical to a smaller ns
+        if (p.key_chunk && cpu > p.n_dbuf) continue;        // a unit's frames each own an accumulator
         long units = base * ns;
         if (units > (1L << 30)) break;
         double rounds = std::ceil((double)units / sms);
@@ -403,8 +409,9 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     int grid = std::max(1, std::min(e->sms, kp.n_units));
     if (q.gop_rounds) grid = std::max(1, std::min(e->sms / pl.n_tiles * pl.n_tiles, kp.n_units));
     cudaError_t err;
-    const int km = pl.key_regs ? csenc::KEY_REGS : (pl.key_resident ? csenc::KEY_RESIDENT : csenc::KEY_STREAMED);
-    // KEY_STREAMED kernels take KParamsTS (with the strip tensor map), the others KParams
+    const int km = pl.key_chunk ? csenc::KEY_CHUNK
+                   : pl.key_regs ? csenc::KEY_REGS : (pl.key_resident ? csenc::KEY_RESIDENT : csenc::KEY_STREAMED);
+    // KEY_STREAMED / KEY_CHUNK kernels take KParamsTS (with the strip tensor map), the others KParams
     auto go = [&](auto kern) {
         auto run = [&](auto& prm) {
             if (q.gop_rounds) {   // the look-back needs every CTA resident: cooperative launch guarantees it
@@ -437,7 +444,7 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     switch ((g.B * 4 + km) * 8 + epi) {
         CSENC_CASE(8, csenc::KEY_STREAMED) CSENC_CASE(8, csenc::KEY_RESIDENT) CSENC_CASE(8, csenc::KEY_REGS)
         CSENC_CASE(16, csenc::KEY_STREAMED) CSENC_CASE(16, csenc::KEY_RESIDENT) CSENC_CASE(16, csenc::KEY_REGS)
-        CSENC_CASE(32, csenc::KEY_STREAMED) CSENC_CASE(32, csenc::KEY_RESIDENT)
+        CSENC_CASE(32, csenc::KEY_STREAMED) CSENC_CASE(32, csenc::KEY_RESIDENT) CSENC_CASE(32, csenc::KEY_CHUNK)
         default: return fail(CS_ERR_UNSUPPORTED, "no kernel instantiation for this plan");
     }
 #undef CSENC_CASE
@@ -473,7 +480,7 @@ cudaError_t set_smem_attr_all(int bytes) {
     if (r != cudaSuccess) e = r;
     CSENC_ATTR(8, csenc::KEY_STREAMED) CSENC_ATTR(8, csenc::KEY_RESIDENT) CSENC_ATTR(8, csenc::KEY_REGS)
     CSENC_ATTR(16, csenc::KEY_STREAMED) CSENC_ATTR(16, csenc::KEY_RESIDENT) CSENC_ATTR(16, csenc::KEY_REGS)
-    CSENC_ATTR(32, csenc::KEY_STREAMED) CSENC_ATTR(32, csenc::KEY_RESIDENT)
+    CSENC_ATTR(32, csenc::KEY_STREAMED) CSENC_ATTR(32, csenc::KEY_RESIDENT) CSENC_ATTR(32, csenc::KEY_CHUNK)
 #undef CSENC_ATTR
     r = adjoint_set_smem_attr(bytes);
     if (r != cudaSuccess) e = r;
@@ -599,7 +606,7 @@ int cs_encoder_create(int W, int H, int gop, int B, int M, const uint16_t* phi_f
     cudaDeviceGetAttribute(&e->smem_limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device);
     e->candidates = plan_candidates(e->geo, e->smem_limit);
     for (size_t i = 0; i < e->candidates.size(); ++i)
-        if (!e->candidates[i].key_resident && !e->candidates[i].key_regs) {
+        if (!e->candidates[i].key_resident && !e->candidates[i].key_regs && !e->candidates[i].key_chunk) {
             e->chained_plan = (int)i;
             break;
         }
@@ -614,6 +621,7 @@ int cs_encoder_create(int W, int H, int gop, int B, int M, const uint16_t* phi_f
     // round (n_tiles <= SMs)
     for (size_t i = 0; i < e->candidates.size(); ++i) {
         Plan c = e->candidates[i];
+        if (c.key_chunk) continue;   // whole-GOP units: more frames than a KEY_CHUNK unit may hold
         // the look-back holds `lag` accumulators: the D ring as deep as TMEM allows, lag = ring - 1
         c.n_dbuf = std::min(csenc::kMaxTmemBufs, ((int)csenc::kTmemCols - c.n_abuf * c.a_cols) / c.d_cols);
         if (c.n_dbuf < 2 || c.n_tiles > e->sms) continue;
@@ -690,7 +698,7 @@ static void fill_info(const Plan& p, const Geometry& g, int sms, cs_plan_info* i
     info->lanes = p.L;
     info->chunk_rows = p.chunk_rows;
     info->stages = p.n_stages;
-    info->key_resident = p.key_regs ? 2 : p.key_resident;
+    info->key_resident = p.key_chunk ? 3 : p.key_regs ? 2 : p.key_resident;
     info->box_w = g.W;  /* strips are full-width rows */
     info->prefetch_items = p.prefetch_items;
     info->a_bufs = p.n_abuf;

@@ -26,7 +26,12 @@ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 float half_bits_to_float(uint16_t h);
-int env_int(const char* name, int dflt);   // tuning / debug knobs (CSENC_*)
+// Tuning / debug knobs (CSENC_* environment variables): read only in CSENC_TUNING=1 builds
+// (tools/, libcsenc_checks.so); the product library always uses the defaults.
+int env_int(const char* name, int dflt);
+#ifndef CSENC_TUNING
+#define CSENC_TUNING 0
+#endif
 
 // Device-buffer calls launch on the calling thread's current device: it must be the device the
 // object was created on (Phi, workspaces and kernel attributes live there).  CS_ERR_ARG otherwise.
@@ -77,7 +82,7 @@ struct Plan {
     int chunk_rows = 0, n_chunks = 0, chunk_k = 0;
     int pieces = 0, piece_rows = 0, single_piece = 0;
     uint32_t piece_bytes = 0, stage_cs_bytes = 0, stage_bytes = 0, key_bytes = 0;
-    int key_resident = 0, key_regs = 0, n_stages = 0, prefetch_items = 0;
+    int key_resident = 0, key_regs = 0, key_chunk = 0, n_stages = 0, prefetch_items = 0;
     int phi_stream = 0;                       // Phi K-slices ride in the stages instead of staying resident
     uint32_t phi_slice_bytes = 0, stage_phi_off = 0;
     uint32_t off_tab = 0, off_epi = 0, off_phi = 0, off_key = 0, off_stage = 0, smem_bytes = 0;

@@ -36,6 +36,11 @@
 
 #include "ptx_sm100.cuh"
 
+// The KEY_CHUNK branches of the role loops end in `continue`, so in those instantiations the other
+// modes' loops that follow are unreachable by construction (warning 128).
+#pragma nv_diagnostic push
+#pragma nv_diag_suppress 128
+
 #ifndef CSENC_DEBUG
 #define CSENC_DEBUG 0  // 1: compile the ablation switches (KParams::dbg_*) into the kernel
 #endif
@@ -56,7 +61,7 @@ constexpr int kMaxStages = 8;
 constexpr int kMaxTmemBufs = 8;                  // TMEM A buffers / accumulators (ring depth cap)
 constexpr uint32_t kTmemCols = 512;
 
-enum KeyMode : int { KEY_STREAMED = 0, KEY_RESIDENT = 1, KEY_REGS = 2 };
+enum KeyMode : int { KEY_STREAMED = 0, KEY_RESIDENT = 1, KEY_REGS = 2, KEY_CHUNK = 3 };
 // epilogue variants (template EPI): fp32 measurements (a6), or 16-bit codes (f1)
 // One instantiation per variant keeps each kernel's code small: the four roles' loops share the SM's
 // instruction cache (measured: a 64-value register path in the shared q16 kernel cost the other
@@ -172,7 +177,7 @@ struct KParamsTS : KParams {
     alignas(64) CUtensorMap smap;
 };
 template <int KM>
-using KParamsFor = typename std::conditional<KM == KEY_STREAMED, KParamsTS, KParams>::type;
+using KParamsFor = typename std::conditional<KM == KEY_STREAMED || KM == KEY_CHUNK, KParamsTS, KParams>::type;
 
 // trace events
 enum : int {
@@ -315,6 +320,18 @@ struct RowConvK<32> {
     }
 };
 
+// KEY_CHUNK, B = 32: the residual words of one row of 32 pixels (u8 words cw[0..7], loaded earlier)
+// against the row's pre-expanded key (kx[2q], kx[2q+1] = magic2 of key word q); the right half is zero
+// when it lies beyond W.
+__device__ __forceinline__ void row32_vs_kexp(const uint32_t* cw, const uint32_t* kx, uint32_t (&w)[16], bool half2) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) ptx::residual4x(cw[q], kx[2 * q], kx[2 * q + 1], w[2 * q], w[2 * q + 1]);
+    if (!half2) {
+#pragma unroll
+        for (int i = 8; i < 16; ++i) w[i] = 0u;
+    }
+}
+
 // u8 words of one row segment of B pixels (B/4 words) from SMEM
 template <int B>
 __device__ __forceinline__ void load_row_words(uint32_t addr, uint32_t* kw) {
@@ -426,6 +443,7 @@ template <int B, int KM, int EPI>
 __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const __grid_constant__ KParamsFor<KM> p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t sbase = (ptx::smem_addr(smem_raw) + 1023u) & ~1023u;
+    const uint8_t* const smem_ptr = smem_raw + (sbase - ptx::smem_addr(smem_raw));   // sbase as a C++ pointer
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31u;
 #if CSENC_DEBUG
@@ -449,15 +467,21 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
     const uint32_t bar_phi_empty = bar_phi + 16;   // per-GOP Phi: MMAs on the current Phi done
     const uint32_t s_phi = sbase + p.off_phi;
     // Phi streaming and 4-D strip boxes only exist for multi-chunk plans, which never hold the key in
-    // registers: compiled out of the KEY_REGS instantiations (their code stays as small as before)
+    // registers: compiled out of the KEY_REGS instantiations (their code stays as small as before).
+    // KEY_STREAMED: the chunk's Phi K-slice rides in every stage (freed by the MMA's commit too);
+    // KEY_CHUNK: it is loaded once per (unit, chunk) into a double-buffered region at off_key
+    // (slice_full / slice_empty = the key_full / key_empty barriers, unused by this mode otherwise).
     const bool phi_stream = KM == KEY_STREAMED && p.phi_stream;
+    const bool phi_slices = KM == KEY_CHUNK && p.phi_stream;
     const CUtensorMap* smap = nullptr;
-    if constexpr (KM == KEY_STREAMED) smap = &p.smap;
+    if constexpr (KM == KEY_STREAMED || KM == KEY_CHUNK) smap = &p.smap;
     const uint32_t s_key = sbase + p.off_key;
     const uint32_t s_stage = sbase + p.off_stage;
     CS_CHECK(p.off_stage + (uint32_t)p.n_stages * p.stage_bytes <= p.smem_bytes);
     CS_CHECK(p.set_bytes * (KM == KEY_STREAMED ? 2u : 1u) <= p.stage_bytes);
-    CS_CHECK(KM != KEY_RESIDENT || p.off_key + 2u * p.key_bytes <= p.off_stage);
+    CS_CHECK((KM != KEY_RESIDENT && !phi_slices) || p.off_key + 2u * p.key_bytes <= p.off_stage);
+    CS_CHECK(!phi_slices || p.phi_slice_bytes <= p.key_bytes);
+    CS_CHECK(KM != KEY_CHUNK || (p.cs_per_unit <= p.n_dbuf && p.n_stages >= 3));
     CS_CHECK(p.n_abuf * p.a_cols + p.n_dbuf * p.d_cols <= (int)kTmemCols);
 
     if (threadIdx.x == 0) {
@@ -467,7 +491,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(bar_key_full + 8 * i, 1);
-            ptx::mbar_init(bar_key_empty + 8 * i, kConvWarps);
+            ptx::mbar_init(bar_key_empty + 8 * i, phi_slices ? 1 : kConvWarps);   // slice freed by the MMA's commit
         }
         for (int i = 0; i < kMaxTmemBufs; ++i) {
             ptx::mbar_init(bar_a_full + 8 * i, kConvWarps);
@@ -527,13 +551,15 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         const uint64_t pol_stream = ptx::policy_evict_first();
         const uint64_t pol_key = ptx::policy_evict_last();
         const size_t frame_bytes = (size_t)p.W * (size_t)p.H;
-        if (p.n_phis == 0 && !phi_stream) {
+        if (p.n_phis == 0 && !phi_stream && !phi_slices) {
             if (elect_one()) {
                 ptx::mbar_arrive_expect_tx(bar_phi, p.phi_bytes);
                 ptx::bulk_load(s_phi, p.phi, p.phi_bytes, bar_phi);
             }
             __syncwarp();
         }
+        int pb = 0;          // KEY_CHUNK phi_slices: slice buffer and its phase
+        uint32_t pbph = 0;
         int phi_cur = -1;
         uint32_t phi_loads = 0;
         int st = 0;
@@ -545,7 +571,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
             Unit w;
             if (!decode_unit(p, u, w)) continue;
             const uint8_t* const phi_src = reinterpret_cast<const uint8_t*>(p.n_phis > 0 ? p.phis + (size_t)(w.g % p.n_phis) * (p.phi_bytes / 2) : p.phi);
-            if (p.n_phis > 0 && !phi_stream) {   // per-GOP Phi: reload when the GOP's matrix differs from the resident one
+            if (p.n_phis > 0 && !phi_stream && !phi_slices) {   // per-GOP Phi: reload when the GOP's matrix differs from the resident one
                 const int gsel = w.g % p.n_phis;
                 if (gsel != phi_cur) {
                     if (phi_loads > 0) ptx::mbar_wait(bar_phi_empty, (phi_loads - 1u) & 1u);
@@ -587,6 +613,44 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                 __syncwarp();
                 kb ^= 1;
                 if (kb == 0) kph ^= 1u;
+            }
+            if constexpr (KM == KEY_CHUNK) {
+                // chunk-outer order: per chunk k, (Phi slice k), key chunk k, then chunk k of every
+                // CS frame of the unit -- the key chunk and the slice cross L2 -> SMEM once per unit
+                for (int k = 0; k < p.n_chunks; ++k) {
+                    if (phi_slices && !dbg_load_only) {   // (load-only ablation: no MMA frees the slices)
+                        ptx::mbar_wait(bar_key_empty + 8 * pb, pbph ^ 1u);
+                        if (elect_one()) {
+                            ptx::mbar_arrive_expect_tx(bar_key_full + 8 * pb, p.phi_slice_bytes);
+                            ptx::bulk_load(s_key + (uint32_t)pb * p.key_bytes, phi_src + (size_t)k * p.phi_slice_bytes,
+                                           p.phi_slice_bytes, bar_key_full + 8 * pb);
+                        }
+                        __syncwarp();
+                        pb ^= 1;
+                        if (pb == 0) pbph ^= 1u;
+                    }
+                    for (int c = w.c0 - 1; c < w.c1; ++c) {   // c = c0 - 1: the key chunk
+                        ptx::mbar_wait(bar_stage_empty + 8 * st, ph ^ 1u);
+                        if (lane == 0 && c >= w.c0) trace_ev(p, EV_P_EMPTY, n_items);
+                        const uint32_t dst = s_stage + (uint32_t)st * p.stage_bytes;
+                        if (elect_one()) {
+                            ptx::mbar_arrive_expect_tx(bar_stage_full + 8 * st, p.set_bytes);
+                            if (c < w.c0)
+                                load_strips<B>(p, dst, key_f, w.t, k, bar_stage_full + 8 * st, pol_key, keyf_idx, smap);
+                            else
+                                load_strips<B>(p, dst, raw_key + (size_t)(1 + c) * frame_bytes, w.t, k,
+                                               bar_stage_full + 8 * st, pol_stream, key_idx + 1 + c, smap);
+                        }
+                        __syncwarp();
+                        if (lane == 0 && c >= w.c0) trace_ev(p, EV_P_ISSUED, n_items);
+                        if (c >= w.c0) ++n_items;
+                        if (++st == p.n_stages) {
+                            st = 0;
+                            ph ^= 1u;
+                        }
+                    }
+                }
+                continue;
             }
             for (int c = w.c0; c < w.c1; ++c) {
                 const uint8_t* cs_f = raw_key + (size_t)(1 + c) * frame_bytes;
@@ -648,10 +712,13 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         // ================================================================ MMA issuer
         // The whole warp walks the schedule (warp-uniform control flow keeps every operand in
         // uniform registers); one elected lane issues the tcgen05 instructions.
-        if (p.n_phis == 0 && !phi_stream) {
+        if (p.n_phis == 0 && !phi_stream && !phi_slices) {
             ptx::mbar_wait(bar_phi, 0);
             ptx::tc_fence_after();
         }
+        int pb = 0;    // KEY_CHUNK phi_slices: slice buffer and its phase
+        uint32_t pbph = 0;
+        uint32_t d_use = 0;   // KEY_CHUNK: per accumulator slot, parity of its uses so far (bit db)
         int pst = 0;   // phi_stream: stage of the current chunk (one stage per chunk: KM 0/1)
         uint32_t pph = 0;
         int phi_cur = -1;
@@ -669,7 +736,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             Unit w;
             if (!decode_unit(p, u, w)) continue;
-            if (p.n_phis > 0 && !phi_stream) {
+            if (p.n_phis > 0 && !phi_stream && !phi_slices) {
                 const int gsel = w.g % p.n_phis;
                 if (gsel != phi_cur) {
                     // release the resident Phi once every MMA issued so far has completed, then wait
@@ -683,6 +750,65 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                     phi_cur = gsel;
                     ++phi_waits;
                 }
+            }
+            if constexpr (KM == KEY_CHUNK) {
+                // chunk-outer: frame j of the unit accumulates into slot (db + j) % n_dbuf over all
+                // chunks; its d_full is committed with its last chunk (the epilogue takes the
+                // frames in the same order as every other mode)
+                const int U = w.c1 - w.c0;
+                for (int k = 0; k < p.n_chunks; ++k) {
+                    uint64_t dk = desc0 + (uint64_t)k * desc_chunk;
+                    if (phi_slices) {
+                        ptx::mbar_wait(bar_key_full + 8 * pb, pbph);
+                        dk = ptx::smem_desc_noswizzle(s_key + (uint32_t)pb * p.key_bytes, p.lbo, p.sbo);
+                    }
+                    int dj = db;
+                    for (int j = 0; j < U; ++j) {
+                        if (k == 0) {
+                            ptx::mbar_wait(bar_d_empty + 8 * dj, ((d_use >> dj) & 1u) ^ 1u);
+                        }
+                        ptx::mbar_wait(bar_a_full + 8 * ab, aph);
+                        ptx::tc_fence_after();
+                        if (lane == 0) trace_ev(p, EV_M_AFULL, n_items);
+                        const uint32_t d_tm = tmem_base + d_col0 + (uint32_t)dj * (uint32_t)p.d_cols;
+                        const uint32_t a_tm = tmem_base + a_col0 + (uint32_t)ab * (uint32_t)p.a_cols;
+                        const uint32_t acc0 = k > 0 ? 1u : 0u;
+                        if (elect_one()) {
+                            for (int f = 0; f < p.F; ++f) {
+                                const uint32_t d_f = d_tm + (uint32_t)(f * p.Mpad);
+                                const uint32_t a_f = a_tm + (uint32_t)f * a_fold;
+                                switch (ksteps) {
+                                    case 4: issue_chunk<4>(d_f, a_f, dk, desc_step, p.idesc, acc0); break;
+                                    case 8: issue_chunk<8>(d_f, a_f, dk, desc_step, p.idesc, acc0); break;
+                                    case 16: issue_chunk<16>(d_f, a_f, dk, desc_step, p.idesc, acc0); break;
+                                    default:
+                                        for (int s2 = 0; s2 < ksteps; ++s2)
+                                            ptx::mma_f16_ts(d_f, a_f + (uint32_t)(s2 * 8), dk + (uint64_t)s2 * desc_step,
+                                                            p.idesc, (k > 0 || s2 > 0) ? 1u : 0u);
+                                }
+                            }
+                            ptx::tc_commit(bar_a_empty + 8 * ab);
+                            if (k == p.n_chunks - 1) ptx::tc_commit(bar_d_full + 8 * dj);
+                        }
+                        __syncwarp();
+                        if (k == p.n_chunks - 1) d_use ^= 1u << dj;
+                        if (lane == 0) trace_ev(p, EV_M_ISSUED, n_items);
+                        ++n_items;
+                        if (++ab == p.n_abuf) {
+                            ab = 0;
+                            aph ^= 1u;
+                        }
+                        if (++dj == p.n_dbuf) dj = 0;
+                    }
+                    if (phi_slices) {   // every MMA of this chunk issued: the slice buffer may be refilled
+                        if (elect_one()) ptx::tc_commit(bar_key_empty + 8 * pb);
+                        __syncwarp();
+                        pb ^= 1;
+                        if (pb == 0) pbph ^= 1u;
+                    }
+                }
+                db = (db + U) % p.n_dbuf;
+                continue;
             }
             for (int c = w.c0; c < w.c1; ++c) {
                 ptx::mbar_wait(bar_d_empty + 8 * db, dph ^ 1u);
@@ -755,7 +881,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         uint32_t kreg[2][16];
         uint32_t g_off[2] = {0, 0}, g_acol[2] = {0, 0};
         bool g_half2[2] = {true, true};
-        if constexpr (KM == KEY_REGS) {
+        if constexpr (KM == KEY_REGS || KM == KEY_CHUNK) {
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const int g = wg + 2 * j;
@@ -774,6 +900,105 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             Unit w;
             if (!decode_unit(p, u, w)) continue;
+            if constexpr (KM == KEY_CHUNK) {
+                // per chunk: the key chunk's rows of this thread's (<= 2) row groups into registers,
+                // already expanded to the fp16 "magic" operand form (the expansion is paid once per
+                // unit and chunk, not once per CS frame), then chunk k of every CS frame of the unit
+                static_assert(KM != KEY_CHUNK || B == 32, "KEY_CHUNK is instantiated for B = 32");
+                for (int k = 0; k < p.n_chunks; ++k) {
+                    uint32_t kx[2][32];
+                    ptx::mbar_wait(bar_stage_full + 8 * st, ph);
+                    {
+                        const uint32_t kbase = s_stage + (uint32_t)st * p.stage_bytes;
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) {
+                            if (wg + 2 * j < n_groups) {
+#pragma unroll
+                                for (int rr = 0; rr < kRowsPerSt; ++rr) {
+                                    uint32_t kw[8];
+                                    load_row_words<B>(kbase + g_off[j] + (uint32_t)(rr * p.W), kw);
+#pragma unroll
+                                    for (int q = 0; q < 8; ++q) ptx::magic2(kw[q], kx[j][rr * 16 + 2 * q], kx[j][rr * 16 + 2 * q + 1]);
+                                }
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(bar_stage_empty + 8 * st);
+                    if (++st == p.n_stages) {
+                        st = 0;
+                        ph ^= 1u;
+                    }
+                    for (int c = w.c0; c < w.c1; ++c) {
+                        ptx::mbar_wait(bar_stage_full + 8 * st, ph);
+                        if (tr) trace_ev(p, EV_C_FULL, n_items);
+                        if (dbg_load_only) {
+                            __syncwarp();
+                            if (lane == 0) ptx::mbar_arrive(bar_stage_empty + 8 * st);
+                            if (++st == p.n_stages) {
+                                st = 0;
+                                ph ^= 1u;
+                            }
+                            ++n_items;
+                            continue;
+                        }
+                        ptx::mbar_wait(bar_a_empty + 8 * ab, aph ^ 1u);
+                        ptx::tc_fence_after();
+                        if (tr) trace_ev(p, EV_C_AEMPTY, n_items);
+                        const uint32_t cs_base = s_stage + (uint32_t)st * p.stage_bytes;
+                        const uint32_t a_tm = tmem_base + lane_bits + a_col0 + (uint32_t)ab * (uint32_t)p.a_cols;
+                        // per row group: both rows loaded (plain C++ shared loads after the stage-full
+                        // wait, so the compiler can issue them together), then the residual words and
+                        // the TMEM stores
+                        const uint8_t* const cs_ptr = smem_ptr + (cs_base - sbase);
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) {
+                            if (wg + 2 * j < n_groups) {
+                                CS_CHECK(g_off[j] + (uint32_t)((kRowsPerSt - 1) * p.W + B) <= p.set_bytes + 128u);
+                                CS_CHECK(g_acol[j] + 32u <= (uint32_t)p.a_cols);
+                                uint32_t cw[kRowsPerSt][8];
+#pragma unroll
+                                for (int rr = 0; rr < kRowsPerSt; ++rr) {
+                                    const uint4* src = reinterpret_cast<const uint4*>(cs_ptr + g_off[j] + (uint32_t)(rr * p.W));
+                                    const uint4 a = src[0], b = src[1];
+                                    cw[rr][0] = a.x, cw[rr][1] = a.y, cw[rr][2] = a.z, cw[rr][3] = a.w;
+                                    cw[rr][4] = b.x, cw[rr][5] = b.y, cw[rr][6] = b.z, cw[rr][7] = b.w;
+                                }
+#pragma unroll
+                                for (int rr = 0; rr < kRowsPerSt; ++rr) {
+                                    uint32_t v[16];
+                                    if (dbg_flags & 2) {   // ablation: no residual ALU
+#pragma unroll
+                                        for (int i = 0; i < 16; ++i) v[i] = 0u;
+                                    } else {
+                                        row32_vs_kexp(cw[rr], &kx[j][rr * 16], v, g_half2[j]);
+                                    }
+                                    ptx::tmem_st_32x32b_x16(a_tm + g_acol[j] + (uint32_t)(rr * 16), v);
+                                }
+                            }
+                        }
+                        if (tr) trace_ev(p, EV_C_CONV, n_items);
+                        ptx::tc_wait_st();
+                        ptx::tc_fence_before();
+                        if (tr) trace_ev(p, EV_C_DONE, n_items);
+                        ++n_items;
+                        __syncwarp();
+                        if (lane == 0) {
+                            ptx::mbar_arrive(bar_a_full + 8 * ab);
+                            ptx::mbar_arrive(bar_stage_empty + 8 * st);
+                        }
+                        if (++ab == p.n_abuf) {
+                            ab = 0;
+                            aph ^= 1u;
+                        }
+                        if (++st == p.n_stages) {
+                            st = 0;
+                            ph ^= 1u;
+                        }
+                    }
+                }
+                continue;
+            }
             if constexpr (KM == KEY_RESIDENT) ptx::mbar_wait(bar_key_full + 8 * kb, kph);
             if constexpr (KM == KEY_REGS) {
                 ptx::mbar_wait(bar_stage_full + 8 * st, ph);
@@ -1427,3 +1652,5 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
 }
 
 }  // namespace csenc
+
+#pragma nv_diagnostic pop

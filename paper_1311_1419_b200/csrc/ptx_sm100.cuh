@@ -317,6 +317,15 @@ __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_
         "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
         : "memory");
 }
+// 32 lanes x 32 bit, 16 consecutive columns.
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
 // 32 lanes x 32 bit, 8 consecutive columns -> 8 registers.
 __device__ __forceinline__ void tmem_ld_32x32b_x8(uint32_t taddr, uint32_t (&v)[8]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
@@ -399,21 +408,8 @@ __device__ __forceinline__ uint32_t hsub2(uint32_t a, uint32_t b) {
     asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
     return d;
 }
-__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t c) {  // (a & b) | c
-    uint32_t d;
-    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-    return d;
-}
-
-// Converter variant (compile-time; measured in DESIGN.md sec.7):
-//   0: four PRMT per four pixels (default)
-//   1: four fused LOP3 + two SHF (ALU pipe only)
-//   2: two fused LOP3 (bytes 0,2) + two PRMT (bytes 1,3)
-// Measured on B200 (C4 sweep / C5): all three within run-to-run noise -- the converter's
-// instruction mix is not the limiter (tools/sweep6.sh).
-#ifndef CSENC_CONV
-#define CSENC_CONV 0
-#endif
+// (Three converter instruction mixes -- four PRMT, fused LOP3 + SHF, and a mix of both -- measured
+// equal on B200; the PRMT form is the one kept.)
 
 // Four u8 pixels of the CS frame (c) and of the key (k) -> two fp16x2 words holding the exact
 // residuals c_i - k_i.  A byte XX placed in the low half of a 16-bit lane under 0x64 is
@@ -422,19 +418,22 @@ __device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t
 // word1 = {px1, px3}: within every group of four pixels the K index order is (0, 2, 1, 3); the
 // host stores Phi with its columns in the same order, so the contraction is unchanged.
 __device__ __forceinline__ void residual4(uint32_t c, uint32_t k, uint32_t& w0, uint32_t& w1) {
-#if CSENC_CONV == 0
     const uint32_t m8 = 0x64646464u;
     w0 = hsub2(prmt(c, m8, 0x4240u), prmt(k, m8, 0x4240u));
     w1 = hsub2(prmt(c, m8, 0x4341u), prmt(k, m8, 0x4341u));
-#elif CSENC_CONV == 1
-    const uint32_t mask = 0x00FF00FFu, magic = 0x64006400u;
-    w0 = hsub2(lop3_and_or(c, mask, magic), lop3_and_or(k, mask, magic));
-    w1 = hsub2(lop3_and_or(c >> 8, mask, magic), lop3_and_or(k >> 8, mask, magic));
-#else
-    const uint32_t mask = 0x00FF00FFu, magic = 0x64006400u, m8 = 0x64646464u;
-    w0 = hsub2(lop3_and_or(c, mask, magic), lop3_and_or(k, mask, magic));
-    w1 = hsub2(prmt(c, m8, 0x4341u), prmt(k, m8, 0x4341u));
-#endif
+}
+
+// u8 word -> its two fp16x2 "magic" words {1024 + b0, 1024 + b2}, {1024 + b1, 1024 + b3} (residual4's
+// operand form, computed once for a key word that is reused against many CS words)
+__device__ __forceinline__ void magic2(uint32_t k, uint32_t& m0, uint32_t& m1) {
+    m0 = prmt(k, 0x64646464u, 0x4240u);
+    m1 = prmt(k, 0x64646464u, 0x4341u);
+}
+// residual4 against a pre-expanded key (magic2 of the key word)
+__device__ __forceinline__ void residual4x(uint32_t c, uint32_t km0, uint32_t km1, uint32_t& w0, uint32_t& w1) {
+    const uint32_t m8 = 0x64646464u;
+    w0 = hsub2(prmt(c, m8, 0x4240u), km0);
+    w1 = hsub2(prmt(c, m8, 0x4341u), km1);
 }
 
 // ------------------------------------------------------------------ UMMA descriptors
