@@ -37,7 +37,7 @@ import synth  # noqa: E402
 L2_BYTES = 126 * 1024 * 1024
 
 
-OUTPUTS = {"f32": None, "q16frame": 0, "q16row": 1, "q16frame1": 2}   # --output -> cs_encode_batch_q16 granularity
+OUTPUTS = {"f32": None, "q16frame": 0, "q16row": 1}   # --output -> cs_encode_batch_q16 granularity
 
 
 def alg_bytes(cfg, M, n_seq, output="f32"):
@@ -48,7 +48,7 @@ def alg_bytes(cfg, M, n_seq, output="f32"):
     n_cs = cfg.T - -(-cfg.T // cfg.G)
     if output == "f32":
         return n_seq * (cfg.T * cfg.W * cfg.H + n_cs * nbx * nby * M * 4)
-    n_scales = n_cs * (nby if output == "q16row" else 1)   # q16frame / q16frame1: one per CS frame
+    n_scales = n_cs * (nby if output == "q16row" else 1)   # q16frame: one per CS frame
     return n_seq * (cfg.T * cfg.W * cfg.H + n_cs * nbx * nby * M * 2 + 4 * n_scales)
 
 

@@ -167,20 +167,12 @@ int cs_encode_batch_gops(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, 
  *     maxima and a re-quantisation kernel makes the codes; otherwise the measurement runs twice: an
  *     absmax pass (no stores, one atomicMax per warp and frame) and a codes pass.  Then a tiny
  *     finalize kernel (memset + 3 launches either way).  Both give the same codes, bit for bit.
- *   CS_Q16_FRAME_1PASS: the same result (bitwise) in ONE pass over the frames: whole-GOP units in
- *     rounds of whole GOPs (grid a multiple of the tiles per frame, cooperative launch), each
- *     tile's |y| maximum published to the frame's maximum and arrival counter by a publisher
- *     warp, and the item `lag` items back quantised from TMEM once its frame is complete
- *     (decoupled look-back).  Measured slower than the two passes on B200 (every CTA's epilogue
- *     is gated by the slowest CTA of its frame); kept as an option.
- *     CS_ERR_UNSUPPORTED when no plan fits (D ring >= 2 accumulators, tiles per frame <= SMs).
  *   CS_Q16_ROW: one scale per (CS frame, block row of B pixel rows): a single fused pass (the
  *     maximum is reduced on chip).  A documented deviation (R19).  Needs tiles of
  *     <= 40 block rows: when the encoder's current plan has taller tiles the call runs the best
  *     candidate plan that qualifies (CS_ERR_UNSUPPORTED only if none does). */
 #define CS_Q16_FRAME 0
 #define CS_Q16_ROW 1
-#define CS_Q16_FRAME_1PASS 2
 
 /* Number of fp32 scales cs_encode_batch_q16 writes: n_cs (FRAME) or n_cs * nby (ROW), where
  * n_cs = n_seq * CS frames per stream; -1 on bad arguments. */

@@ -349,7 +349,7 @@ class Encoder:
         return out
 
     # -- 16-bit quantisation (f1)
-    Q16_FRAME, Q16_ROW, Q16_FRAME_1PASS = 0, 1, 2
+    Q16_FRAME, Q16_ROW = 0, 1
 
     def q16_scale_shape(self, n_seq: int, T: int, granularity: int = 0):
         n_cs = self.out_shape(n_seq, T)[0]

@@ -11,7 +11,7 @@ LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.environ.get("CSENC_LIB") or os.path.join(LIB_DIR, "libcsenc.so")
 SOURCES = ["cs_common.cu", "cs_encoder.cu", "cs_adjoint.cu", "cs_keys.cu", "cs_frame.cu"]
 HEADERS = ["cs_measure_kernel.cuh", "ptx_sm100.cuh", "cs_adjoint_kernel.cuh", "cs_key_codec_kernel.cuh",
-           "cs_frame_kernel.cuh", "cs_frame2_kernel.cuh", "cs_internal.h"]
+           "cs_frame_kernel.cuh", "cs_internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

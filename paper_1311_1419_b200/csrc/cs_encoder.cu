@@ -290,8 +290,6 @@ namespace {
 struct QArgs {
     const uint8_t* keys = nullptr;   // f4: decoded key frames [n_seq][ceil(T/G)][H][W]
     int chained = 0;                 // f4 variant: previous-frame reference (needs a KEY_STREAMED plan)
-    int gop_rounds = 0;              // f1 single pass: whole-GOP units, grid a multiple of n_tiles
-    unsigned* arrivals = nullptr;    // f1 single pass: per-frame arrival counters (zeroed)
     const Plan* plan = nullptr;      // plan override (default e->plan)
     int qmode = 0;
     int16_t* codes = nullptr;
@@ -352,11 +350,7 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.gop_begin = g0;
     kp.n_gops_sel = g1 - g0;
     kp.cs_per_stream_sel = (int)cs_frames_in_gops(T, g.G, g0, g1);
-    if (q.gop_rounds) {
-        kp.n_splits = 1;
-        kp.cs_per_unit = g.G - 1;
-        kp.n_units = n_seq * (g1 - g0) * pl.n_tiles;
-    } else {
+    {
         WorkSplit ws = choose_split(g, pl, n_seq, g1 - g0, e->sms);
         kp.n_splits = ws.n_splits;
         kp.cs_per_unit = ws.cs_per_unit;
@@ -385,8 +379,6 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.codes = q.codes;
     kp.amax = q.amax;
     kp.scales = q.scales;
-    kp.arrivals = q.arrivals;
-    kp.lookback = std::max(1, std::min(std::min(csenc::kMaxLag, pl.n_dbuf - 1), env_int("CSENC_LOOKBACK", 99)));
     // multi-piece strips by one 4-D TMA box (H % B == 0 so block rows never run into the next frame;
     // the box's inner extent W/4 u32 words <= 256; pieces packed back to back in the stage)
     csenc::KParamsTS kpt;
@@ -406,29 +398,30 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
             kpt.tma_strips = (r == CUDA_SUCCESS && pl.T_r <= 256) ? 1 : 0;
         }
     }
+#if CSENC_CHECKS
+    {   // race gate: random delays after mbarrier waits (ptx::stress_point), seed from CSENC_STRESS
+        static const unsigned int stress = [] {
+            const char* v = std::getenv("CSENC_STRESS");
+            return v ? (unsigned int)std::strtoul(v, nullptr, 10) : 0u;
+        }();
+        static std::once_flag once;
+        std::call_once(once, [] { cudaMemcpyToSymbol(csenc::ptx::g_csenc_stress, &stress, sizeof(stress)); });
+    }
+#endif
     int grid = std::max(1, std::min(e->sms, kp.n_units));
-    if (q.gop_rounds) grid = std::max(1, std::min(e->sms / pl.n_tiles * pl.n_tiles, kp.n_units));
     cudaError_t err;
     const int km = pl.key_chunk ? csenc::KEY_CHUNK
                    : pl.key_regs ? csenc::KEY_REGS : (pl.key_resident ? csenc::KEY_RESIDENT : csenc::KEY_STREAMED);
     // KEY_STREAMED / KEY_CHUNK kernels take KParamsTS (with the strip tensor map), the others KParams
     auto go = [&](auto kern) {
-        auto run = [&](auto& prm) {
-            if (q.gop_rounds) {   // the look-back needs every CTA resident: cooperative launch guarantees it
-                void* args[] = {&prm};
-                cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(csenc::threads_for<csenc::EPI_Q16F>()),
-                                            args, pl.smem_bytes, stream);
-            } else {
-                kern<<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(prm);
-            }
-        };
+        auto run = [&](auto& prm) { kern<<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(prm); };
         if constexpr (std::is_invocable_v<decltype(kern), const csenc::KParamsTS&> &&
                       !std::is_invocable_v<decltype(kern), const csenc::KParams&>)
             run(kpt);
         else
             run(kp);
     };
-    int epi = q.qmode == csenc::Q_FRAME1 ? csenc::EPI_Q16F : (q.qmode ? csenc::EPI_Q16 : csenc::EPI_F32);
+    int epi = q.qmode ? csenc::EPI_Q16 : csenc::EPI_F32;
     if (q.qmode == csenc::Q_STOREMAX) epi = csenc::EPI_F32A;
     if (q.qmode == csenc::Q_ROW)
         epi = (pl.F != 1 || g.Mpad != g.M || pl.T_r > csenc::kRowRegRows || g.Mpad > 64) ? csenc::EPI_Q16R
@@ -436,7 +429,6 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
 #define CSENC_CASE(B_, K_)                                                                                \
     case (B_ * 4 + K_) * 8 + csenc::EPI_F32: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_F32>); break;   \
     case (B_ * 4 + K_) * 8 + csenc::EPI_Q16: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16>); break;   \
-    case (B_ * 4 + K_) * 8 + csenc::EPI_Q16F: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16F>); break; \
     case (B_ * 4 + K_) * 8 + csenc::EPI_Q16R: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16R>); break; \
     case (B_ * 4 + K_) * 8 + csenc::EPI_Q16RR: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16RR>); break; \
     case (B_ * 4 + K_) * 8 + csenc::EPI_Q16RR64: go(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16RR64>); break; \
@@ -461,9 +453,6 @@ cudaError_t set_smem_attr_all(int bytes) {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);                         \
     if (r != cudaSuccess) e = r;                                                                          \
     r = cudaFuncSetAttribute(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16>,                           \
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);                         \
-    if (r != cudaSuccess) e = r;                                                                          \
-    r = cudaFuncSetAttribute(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16F>,                          \
                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);                         \
     if (r != cudaSuccess) e = r;                                                                          \
     r = cudaFuncSetAttribute(csenc::cs_measure_kernel<B_, K_, csenc::EPI_Q16R>,                          \
@@ -617,18 +606,6 @@ int cs_encoder_create(int W, int H, int gop, int B, int M, const uint16_t* phi_f
             e->row_plan = (int)i;
             break;
         }
-    // f1 single pass: the best plan with a D ring deep enough for the look-back whose tiles fit one
-    // round (n_tiles <= SMs)
-    for (size_t i = 0; i < e->candidates.size(); ++i) {
-        Plan c = e->candidates[i];
-        if (c.key_chunk) continue;   // whole-GOP units: more frames than a KEY_CHUNK unit may hold
-        // the look-back holds `lag` accumulators: the D ring as deep as TMEM allows, lag = ring - 1
-        c.n_dbuf = std::min(csenc::kMaxTmemBufs, ((int)csenc::kTmemCols - c.n_abuf * c.a_cols) / c.d_cols);
-        if (c.n_dbuf < 2 || c.n_tiles > e->sms) continue;
-        e->frame1_plan = (int)i;
-        e->frame1 = c;
-        break;
-    }
     if (!make_plan(e->geo, e->smem_limit, e->plan)) {
         delete e;
         return fail(CS_ERR_UNSUPPORTED, "no tiling fits shared memory / TMEM for this configuration");
@@ -893,7 +870,7 @@ int cs_encode_batch_keys(cs_encoder* e, const uint8_t* frames, int n_seq, int T,
 int64_t cs_q16_scale_count(const cs_encoder* e, int n_seq, int T, int granularity) {
     if (!e || n_seq < 0 || T < 0) return -1;
     const long long n_cs = (long long)n_seq * cs_frames_per_stream(T, e->geo.G);
-    if (granularity == CS_Q16_FRAME || granularity == CS_Q16_FRAME_1PASS) return n_cs;
+    if (granularity == CS_Q16_FRAME) return n_cs;
     if (granularity == CS_Q16_ROW) return n_cs * e->geo.nby;
     return -1;
 }
@@ -903,8 +880,7 @@ int cs_encode_batch_q16(cs_encoder* e, const uint8_t* frames, int n_seq, int T, 
     csenc::host::NvtxScope nvtx_scope("cs_encode_batch_q16");
     if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
     if (n_seq < 0 || T < 0) return fail(CS_ERR_ARG, "n_seq and T must be >= 0");
-    if (granularity != CS_Q16_FRAME && granularity != CS_Q16_ROW && granularity != CS_Q16_FRAME_1PASS)
-        return fail(CS_ERR_ARG, "bad granularity");
+    if (granularity != CS_Q16_FRAME && granularity != CS_Q16_ROW) return fail(CS_ERR_ARG, "bad granularity");
     const Geometry& g = e->geo;
     const long long n_cs = (long long)n_seq * cs_frames_per_stream(T, g.G);
     if (n_cs == 0) return CS_OK;
@@ -926,28 +902,6 @@ int cs_encode_batch_q16(cs_encoder* e, const uint8_t* frames, int n_seq, int T, 
         q.qmode = csenc::Q_ROW;
         q.scales = scales;
         return launch(e, frames, n_seq, T, 0, n_gops, nullptr, st, q);
-    }
-    if (granularity == CS_Q16_FRAME_1PASS && e->frame1_plan < 0)
-        return fail(CS_ERR_UNSUPPORTED, "single-pass per-frame quantisation: no plan (D ring >= 2, tiles <= SMs)");
-    if (granularity == CS_Q16_FRAME_1PASS) {
-        // per-frame scale in ONE pass: frame-major units, decoupled look-back on per-frame maxima
-        // (workspace: |y| maxima and arrival counters, stream-ordered, zeroed)
-        uint32_t* ws = nullptr;
-        cudaError_t err = scratch_alloc(e, (void**)&ws, (size_t)n_cs * 8, st);
-        if (err != cudaSuccess) return fail(CS_ERR_OOM, std::string("q16 workspace: ") + cudaGetErrorString(err));
-        err = cudaMemsetAsync(ws, 0, (size_t)n_cs * 8, st);
-        int rc = err == cudaSuccess ? CS_OK : cuda_fail(err, "cudaMemsetAsync");
-        if (rc == CS_OK) {
-            q.qmode = csenc::Q_FRAME1;
-            q.amax = ws;
-            q.arrivals = ws + n_cs;
-            q.scales = scales;
-            q.gop_rounds = 1;
-            q.plan = &e->frame1;
-            rc = launch(e, frames, n_seq, T, 0, n_gops, nullptr, st, q);
-        }
-        cudaFreeAsync(ws, st);
-        return rc;
     }
     // per-frame scale: zero the |y| maxima, then either
     //  (a) 8 M < N: one measurement pass storing fp32 y in a stream-ordered workspace + the maxima,
@@ -1017,8 +971,7 @@ int host_pipeline(cs_encoder* const* encs, int n_enc, const uint8_t* frames_host
     }
     if (n_seq < 0 || T < 0) return fail(CS_ERR_ARG, "n_seq and T must be >= 0");
     const bool q16 = granularity >= 0;
-    if (q16 && granularity != CS_Q16_FRAME && granularity != CS_Q16_ROW && granularity != CS_Q16_FRAME_1PASS)
-        return fail(CS_ERR_ARG, "bad granularity");
+    if (q16 && granularity != CS_Q16_FRAME && granularity != CS_Q16_ROW) return fail(CS_ERR_ARG, "bad granularity");
     cs_encoder* const e = encs[0];   // frames workspace, streams and events
     const Geometry& g = e->geo;
     const long long cs_s = cs_frames_per_stream(T, g.G);

@@ -1,6 +1,6 @@
 // cs_frame.cu -- host side of K4, the paper-faithful frame-level measurement y = A vec(F_cs - F_key)
 // with one dense A: the frame encoder object, window planning (load
-// balance), tensor maps, cluster launch, split-K reduction.
+// balance), tensor maps, launch, split-K reduction.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -10,7 +10,6 @@
 
 #include "cs_internal.h"
 #include "cs_frame_kernel.cuh"
-#include "cs_frame2_kernel.cuh"
 
 using namespace csenc::host;
 
@@ -52,14 +51,8 @@ int cs_frame_encoder_create(int W, int H, int gop, int m, const uint16_t* A_fp16
     f->device = dev;
     cudaDeviceGetAttribute(&f->sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&f->smem_limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    err = cudaFuncSetAttribute(csenc::frm::cs_frame_measure_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    err = cudaFuncSetAttribute(csenc::frm::cs_frame_measure_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                f->smem_limit);
-    if (err == cudaSuccess)
-        err = cudaFuncSetAttribute(csenc::frm::cs_frame_measure_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   f->smem_limit);
-    if (err == cudaSuccess)
-        err = cudaFuncSetAttribute(csenc::frm2::cs_frame2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   f->smem_limit);
     if (err != cudaSuccess) {
         delete f;
         return cuda_fail(err, "cudaFuncSetAttribute");
@@ -108,145 +101,6 @@ int64_t cs_frame_measurement_count(const cs_frame_encoder* f, int n_seq, int T) 
 
 }  // extern "C"
 
-namespace {
-
-// K4b: CTA pairs with the 2-SM MMA (cs_frame2_kernel.cuh).  Returns CS_ERR_UNSUPPORTED (nothing
-// launched) when the shape does not suit it; the caller then runs K4.
-int encode_2sm(cs_frame_encoder* f, const uint8_t* frames, int n_seq, int T, float* y, cudaStream_t st) {
-    const int G = f->G;
-    const long long cs_s = cs_frames_per_stream(T, G);
-    PFN_encodeTiled enc = get_encode_tiled();
-    if (!enc) return fail(CS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    csenc::frm2::F2Params fp;
-    std::memset(&fp, 0, sizeof(fp));
-    // each CTA of a pair takes gw2 GOPs of the window: <= 128 CS frames (B rows) and <= 256 box rows
-    const int n_gops = cdiv(T, G);
-    fp.gw2 = std::max(1, std::min(128 / (G - 1), 256 / G));
-    if (T % G == 0) {
-        fp.global_win = 1;
-        fp.total_gops = n_seq * n_gops;
-        fp.gw2 = std::min(fp.gw2, cdiv(fp.total_gops, 2));
-        fp.n_win = cdiv(fp.total_gops, 2 * fp.gw2);
-    } else {
-        fp.global_win = 0;
-        fp.total_gops = n_seq * n_gops;
-        fp.gw2 = std::min(fp.gw2, cdiv(n_gops, 2));
-        fp.n_win_s = cdiv(n_gops, 2 * fp.gw2);
-        fp.n_win = n_seq * fp.n_win_s;
-    }
-    fp.nf_box = fp.gw2 * G;
-    fp.nhalf = (fp.gw2 * (G - 1) + 7) / 8 * 8;
-    if (fp.nhalf > 128) return CS_ERR_UNSUPPORTED;
-    fp.n = f->n;
-    fp.m = f->m;
-    fp.G = G;
-    fp.T = T;
-    fp.cs_s = (int)cs_s;
-    fp.n_mp = cdiv(f->m, 256);
-    fp.n_chunks = cdiv(f->n, csenc::frm2::kKc);
-    // pairs that can be resident at once (a pair needs both SMs of a TPC; query, do not assume SMs / 2)
-    static int max_pairs = 0;
-    if (max_pairs == 0) {
-        cudaLaunchConfig_t qc;
-        std::memset(&qc, 0, sizeof(qc));
-        qc.gridDim = dim3((unsigned)(f->sms / 2 * 2));
-        qc.blockDim = dim3(csenc::frm2::kThreads);
-        qc.dynamicSmemBytes = (size_t)f->smem_limit;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 2;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        qc.attrs = at;
-        qc.numAttrs = 1;
-        int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, (void*)csenc::frm2::cs_frame2_kernel, &qc) != cudaSuccess || n < 1)
-            n = f->sms / 2;
-        max_pairs = n;
-    }
-    // K splits: the best balance of the pair units over the resident pairs (a little penalty per
-    // partial plane)
-    const long long pairs = max_pairs, base = (long long)fp.n_win * fp.n_mp;
-    int best_ks = 1;
-    double best = -1.0;
-    for (int ks = 1; ks <= std::max(1, std::min(8, fp.n_chunks / 8)); ++ks) {
-        const long long units = base * ks;
-        const long long rounds = (units + pairs - 1) / pairs;
-        const double eff = (double)units / (double)(rounds * pairs) - (ks > 1 ? 0.03 * ks : 0.0);
-        if (eff > best + 1e-9) {
-            best = eff;
-            best_ks = ks;
-        }
-    }
-    fp.n_ks = best_ks;
-    {   // no empty K split
-        const int per = cdiv(fp.n_chunks, fp.n_ks);
-        fp.n_ks = cdiv(fp.n_chunks, per);
-    }
-    if (base * fp.n_ks > 0x7FFFFFFFLL) return fail(CS_ERR_UNSUPPORTED, "too many work units");
-    fp.n_units = (int)(base * fp.n_ks);
-    {
-        cuuint64_t dims[2] = {(cuuint64_t)f->n, (cuuint64_t)n_seq * T};
-        cuuint64_t strides[1] = {(cuuint64_t)f->n};
-        cuuint32_t box[2] = {(cuuint32_t)csenc::frm2::kKc, (cuuint32_t)fp.nf_box};
-        cuuint32_t estr[2] = {1, 1};
-        CUresult r = enc(&fp.fmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(frames), dims, strides, box,
-                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return fail(CS_ERR_CUDA, "cuTensorMapEncodeTiled(frames) failed");
-    }
-    {
-        cuuint64_t dims[2] = {(cuuint64_t)f->n, (cuuint64_t)f->m};
-        cuuint64_t strides[1] = {(cuuint64_t)f->n * 2u};
-        cuuint32_t box[2] = {(cuuint32_t)csenc::frm2::kKc, 128u};
-        cuuint32_t estr[2] = {1, 1};
-        CUresult r = enc(&fp.amap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, f->A_dev, dims, strides, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return fail(CS_ERR_CUDA, "cuTensorMapEncodeTiled(A) failed");
-    }
-    fp.fbox_bytes = (uint32_t)fp.nf_box * (uint32_t)csenc::frm2::kKc;
-    fp.off_a = align_up(fp.fbox_bytes, 1024);
-    fp.stage_bytes = fp.off_a + 128u * csenc::frm2::kKc * 2u;
-    fp.b_bytes = align_up((uint32_t)fp.nhalf * 128u, 1024);
-    fp.n_b = std::max(2, std::min(csenc::frm2::kMaxB, env_int("CSENC_FRAME2_BBUFS", 4)));
-    fp.off_stage = csenc::frm2::kOffB + (uint32_t)fp.n_b * fp.b_bytes;
-    const long avail = (long)f->smem_limit - 1024 - (long)fp.off_stage;
-    fp.n_stages = (int)std::min<long>(csenc::frm2::kMaxStages, avail / (long)fp.stage_bytes);
-    if (fp.n_stages < 2) return CS_ERR_UNSUPPORTED;
-    const uint32_t smem = 1024 + fp.off_stage + (uint32_t)fp.n_stages * fp.stage_bytes;
-    fp.smem_bytes = smem - 1024;
-    fp.trace = f->trace;
-    fp.trace_cap = f->trace_cap;
-    fp.dbg = env_int("CSENC_F2_DBG", 0);
-    const long long ny = (long long)n_seq * cs_s * f->m;
-    fp.out_floats = ny;
-    if (env_int("CSENC_FRAME_VERBOSE", 0))
-        std::fprintf(stderr, "frame2: pairs %lld win %d gw2 %d nhalf %d ks %d units %d stages %d bbufs %d\n", pairs,
-                     fp.n_win, fp.gw2, fp.nhalf, fp.n_ks, fp.n_units, fp.n_stages, fp.n_b);
-    float* part = nullptr;
-    cudaError_t err;
-    if (fp.n_ks > 1) {
-        fp.part_stride = (ny + 3) / 4 * 4;
-        err = cudaMallocAsync((void**)&part, (size_t)fp.part_stride * fp.n_ks * sizeof(float), st);
-        if (err != cudaSuccess) return fail(CS_ERR_OOM, std::string("partials: ") + cudaGetErrorString(err));
-        fp.out = part;
-    } else {
-        fp.part_stride = 0;
-        fp.out = y;
-    }
-    const int n_pairs = (int)std::max(1LL, std::min(pairs, (long long)fp.n_units));
-    csenc::frm2::cs_frame2_kernel<<<2 * n_pairs, csenc::frm2::kThreads, smem, st>>>(fp);
-    err = cudaGetLastError();
-    if (err == cudaSuccess && fp.n_ks > 1) {
-        csenc::frm::cs_frame_reduce_kernel<<<f->sms * 4, 256, 0, st>>>(part, y, ny, fp.part_stride, fp.n_ks);
-        err = cudaGetLastError();
-    }
-    if (part) cudaFreeAsync(part, st);
-    return err == cudaSuccess ? CS_OK : cuda_fail(err, "frame measurement (2-SM) launch");
-}
-
-}  // namespace
 
 extern "C" {
 
@@ -261,10 +115,6 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     if ((long long)n_seq * T > 0x7FFFFFFFLL) return fail(CS_ERR_UNSUPPORTED, "too many frames");
     if (int rc = check_device(f->device)) return rc;
     const cudaStream_t st = (cudaStream_t)stream;
-    if (env_int("CSENC_FRAME_2SM", 0) == 1) {   // K4b: CTA pairs, 2-SM MMA (opt-in: measured slower, DESIGN 6d)
-        const int rc = encode_2sm(f, frames, n_seq, T, y, st);
-        if (rc != CS_ERR_UNSUPPORTED) return rc;
-    }
     csenc::frm::FParams fp;
     std::memset(&fp, 0, sizeof(fp));
     PFN_encodeTiled enc = get_encode_tiled();
@@ -300,10 +150,6 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
         fp.n_win = n_seq * fp.n_win_s;
     }
     fp.nf_box = fp.gw * G;
-    // pairs of CTAs (a cluster) can share each A tile by TMA multicast
-    // (measured slower on B200 than independent CTAs: 876 vs 966 TFLOP/s -- the pair is coupled
-    // through the shared stage; opt-in with CSENC_FRAME_CLUSTER=1)
-    const int CL = (fp.n_win >= 2 && env_int("CSENC_FRAME_CLUSTER", 0) == 1) ? 2 : 1;
     {
         cuuint64_t dims[2] = {(cuuint64_t)f->n, (cuuint64_t)n_seq * T};
         cuuint64_t strides[1] = {(cuuint64_t)f->n};
@@ -317,7 +163,7 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     {
         cuuint64_t dims[2] = {(cuuint64_t)f->n, (cuuint64_t)f->m};
         cuuint64_t strides[1] = {(cuuint64_t)f->n * 2u};
-        cuuint32_t box[2] = {(cuuint32_t)csenc::frm::kKc, (cuuint32_t)(256 / CL)};
+        cuuint32_t box[2] = {(cuuint32_t)csenc::frm::kKc, 256u};
         cuuint32_t estr[2] = {1, 1};
         CUresult r = enc(&fp.amap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, f->A_dev, dims, strides, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -331,8 +177,8 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     fp.cs_s = (int)cs_s;
 
     fp.n_chunks = cdiv(f->n, csenc::frm::kKc);
-    const long long n_cl = f->sms / CL;                                 // clusters resident at once
-    const long long tiles = (long long)((fp.n_win + CL - 1) / CL) * fp.n_mp;   // cluster work units
+    const long long n_cl = f->sms;                                      // CTAs resident at once
+    const long long tiles = (long long)fp.n_win * fp.n_mp;              // work units per K split
     long long ks = (n_cl + tiles - 1) / tiles;                        // K splits to fill the SMs
     ks = std::max(1LL, std::min(ks, (long long)std::max(1, fp.n_chunks / 8)));
     if (const int ksf = env_int("CSENC_FRAME_KS", 0)) ks = std::max(1, std::min(ksf, fp.n_chunks));   // experiment knob
@@ -378,23 +224,9 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
         fp.part_stride = 0;
         fp.out = y;
     }
-    const int n_clusters = (int)std::max(1LL, std::min(n_cl, (long long)fp.n_units));
-    cudaLaunchConfig_t cfg;
-    std::memset(&cfg, 0, sizeof(cfg));
-    cfg.gridDim = dim3((unsigned)(n_clusters * CL));
-    cfg.blockDim = dim3(csenc::frm::kThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)CL;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    err = CL == 2 ? cudaLaunchKernelEx(&cfg, csenc::frm::cs_frame_measure_kernel<2>, fp)
-                  : cudaLaunchKernelEx(&cfg, csenc::frm::cs_frame_measure_kernel<1>, fp);
-    if (err == cudaSuccess) err = cudaGetLastError();
+    const int grid = (int)std::max(1LL, std::min(n_cl, (long long)fp.n_units));
+    csenc::frm::cs_frame_measure_kernel<<<grid, csenc::frm::kThreads, smem, st>>>(fp);
+    err = cudaGetLastError();
     if (err == cudaSuccess && fp.n_ks > 1) {
         csenc::frm::cs_frame_reduce_kernel<<<f->sms * 4, 256, 0, st>>>(part, y, ny, fp.part_stride, fp.n_ks);
         err = cudaGetLastError();

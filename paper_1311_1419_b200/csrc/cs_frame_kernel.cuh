@@ -44,7 +44,7 @@ constexpr uint32_t kOffB = 1024;                 // two residual (B operand) buf
 
 struct FParams {
     CUtensorMap fmap;         // frames: 2-D [n_seq*T rows][n bytes], box [nf_box][64], SWIZZLE_64B
-    CUtensorMap amap;         // A (permuted): 2-D [m rows][n fp16], box [256 / CL][64], SWIZZLE_128B
+    CUtensorMap amap;         // A (permuted): 2-D [m rows][n fp16], box [256][64], SWIZZLE_128B
     float* out;               // y [n_seq*cs_s][m] (n_ks == 1) or partials [n_ks][n_seq*cs_s][m]
     int n, m, G, T, cs_s;     // pixels, measurements, GOP, frames/stream, CS frames/stream
     int gw, nf_box;           // GOPs per window, frame rows per box (= gw * G)
@@ -78,18 +78,13 @@ struct FUnit {
     int s, g0, ngops, n_cs, cs0, mp, ks, kc0, kc1;
 };
 
-// CL CTAs (a cluster) work on one unit = (K split, window group, m-pair) together: CTA `rank` of
-// the cluster takes window group * CL + rank (a window past the end is an empty dummy that still
-// loads and multicasts its share of A).
-template <int CL>
-__device__ __forceinline__ void decode_funit(const FParams& p, int u, int rank, FUnit& w) {
-    // u = (ks * n_grp + grp) * n_mp + mp: clusters running together share the K range
+// Unit u = (ks * n_win + win) * n_mp + mp: (K split, window, m-pair); CTAs running together share
+// the K range.
+__device__ __forceinline__ void decode_funit(const FParams& p, int u, FUnit& w) {
     w.mp = u % p.n_mp;
     const int r = u / p.n_mp;
-    const int n_grp = (p.n_win + CL - 1) / CL;
-    const int grp = r % n_grp;
-    w.ks = r / n_grp;
-    const int win = grp * CL + rank;
+    const int win = r % p.n_win;
+    w.ks = r / p.n_win;
     const int per = (p.n_chunks + p.n_ks - 1) / p.n_ks;
     w.kc0 = w.ks * per;
     w.kc1 = min(p.n_chunks, w.kc0 + per);
@@ -120,7 +115,6 @@ __device__ __forceinline__ void decode_funit(const FParams& p, int u, int rank, 
     w.cs0 = w.g0 * (p.G - 1);
 }
 
-template <int CL>
 __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __grid_constant__ FParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t sbase = (ptx::smem_addr(smem_raw) + 1023u) & ~1023u;
@@ -137,9 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
     const uint32_t bar_dempty = bar_dfull + 8;
     const uint32_t tmem_slot = bar_dempty + 8;
 
-    const int rank = CL > 1 ? (int)ptx::cluster_ctarank() : 0;
-    const int cid = (int)blockIdx.x / CL, n_cl = (int)gridDim.x / CL;
-    constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
+    const int cid = (int)blockIdx.x, n_cl = (int)gridDim.x;
     if (threadIdx.x == 0) {
         for (int i = 0; i < p.n_stages; ++i) {
             ptx::mbar_init(bar_full + 8 * i, 1);
@@ -147,7 +139,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         }
         for (int i = 0; i < p.n_a; ++i) {
             ptx::mbar_init(bar_afull + 8 * i, 1);
-            ptx::mbar_init(bar_aempty + 8 * i, CL);   // every CTA's MMAs must be done with the (shared) A tile
+            ptx::mbar_init(bar_aempty + 8 * i, 1);
         }
         for (int i = 0; i < 4; ++i) {
             ptx::mbar_init(bar_conv + 8 * i, kConvWarps);
@@ -169,10 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
     CS_CHECK(p.off_a + (uint32_t)p.n_a * 256u * kKc * 2u <= p.smem_bytes && p.n_a <= kMaxStages);
     CS_CHECK(p.fbox_bytes <= p.stage_bytes && p.n_b <= 4);
     ptx::tc_fence_before();
-    if constexpr (CL > 1)
-        ptx::cluster_sync();   // peers' barriers initialised before any multicast lands in them
-    else
-        __syncthreads();
+    __syncthreads();
     ptx::tc_fence_after();
     uint32_t tmem_base;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem_base) : "r"(tmem_slot));
@@ -183,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         uint32_t ph = 0;
         for (int u = cid; u < p.n_units; u += n_cl) {
             FUnit w;
-            decode_funit<CL>(p, u, rank, w);
+            decode_funit(p, u, w);
             const int row0 = w.s * p.T + w.g0 * p.G;
             if (lane == 0)   // frames stream from HBM: pull the first boxes of the unit into L2 early
                 for (int kc = w.kc0; kc < min(w.kc1, w.kc0 + p.prefetch); ++kc)
@@ -194,12 +183,8 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                     ptx::tma_prefetch_2d(&p.fmap, (kc + p.prefetch) * kKc, row0);
                 if (lane == 0) {
                     const uint32_t sf = sbase + p.off_stage + (uint32_t)st * p.stage_bytes;
-                    if (w.n_cs > 0) {
-                        ptx::mbar_arrive_expect_tx(bar_full + 8 * st, p.fbox_bytes);
-                        ptx::tma_load_2d(sf, &p.fmap, bar_full + 8 * st, kc * kKc, row0);
-                    } else {
-                        ptx::mbar_arrive(bar_full + 8 * st);   // empty dummy window (cluster padding)
-                    }
+                    ptx::mbar_arrive_expect_tx(bar_full + 8 * st, p.fbox_bytes);
+                    ptx::tma_load_2d(sf, &p.fmap, bar_full + 8 * st, kc * kKc, row0);
                     ftrace(p, 0, ntr);
                 }
                 ++ntr;
@@ -216,20 +201,13 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         uint32_t aph = 0;
         for (int u = cid; u < p.n_units; u += n_cl) {
             FUnit w;
-            decode_funit<CL>(p, u, rank, w);
+            decode_funit(p, u, w);
             for (int kc = w.kc0; kc < w.kc1; ++kc) {
                 ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
                 if (lane == 0) {
                     const uint32_t sa = sbase + p.off_a + (uint32_t)as * (256u * kKc * 2u);
                     ptx::mbar_arrive_expect_tx(bar_afull + 8 * as, 256u * kKc * 2u);
-                    if constexpr (CL == 1) {
-                        ptx::tma_load_2d(sa, &p.amap, bar_afull + 8 * as, kc * kKc, w.mp * 256);
-                    } else {
-                        // this CTA's share of the 256-row A tile, multicast to every CTA of the cluster
-                        constexpr int kRows = 256 / CL;
-                        ptx::tma_load_2d_mc(sa + (uint32_t)(rank * kRows * kKc * 2), &p.amap, bar_afull + 8 * as,
-                                            kc * kKc, w.mp * 256 + rank * kRows, kMask);
-                    }
+                    ptx::tma_load_2d(sa, &p.amap, bar_afull + 8 * as, kc * kKc, w.mp * 256);
                 }
                 __syncwarp();
                 if (++as == p.n_a) {
@@ -255,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         uint32_t ph = 0, bph = 0;
         for (int u = cid; u < p.n_units; u += n_cl) {
             FUnit w;
-            decode_funit<CL>(p, u, rank, w);
+            decode_funit(p, u, w);
             for (int kc = w.kc0; kc < w.kc1; ++kc) {
                 ptx::mbar_wait(bar_full + 8 * st, ph);
                 if (tid == 0) ftrace(p, 1, ntr);
@@ -314,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         uint32_t ph = 0, bph = 0, dph = 0;
         for (int u = cid; u < p.n_units; u += n_cl) {
             FUnit w;
-            decode_funit<CL>(p, u, rank, w);
+            decode_funit(p, u, w);
             const uint32_t nmma = (uint32_t)((w.n_cs + 15) & ~15);
             const uint32_t idesc = (1u << 4) | ((nmma >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
             const bool two = (w.mp * 256 + 128) < p.m;          // second m-tile has rows
@@ -331,16 +309,12 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                     const uint64_t bd = ptx::smem_desc_swizzled(sbase + kOffB + (uint32_t)b * p.b_bytes, 128u, 1024u);
 #pragma unroll
                     for (int ks = 0; ks < kKc / 16; ++ks) {   // K = 16 per MMA: +32 B inside the SW128 rows
-                        if (nmma == 0) break;                   // empty dummy window (cluster padding)
                         const uint32_t acc = (kc != w.kc0 || ks != 0) ? 1u : 0u;
                         ptx::mma_f16_ss(tmem_base, a0 + (uint64_t)(ks * 2), bd + (uint64_t)(ks * 2), idesc, acc);
                         if (two)
                             ptx::mma_f16_ss(tmem_base + 256u, a1 + (uint64_t)(ks * 2), bd + (uint64_t)(ks * 2), idesc, acc);
                     }
-                    if constexpr (CL == 1)
-                        ptx::tc_commit(bar_aempty + 8 * st);
-                    else
-                        ptx::tc_commit_mc(bar_aempty + 8 * st, kMask);   // frees the A slot in every CTA
+                    ptx::tc_commit(bar_aempty + 8 * st);
                     ptx::tc_commit(bar_bempty + 8 * b);
                     if (kc == w.kc1 - 1) ptx::tc_commit(bar_dfull);
                     ftrace(p, 3, ntr);
@@ -365,7 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         uint32_t dph = 0;
         for (int u = cid; u < p.n_units; u += n_cl) {
             FUnit w;
-            decode_funit<CL>(p, u, rank, w);
+            decode_funit(p, u, w);
             ptx::mbar_wait(bar_dfull, dph);
             ptx::tc_fence_after();
             for (int half = 0; half < 2; ++half) {
@@ -394,10 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
     }
 
     ptx::tc_fence_before();
-    if constexpr (CL > 1)
-        ptx::cluster_sync();   // no CTA exits while a peer may still multicast into it
-    else
-        __syncthreads();
+    __syncthreads();
     ptx::tc_fence_after();
     if (warp == kMmaWarp) ptx::tmem_dealloc(tmem_base, kTmemCols);
 }

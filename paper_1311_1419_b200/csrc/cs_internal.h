@@ -116,8 +116,6 @@ struct cs_encoder {
     std::vector<csenc::host::Plan> candidates;  // planner's ranked plans (autotune)
     int chained_plan = -1;         // best KEY_STREAMED candidate (previous-frame reference), -1 = none
     int row_plan = -1;             // best candidate with <= kRowSlots block rows per tile (CS_Q16_ROW), -1 = none
-    int frame1_plan = -1;          // f1 single-pass plan: D ring >= 2 (look-back lag >= 1), tiles <= SMs; -1 = none
-    csenc::host::Plan frame1{};                 // that candidate with the D ring as deep as TMEM allows (<= 8)
     void* phis_dev = nullptr;      // per-GOP Phi copies (arranged like phi_dev), n_phis of phi_bytes
     int n_phis = 0;
     int tuned = -1;                // index of the autotuned plan, -1 = model choice

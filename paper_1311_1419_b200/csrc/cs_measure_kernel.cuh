@@ -53,9 +53,6 @@ constexpr int kEpiWarp0 = 8;                     // warps 8..11: epilogue warpgr
 constexpr int kProducerWarp = 12;                // TMA producer
 constexpr int kMmaWarp = 13;                     // MMA issuer + TMEM allocator
 constexpr int kThreads = 14 * 32;
-constexpr int kPubWarp = 14;                     // EPI_Q16F only: publishes per-frame maxima (15 warps)
-template <int EPI>
-constexpr int threads_for() { return EPI == 2 ? 15 * 32 : kThreads; }
 constexpr int kMaxFolds = 8;
 constexpr int kMaxStages = 8;
 constexpr int kMaxTmemBufs = 8;                  // TMEM A buffers / accumulators (ring depth cap)
@@ -69,7 +66,7 @@ enum KeyMode : int { KEY_STREAMED = 0, KEY_RESIDENT = 1, KEY_REGS = 2, KEY_CHUNK
 enum Epilogue : int {
     EPI_F32 = 0,    // fp32 measurements
     EPI_Q16 = 1,    // Q_ABSMAX / Q_FRAME (the two passes of the per-frame scale)
-    EPI_Q16F = 2,   // Q_FRAME1 look-back only
+    // (2: a single-pass per-frame look-back mode, measured slower than two passes and removed in round 2)
     EPI_Q16R = 3,   // Q_ROW, general (two TMEM passes, named barrier)
     EPI_Q16RR = 4,  // Q_ROW, register path: one fold, M = 16 or 32, <= kRowRegRows block rows
     EPI_Q16RR64 = 5,  // the same for M = 48 or 64
@@ -82,14 +79,8 @@ enum QMode : int {
     Q_ABSMAX = 1,     // pass 1 of the per-frame scale: atomicMax of |y| bits into amax[cs], no stores
     Q_FRAME = 2,      // pass 2: codes with scale = amax[cs] / 32767 (1 if 0)
     Q_ROW = 3,        // single pass: one scale per (CS frame, block row), reduced in SMEM
-    Q_FRAME1 = 4,     // single pass, per-frame scale: decoupled look-back over GOP-aligned rounds
     Q_STOREMAX = 5,   // EPI_F32A: fp32 y to a workspace + atomicMax of |y| bits into amax[cs]
 };
-constexpr int kMaxLag = 7;                       // Q_FRAME1: items held in TMEM before quantising (<= ring-1);
-                                                 // kMaxLag + 1 must be a power of two (pending ring)
-constexpr uint32_t kPubBarOff = 512;             // Q_FRAME1: pub_full[8], pub_empty[8] (barrier page 512..639)
-constexpr uint32_t kPubSlotOff = 640;            // Q_FRAME1: 8 slots x (4 maxima + cs index) = 8 x 32 B
-constexpr int kPubSlots = 8;
 constexpr int kRowSlots = 40;                    // Q_ROW: max block rows per tile (3 x 40 u32 slots)
 constexpr uint32_t kRowSlotOff = 512;            // Q_ROW slots live in the barrier page (bytes 512..991)
 static_assert(16 * kMaxStages + 32 + 32 * kMaxTmemBufs + 24 <= (int)kRowSlotOff, "barrier block overlaps row slots");
@@ -164,10 +155,8 @@ struct KParams {
     // EPI_Q16 (f1)
     int qmode;                // QMode
     int16_t* codes;           // [n_cs][nblk][M] int16, same layout as out
-    uint32_t* amax;           // Q_ABSMAX / Q_FRAME / Q_FRAME1: [n_cs] fp32 |y| max bits (zeroed)
-    float* scales;            // Q_ROW: [n_cs][nby] fp32 scales; Q_FRAME1: [n_cs]
-    unsigned* arrivals;       // Q_FRAME1: [n_cs] contributions so far (zeroed); complete at n_tiles
-    int lookback;             // Q_FRAME1: lag in items (1 .. min(n_dbuf - 1, kMaxLag))
+    uint32_t* amax;           // Q_ABSMAX / Q_FRAME / Q_STOREMAX: [n_cs] fp32 |y| max bits (zeroed)
+    float* scales;            // Q_ROW: [n_cs][nby] fp32 scales
 };
 
 // KEY_STREAMED kernels' parameters: + the strip tensor map (frames as u32 words [n_seq*T][nby][B][W/4],
@@ -440,7 +429,7 @@ __device__ __forceinline__ float q16_scale(uint32_t amax_bits) {
 __device__ __forceinline__ float q16_inv(float scale) { return __frcp_rn(scale); }
 
 template <int B, int KM, int EPI>
-__global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const __grid_constant__ KParamsFor<KM> p) {
+__global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_constant__ KParamsFor<KM> p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t sbase = (ptx::smem_addr(smem_raw) + 1023u) & ~1023u;
     const uint8_t* const smem_ptr = smem_raw + (sbase - ptx::smem_addr(smem_raw));   // sbase as a C++ pointer
@@ -503,11 +492,6 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         ptx::mbar_init(bar_phi_empty, 1);
         if (EPI == EPI_Q16RR || EPI == EPI_Q16RR64)
             for (int i = 0; i < kRowBufs; ++i) ptx::mbar_init(sbase + kRowBarOff + 8 * i, 4);   // row_full
-        if (EPI == EPI_Q16F)
-            for (int i = 0; i < kPubSlots; ++i) {
-                ptx::mbar_init(sbase + kPubBarOff + 8 * i, 4);                   // pub_full: 4 epilogue warps
-                ptx::mbar_init(sbase + kPubBarOff + 8 * (kPubSlots + i), 1);    // pub_empty: the publisher
-            }
         ptx::fence_mbarrier_init();
     }
     if (warp == kMmaWarp) {
@@ -676,35 +660,6 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                         st = 0;
                         ph ^= 1u;
                     }
-                }
-            }
-        }
-    } else if (EPI == EPI_Q16F && warp == kPubWarp) {
-        // ================================================================ publisher (Q_FRAME1)
-        // Per item: the 4 epilogue warps' |y| maxima (SMEM slot) -> one atomicMax on the frame's bits,
-        // a fence (this thread has no other outstanding stores, so it is cheap) and one arrival.
-        int ps = 0;
-        uint32_t pph = 0;
-        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-            Unit w;
-            if (!decode_unit(p, u, w)) continue;
-            for (int c = w.c0; c < w.c1; ++c) {
-                ptx::mbar_wait(sbase + kPubBarOff + 8 * ps, pph);
-                if (lane == 0) {
-                    const uint32_t slot = sbase + kPubSlotOff + (uint32_t)ps * 32u;
-                    const uint32_t m = max(max(ptx::lds32(slot), ptx::lds32(slot + 4)),
-                                           max(ptx::lds32(slot + 8), ptx::lds32(slot + 12)));
-                    const uint2 csv = ptx::lds64(slot + 16);
-                    const long long cs = (long long)(((uint64_t)csv.y << 32) | csv.x);
-                    ptx::mbar_arrive(sbase + kPubBarOff + 8 * (kPubSlots + ps));   // slot read: free it
-                    if (m != 0) atomicMax(p.amax + cs, m);
-                    __threadfence();
-                    atomicAdd(p.arrivals + cs, 1u);
-                }
-                __syncwarp();
-                if (++ps == kPubSlots) {
-                    ps = 0;
-                    pph ^= 1u;
                 }
             }
         }
@@ -942,7 +897,9 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                             ++n_items;
                             continue;
                         }
+#ifndef CSENC_INJECT_RACE
                         ptx::mbar_wait(bar_a_empty + 8 * ab, aph ^ 1u);
+#endif
                         ptx::tc_fence_after();
                         if (tr) trace_ev(p, EV_C_AEMPTY, n_items);
                         const uint32_t cs_base = s_stage + (uint32_t)st * p.stage_bytes;
@@ -954,13 +911,14 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
 #pragma unroll
                         for (int j = 0; j < 2; ++j) {
                             if (wg + 2 * j < n_groups) {
-                                CS_CHECK(g_off[j] + (uint32_t)((kRowsPerSt - 1) * p.W + B) <= p.set_bytes + 128u);
+                                // the CS part of the slot (pieces 128-B aligned); a right half beyond W is not read
+                                CS_CHECK(g_off[j] + (uint32_t)((kRowsPerSt - 1) * p.W + (g_half2[j] ? B : B / 2)) <= p.stage_cs_bytes);
                                 CS_CHECK(g_acol[j] + 32u <= (uint32_t)p.a_cols);
                                 uint32_t cw[kRowsPerSt][8];
 #pragma unroll
                                 for (int rr = 0; rr < kRowsPerSt; ++rr) {
                                     const uint4* src = reinterpret_cast<const uint4*>(cs_ptr + g_off[j] + (uint32_t)(rr * p.W));
-                                    const uint4 a = src[0], b = src[1];
+                                    const uint4 a = src[0], b = g_half2[j] ? src[1] : make_uint4(0u, 0u, 0u, 0u);
                                     cw[rr][0] = a.x, cw[rr][1] = a.y, cw[rr][2] = a.z, cw[rr][3] = a.w;
                                     cw[rr][4] = b.x, cw[rr][5] = b.y, cw[rr][6] = b.z, cw[rr][7] = b.w;
                                 }
@@ -1078,7 +1036,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
                                          : "r"(tab_lane + (uint32_t)(f * 1024)));
                             off += (uint32_t)(r0 * p.W);
                             const bool half2 = (meta >> 16) & 1u;
-                            CS_CHECK(off + (uint32_t)((kRowsPerSt - 1) * p.W + B) <= p.set_bytes + 128u);
+                            CS_CHECK(off + (uint32_t)((kRowsPerSt - 1) * p.W + (half2 ? B : B / 2)) <= p.stage_cs_bytes);
                             CS_CHECK((uint32_t)(f * (p.chunk_k / 2) + r0 * kWords + 32) <= (uint32_t)p.a_cols);
                             uint32_t v[32];
 #pragma unroll
@@ -1133,7 +1091,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         const uint32_t stage_tile = sbase + p.off_epi + (uint32_t)ew * 4096u;
         // the mode is fixed by the instantiation where it can be (dead modes compile away)
         const int qmode = (EPI == EPI_Q16R || EPI == EPI_Q16RR || EPI == EPI_Q16RR64) ? (int)Q_ROW
-                        : EPI == EPI_Q16F ? (int)Q_FRAME1 : (p.qmode == Q_ABSMAX ? (int)Q_ABSMAX : (int)Q_FRAME);
+                        : (p.qmode == Q_ABSMAX ? (int)Q_ABSMAX : (int)Q_FRAME);
         const int smode = (p.M == 4) ? 0 : ((p.M & 7) == 0 ? 1 : 2);   // store mode
         // Q_ROW: block row (within the tile) of this lane's block in fold f, and the warp's lowest /
         // highest row in fold f, 6 bits per fold (rows < kRowSlots <= 63; fixed for the kernel)
@@ -1154,164 +1112,7 @@ __global__ void __launch_bounds__(threads_for<EPI>(), 1) cs_measure_kernel(const
         uint32_t dph = 0;
         int n_items = 0;
         const bool tr = (warp == kEpiWarp0 && lane == 0);
-        if constexpr (EPI == EPI_Q16F) {
-            // Per item: this warp's |y| maximum -> atomicMax on the frame's bits, then (after a fence)
-            // one arrival (through the publisher warp); the item `lookback` items back is quantised
-            // once its frame has all n_tiles arrivals.  Units are (tile, whole GOP) and the grid is a multiple of
-            // n_tiles, so all tiles of a GOP run in the same round r = u / gridDim.x and the
-            // contributions to CS frame c of the GOP are made at position (r, c) of every CTA's
-            // sequence; a CTA waits for (r, c) at position (r, c + lookback) or later.  Every wait
-            // depends only on lexicographically earlier positions (all CTAs resident: cooperative
-            // launch), so the look-back cannot deadlock.
-            int pdb[kMaxLag + 1], pblk0[kMaxLag + 1], pbh[kMaxLag + 1], pt[kMaxLag + 1];
-            long long pcs[kMaxLag + 1];
-            int npend = 0, phead = 0;
-            const int lag = p.lookback;
-            const unsigned target = (unsigned)p.n_tiles;
-            int ps = 0;
-            uint32_t pph = 0;
-            auto quantise = [&](int qdb, long long cs, int blk0, int blocks_here, int t) {
-                uint32_t am = 0;
-                if (lane == 0) {
-                    const unsigned long long t0 = ptx::globaltimer_ns();
-                    unsigned n;
-                    while (!(dbg_flags & 16)) {   // (debug 16: no wait -- timing experiments only)
-                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(n) : "l"(p.arrivals + cs) : "memory");
-                        if (n >= target) break;
-                        __nanosleep(100);
-                        if (ptx::globaltimer_ns() - t0 > 20000000000ULL) __trap();   // 20 s watchdog
-                    }
-                    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(am) : "l"(p.amax + cs) : "memory");
-                }
-                am = __shfl_sync(0xFFFFFFFFu, am, 0);
-                CS_CHECK((cs + 1) * p.nblk * (long long)p.M <= p.out_floats);
-                if (tr) trace_ev(p, EV_C_AEMPTY, n_items);   // look-back wait done
-                const float inv = q16_inv(q16_scale(am));
-                if (t == 0 && ew == 0 && lane == 0) p.scales[cs] = q16_scale(am);
-                const uint32_t d_tm = tmem_base + lane_bits + d_col0 + (uint32_t)qdb * (uint32_t)p.d_cols;
-                int16_t* const codes_cs = p.codes + (cs * p.nblk + blk0) * (long long)p.M;
-                for (int f = 0; f < p.F; ++f) {
-                    const int row0 = f * p.L + ew * p.Lq;
-                    const int b = row0 + (int)lane;
-                    const bool valid = (int)lane < p.Lq && ew * p.Lq + (int)lane < p.L && b < blocks_here;
-                    const int rows_valid = min(p.Lq, min(p.L - ew * p.Lq, blocks_here - row0));
-                    if (smode == 0) {
-                        uint32_t v[16];
-                        ptx::tmem_ld_32x32b_x16(d_tm + (uint32_t)(f * p.Mpad), v);
-                        ptx::tc_wait_ld();
-                        if (valid)
-                            ptx::stg64(codes_cs + (long long)b * 4, q16_pack(v[0], v[1], inv), q16_pack(v[2], v[3], inv));
-                        continue;
-                    }
-                    for (int j0 = 0; j0 < p.Mpad; j0 += 32) {
-                        const int cw = min(32, p.Mpad - j0);
-                        uint32_t v[32];
-                        if (cw == 32) {
-                            ptx::tmem_ld_32x32b_x32(d_tm + (uint32_t)(f * p.Mpad + j0), v);
-                        } else {
-                            ptx::tmem_ld_32x32b_x16(d_tm + (uint32_t)(f * p.Mpad + j0),
-                                                    *reinterpret_cast<uint32_t(*)[16]>(v));
-                        }
-                        ptx::tc_wait_ld();
-                        if (smode == 2) {
-                            if (valid) {
-                                int16_t* dst = codes_cs + (long long)b * p.M + j0;
-#pragma unroll
-                                for (int q = 0; q < 32; ++q)
-                                    if (q < cw && j0 + q < p.M) dst[q] = (int16_t)(q16_bits(v[q], inv) & 0xFFFFu);
-                            }
-                            continue;
-                        }
-                        uint32_t wd[16];
-#pragma unroll
-                        for (int q = 0; q < 16; ++q) wd[q] = q16_pack(v[2 * q], v[2 * q + 1], inv);
-                        uint32_t* dst_row0 = reinterpret_cast<uint32_t*>(codes_cs + (long long)row0 * p.M + j0);
-                        if (cw == 32)
-                            stage_store_codes<4>(wd, stage_tile, lane, dst_row0, p.M / 2, j0 / 2, p.M / 2, rows_valid);
-                        else
-                            stage_store_codes<2>(wd, stage_tile, lane, dst_row0, p.M / 2, j0 / 2, p.M / 2, rows_valid);
-                    }
-                }
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(bar_d_empty + 8 * qdb);
-            };
-            for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-                Unit w;
-                if (!decode_unit(p, u, w)) continue;
-                const int rows_here = min(p.T_r, p.nby - w.t * p.T_r);
-                const int blocks_here = rows_here * p.nbx;
-                const int blk0 = w.t * p.T_r * p.nbx;
-              for (int c = w.c0; c < w.c1; ++c) {
-                const long long cs_global = (long long)w.s * p.cs_per_stream_sel +
-                                            (long long)(w.g - p.gop_begin) * (p.G - 1) + c;
-                ptx::mbar_wait(bar_d_full + 8 * db, dph);
-                ptx::tc_fence_after();
-                if (tr) trace_ev(p, EV_E_DFULL, n_items);
-                const uint32_t d_tm = tmem_base + lane_bits + d_col0 + (uint32_t)db * (uint32_t)p.d_cols;
-                float mff = 0.0f;
-                for (int f = 0; f < p.F; ++f) {
-                    const int b = f * p.L + ew * p.Lq + (int)lane;
-                    const bool valid = (int)lane < p.Lq && ew * p.Lq + (int)lane < p.L && b < blocks_here;
-                    float mf = 0.0f;
-                    for (int j0 = 0; j0 < p.Mpad; j0 += 32) {
-                        uint32_t v[32];
-                        if (p.Mpad - j0 >= 32) {
-                            ptx::tmem_ld_32x32b_x32(d_tm + (uint32_t)(f * p.Mpad + j0), v);
-                        } else {
-                            ptx::tmem_ld_32x32b_x16(d_tm + (uint32_t)(f * p.Mpad + j0),
-                                                    *reinterpret_cast<uint32_t(*)[16]>(v));
-#pragma unroll
-                            for (int q = 16; q < 32; ++q) v[q] = 0;
-                        }
-                        ptx::tc_wait_ld();
-#pragma unroll
-                        for (int q = 0; q < 32; ++q) mf = fmaxf(mf, fabsf(__uint_as_float(v[q])));
-                    }
-                    if (valid) mff = fmaxf(mff, mf);
-                }
-                const uint32_t mx = __reduce_max_sync(0xFFFFFFFFu, __float_as_uint(mff));
-                // hand the warp's maximum to the publisher warp (slot ring, 4 arrivals per slot)
-                ptx::mbar_wait(sbase + kPubBarOff + 8 * (kPubSlots + ps), pph ^ 1u);
-                if (lane == 0) {
-                    const uint32_t slot = sbase + kPubSlotOff + (uint32_t)ps * 32u;
-                    ptx::sts32(slot + 4u * (uint32_t)ew, mx);
-                    if (ew == 0)
-                        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(slot + 16), "r"((uint32_t)cs_global),
-                                     "r"((uint32_t)((uint64_t)cs_global >> 32)) : "memory");
-                    ptx::mbar_arrive(sbase + kPubBarOff + 8 * ps);
-                }
-                __syncwarp();
-                if (++ps == kPubSlots) {
-                    ps = 0;
-                    pph ^= 1u;
-                }
-                if (tr) trace_ev(p, EV_M_AFULL, n_items);      // contribution handed over
-                {   // pending ring (head..head+npend-1, mod kMaxLag+1)
-                    const int tail = (phead + npend) & kMaxLag;
-                    pdb[tail] = db;
-                    pcs[tail] = cs_global;
-                    pblk0[tail] = blk0;
-                    pbh[tail] = blocks_here;
-                    pt[tail] = w.t;
-                    ++npend;
-                }
-                if (npend > lag) {
-                    quantise(pdb[phead], pcs[phead], pblk0[phead], pbh[phead], pt[phead]);
-                    phead = (phead + 1) & kMaxLag;
-                    --npend;
-                }
-                if (tr) trace_ev(p, EV_E_DONE, n_items);
-                ++n_items;
-                if (++db == p.n_dbuf) {
-                    db = 0;
-                    dph ^= 1u;
-                }
-              }
-            }
-            for (; npend > 0; --npend, phead = (phead + 1) & kMaxLag)
-                quantise(pdb[phead], pcs[phead], pblk0[phead], pbh[phead], pt[phead]);
-        } else if constexpr (EPI == EPI_Q16RR || EPI == EPI_Q16RR64) {
+        if constexpr (EPI == EPI_Q16RR || EPI == EPI_Q16RR64) {
             constexpr int NV = EPI == EPI_Q16RR ? 32 : 64;   // accumulator columns held in registers
             CS_CHECK(p.F == 1 && p.Mpad <= NV && p.Mpad == p.M && p.T_r <= kRowRegRows);
             // Q_ROW, register path (M = 16..64, one fold): the accumulator is read from TMEM once and

@@ -100,13 +100,36 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t bar, uint32_t parit
 }
 // Wait for the phase with the given parity to complete.  A watchdog traps after ~20 s so a
 // protocol bug surfaces as a launch error instead of a hung GPU.
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    if (mbar_try_wait(bar, parity)) return;
-    uint64_t t0 = globaltimer_ns();
-    uint32_t n = 0;
-    while (!mbar_try_wait(bar, parity)) {
-        if (((++n) & 1023u) == 0u && globaltimer_ns() - t0 > 20000000000ull) __trap();
+#if CSENC_CHECKS
+// Race gate (CSENC_CHECKS builds): when g_csenc_stress != 0 (set from CSENC_STRESS by the host), every
+// mbarrier wait is followed, one time in four, by a pseudo-random delay of up to ~2 us, so every role
+// runs ahead of / behind the others in orders the normal schedule never produces; a missing wait,
+// a wrong parity or a buffer reused too early then shows up as a parity mismatch or a hang (the
+// 20 s watchdog traps).
+__device__ unsigned int g_csenc_stress;
+__device__ __forceinline__ void stress_point(uint32_t salt) {
+    const uint32_t s = *reinterpret_cast<volatile unsigned int*>(&g_csenc_stress);
+    if (s != 0u) {
+        uint32_t h = (uint32_t)clock64() * 0x9E3779B1u ^ salt * 0x85EBCA6Bu ^ s * 0xC2B2AE35u ^ blockIdx.x;
+        h ^= h >> 15;
+        h *= 0x2C1B3C6Du;
+        h ^= h >> 12;
+        if ((h & 3u) == 0u) __nanosleep(h >> 21);
     }
+}
+#else
+__device__ __forceinline__ void stress_point(uint32_t) {}
+#endif
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    if (!mbar_try_wait(bar, parity)) {
+        uint64_t t0 = globaltimer_ns();
+        uint32_t n = 0;
+        while (!mbar_try_wait(bar, parity)) {
+            if (((++n) & 1023u) == 0u && globaltimer_ns() - t0 > 20000000000ull) __trap();
+        }
+    }
+    stress_point(bar);
 }
 
 // ------------------------------------------------------------------ TMA

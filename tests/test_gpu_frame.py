@@ -119,11 +119,8 @@ def test_frame_args():
     assert y.numel() == 0
 
 
-@pytest.mark.parametrize("two_sm", ["0", "1"])
-def test_frame_paths_single_cta_and_pair(two_sm, monkeypatch):
-    """Both frame-GEMM kernels -- K4 (one CTA per tile) and K4b (CTA pairs, 2-SM MMA, opt-in) -- give
-    the oracle's measurements (windows within and across streams, split-K)."""
-    monkeypatch.setenv("CSENC_FRAME_2SM", two_sm)
+def test_frame_windows_and_split_k():
+    """K4 gives the oracle's measurements with windows within and across streams and split-K."""
     for (W, H, G, T, S, m) in [(176, 144, 5, 40, 4, 507), (64, 16, 3, 8, 3, 100), (48, 32, 4, 11, 2, 300)]:
         cfg = synth.CONFIGS["C1"].with_(W=W, H=H, G=G, T=T, S=S)
         frames = synth.gen_video(cfg)

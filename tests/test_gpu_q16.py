@@ -249,29 +249,11 @@ def test_q16_bad_args():
     assert c.numel() == 0 and s.numel() == 0
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
-def test_q16_frame_single_pass_equals_two_pass(name):
-    """The single-pass per-frame mode (GOP-round look-back) and the two-pass mode quantise the
-    same fp32 measurements with the same per-frame maxima: bitwise identical codes and scales; and
-    both match the oracle."""
-    base = synth.CONFIGS[name]
-    cfg = base.with_(T=min(base.T, 2 * base.G + 3), S=min(base.S, 3))
-    frames = synth.gen_video(cfg)
-    fd = torch.from_numpy(frames).cuda()
-    for M in base.Ms[:2]:
-        phi = synth.phi_from_seed(synth.phi_seed(), M, cfg.B ** 2)
-        enc = P.Encoder(cfg.W, cfg.H, cfg.G, cfg.B, M, phi)
-        c1, s1 = run_q16(enc, fd, P.Encoder.Q16_FRAME_1PASS)
-        c2, s2 = run_q16(enc, fd, P.Encoder.Q16_FRAME)
-        assert torch.equal(c1, c2) and torch.equal(s1, s2)
-        y, S = oracle.encode(frames, phi, cfg.G, cfg.B)
-        check_q16(c1.cpu().numpy(), s1.cpu().numpy(), y, S, enc.nby, enc.nbx, P.Encoder.Q16_FRAME)
-
-
 @pytest.mark.parametrize("name,M", [("C4", 16), ("C4", 32), ("C5", 4), ("C3", 64)])
-def test_q16_frame_store_path_equals_two_pass(name, M, monkeypatch):
-    """CS_Q16_FRAME with 8 M <= N stores y and re-quantises it; the two-pass path (CSENC_Q16_STORE=0)
-    measures twice.  Same codes and scales, bit for bit."""
+def test_q16_frame_store_path_bitwise(name, M):
+    """CS_Q16_FRAME with 8 M <= N stores y and re-quantises it (one measurement pass).  Bitwise: the
+    scales are fl32(max|y_gpu| / 32767) of the fp32 kernel's own output and the codes are the kernel's
+    fp32 decision on that output (kernel_fp32_decision); and the oracle check with the tie band."""
     base = synth.CONFIGS[name]
     cfg = base.with_(T=min(base.T, 2 * base.G + 3), S=min(base.S, 2))
     frames = synth.gen_video(cfg)
@@ -279,11 +261,13 @@ def test_q16_frame_store_path_equals_two_pass(name, M, monkeypatch):
     phi = synth.phi_from_seed(synth.phi_seed(), M, cfg.B ** 2)
     enc = P.Encoder(cfg.W, cfg.H, cfg.G, cfg.B, M, phi)
     assert 8 * M <= cfg.B ** 2
-    monkeypatch.setenv("CSENC_Q16_STORE", "1")
     c1, s1 = run_q16(enc, fd, P.Encoder.Q16_FRAME)
-    monkeypatch.setenv("CSENC_Q16_STORE", "0")
-    c0, s0 = run_q16(enc, fd, P.Encoder.Q16_FRAME)
+    y32 = enc.encode_batch(fd)
     torch.cuda.synchronize()
-    assert torch.equal(c0, c1) and torch.equal(s0, s1)
+    y32 = y32.cpu().numpy()
+    amax = np.abs(y32).reshape(y32.shape[0], -1).max(axis=1)
+    want_s = np.where(amax > 0, (amax / np.float32(32767)).astype(np.float32), np.float32(1.0))
+    assert np.array_equal(s1.cpu().numpy(), want_s)
+    assert np.array_equal(c1.cpu().numpy(), kernel_fp32_decision(y32, want_s[:, None, None]))
     y, S = oracle.encode(frames, phi, cfg.G, cfg.B)
     check_q16(c1.cpu().numpy(), s1.cpu().numpy(), y, S, enc.nby, enc.nbx, P.Encoder.Q16_FRAME)

@@ -15,7 +15,6 @@ run C3 --workload C3
 run C5 --workload C5
 run C4_q16row --output q16row
 run C4_q16frame --output q16frame
-run C4_q16frame1 --output q16frame1
 run C4_adjoint --op adjoint
 run C5_adjoint --op adjoint --workload C5
 run C4_closed_loop --op closed_loop --tune-file $OUT/plans.json
