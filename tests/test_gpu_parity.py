@@ -313,6 +313,30 @@ def test_all_candidate_plans_bitwise_identical():
         assert torch.equal(out, ref) and chosen["smem_bytes"] > 0
 
 
+@pytest.mark.parametrize("M", [16, 32, 64, 128])
+def test_bench_candidate_plans_bitwise_identical_c4(M):
+    """bench.py autotunes among the top 12 plans of every C4 M; each of them gives the same bits as the
+    first, which is checked against the oracle -- so whichever plan the bench times is a checked plan.
+    T = 2G + 3 = 19: two full GOPs and a ragged third."""
+    base = synth.CONFIGS["C4"]
+    cfg = base.with_(T=2 * base.G + 3, S=1)
+    frames = synth.gen_video(cfg)
+    fd = torch.from_numpy(frames).cuda()
+    phi = synth.phi_from_seed(synth.phi_seed(), M, cfg.B ** 2)
+    enc = P.Encoder(cfg.W, cfg.H, cfg.G, cfg.B, M, phi)
+    n = min(enc.num_candidates(), 12)
+    ref = None
+    for i in range(n):
+        plan = enc.set_candidate(i)
+        out = enc.encode_batch(fd)
+        torch.cuda.synchronize()
+        if ref is None:
+            ref = out.clone()
+            assert_parity(out.cpu().numpy(), frames, phi, cfg.G, cfg.B)
+        else:
+            assert torch.equal(out, ref), (M, i, plan)
+
+
 def test_host_multi_encoder_path():
     """cs_encode_batch_host_multi: several encoders (different M and B) over the same host frames
     give exactly the device-path outputs; mismatched geometry is rejected."""
