@@ -609,8 +609,19 @@ def run_frame(args):
         "e2e": {"value": None, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                 "how": "not measured: the frame-level path has a device-buffer C-ABI call only"},
     }
+    # parity of the timed output (outside the timed region): every CS frame of the rank's first stream
+    # against the oracle; R24's worst-case bound and the observed max |dy|/S
+    import oracle
+    y0 = y[: oracle.cs_frame_count(T, G)].double().cpu().numpy()
+    yo, So = oracle.measure_frame(frames[0].cpu().numpy(), A, G)
+    d = np.abs(y0 - yo)
+    rel = np.where(So > 0, d / np.where(So > 0, So, 1.0), 0.0)
+    bound = (n / 16 + 16) * 2.0 ** -23
+    n_bad = int(((d > bound * So) | ((So == 0) & (y0 != 0))).sum())
+    line["parity"] = {"values": int(y0.size), "n_bad": n_bad, "max_rel": float(rel.max()), "bound_rel": bound,
+                      "ok": n_bad == 0, "how": "every CS frame of stream 0 of the timed output vs oracle.measure_frame "
+                                                "(|dy| <= (n/16+16) 2^-23 S, DESIGN R24)"}
     if not args.no_cpu_baseline and world == 1:   # (rank 0 at N=1 only)
-        import oracle
         fr = synth.gen_stream(cfg, 0, T=2 * G)
         t0 = time.perf_counter()
         oracle.measure_frame(fr, A, G, with_scale=False)

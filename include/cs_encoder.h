@@ -123,9 +123,10 @@ int cs_encoder_plan(const cs_encoder* enc, cs_plan_info* info);
  * Events: 0 producer slot free, 1 producer TMA issued, 2 converter data landed, 3 converter A
  * buffer free, 4 converter A written, 5 MMA A ready, 6 MMA issued+committed, 7 epilogue
  * accumulator ready, 8 epilogue done, 9 converter tcgen05.st issued, 10 / 11 (q16 row-scale register
- * path) epilogue row maxima published / all four warps' maxima present.  cap = 0 disables (default).
+ * path) epilogue row maxima published / all four warps' maxima present, 12 kernel entry and 13 CTA
+ * exit (one occurrence each).  cap = 0 disables (default).
  * Not thread-safe with concurrent encodes of the same encoder. */
-#define CS_TRACE_EVENTS 12
+#define CS_TRACE_EVENTS 14
 /* Profiling ranges: with CSENC_NVTX=1 in the environment (read once per process), every encode /
  * adjoint / key-codec / frame-encode entry point opens an NVTX range named after itself (ncu --nvtx,
  * nsys); header-only nvtx3, a no-op when no tool is attached. */

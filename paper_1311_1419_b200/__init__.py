@@ -245,7 +245,7 @@ class Encoder:
 
     # -- tracing (debug timeline of CTA 0; see include/cs_encoder.h)
     TRACE_EVENTS = ("p_empty", "p_issued", "c_full", "c_aempty", "c_done", "m_afull", "m_issued", "e_dfull",
-                    "e_done", "c_conv", "e_arrived", "e_rows")
+                    "e_done", "c_conv", "e_arrived", "e_rows", "k_start", "k_end")
 
     def set_trace(self, buf=None, cap: int = 0):
         """buf: CUDA int64 tensor of len(TRACE_EVENTS) * cap elements (None/0 disables)."""

@@ -182,6 +182,8 @@ enum : int {
     EV_C_CONV,        // converter: all tcgen05.st issued (before wait::st)
     EV_E_ARRIVED,     // epilogue (Q_ROW register path): row maxima published
     EV_E_ROWS,        // epilogue (Q_ROW register path): all 4 warps' row maxima present
+    EV_K_START,       // CTA 0 thread 0: kernel entry (one occurrence)
+    EV_K_END,         // CTA 0 thread 0: after the final barrier (one occurrence)
     EV_COUNT
 };
 
@@ -435,6 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
     const uint8_t* const smem_ptr = smem_raw + (sbase - ptx::smem_addr(smem_raw));   // sbase as a C++ pointer
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31u;
+    if (threadIdx.x == 0) trace_ev(p, EV_K_START, 0);
 #if CSENC_DEBUG
     const int dbg_load_only = p.dbg_load_only, dbg_flags = p.dbg_flags;
 #else
@@ -1449,6 +1452,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
+    if (threadIdx.x == 0) trace_ev(p, EV_K_END, 0);
     if (warp == kMmaWarp) ptx::tmem_dealloc(tmem_base, kTmemCols);
 }
 

@@ -106,6 +106,25 @@ def test_frame_paper_config_full_batch():
         check(y_gpu[s * n_cs:(s + 1) * n_cs], y, Sc, W * H)
 
 
+def test_frame_bench_batch_parity():
+    """The bench's exact launch (64 streams x 400 QCIF frames, m = 507; bench.py --op frame, R25):
+    three streams' CS frames (320 each) against the oracle.  Prints the observed max |dy|/S next to
+    the R24 worst-case bound (accumulation-order guarantee) and the north star's 1e-5."""
+    W, H, G, m, T, S = 176, 144, 5, 507, 400, 64
+    cfg = synth.CONFIGS["C1"].with_(W=W, H=H, G=G, T=T, S=S)
+    frames = synth.gen_video(cfg)
+    A = synth.phi_from_seed(synth.phi_seed(), m, W * H)
+    fe = P.FrameEncoder(W, H, G, m, A)
+    y_gpu = fe.encode_batch(torch.from_numpy(frames).cuda()).cpu().numpy()
+    n_cs = oracle.cs_frame_count(T, G)
+    worst = 0.0
+    for s in (0, 31, 63):
+        y, Sc = oracle.measure_frame(frames[s], A, G)
+        worst = max(worst, check(y_gpu[s * n_cs:(s + 1) * n_cs], y, Sc, W * H))
+    print(f"f2 bench batch: observed max |dy|/S = {worst:.3e}; R24 bound {rel_bound(W * H):.3e}; north star 1e-5")
+    assert worst < rel_bound(W * H)
+
+
 def test_frame_args():
     A = synth.phi_from_seed(1, 4, 32 * 16)
     with pytest.raises(P.CSError):

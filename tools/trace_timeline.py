@@ -54,6 +54,14 @@ def main(workload="C4", M=None, cap=256, T=None, q16=None):
         rep["  epilogue ld+reduce (e_arrived - e_dfull)"] = med(d["e_arrived"] - d["e_dfull"])
         rep["  epilogue row wait (e_rows - e_arrived)"] = med(d["e_rows"] - d["e_arrived"])
         rep["  epilogue scale+codes (e_done - e_rows)"] = med(d["e_done"] - d["e_rows"])
+    if "k_start" in ev and t[ev.index("k_end"), 0] > 0:
+        ks, ke = t[ev.index("k_start"), 0], t[ev.index("k_end"), 0]
+        ne_ = int((t[ev.index("e_done")] > 0).sum())
+        rep["CTA 0 kernel (k_end - k_start)"] = float(ke - ks)
+        rep["  prologue (first p_issued - k_start)"] = float(d["p_issued"][0] - ks)
+        rep["  fill (first e_done - first p_issued)"] = float(t[ev.index("e_done"), 0] - d["p_issued"][0])
+        rep["  drain (k_end - last e_done)"] = float(ke - t[ev.index("e_done"), ne_ - 1]) if ne_ else float("nan")
+        rep["  CS items / epilogue items of CTA 0"] = float(n * 1000 + ne_)
     for k, v in rep.items():
         print(f"  {k:45s} {v:9.0f} cycles")
     # utilisation over the traced window (items 2..n-2 to skip the prologue)
