@@ -523,18 +523,31 @@ namespace {
 // frame -- the same expressions as the K1 epilogue (q16_bits / q16_scale / q16_inv), so the codes are
 // bitwise those of the two-pass path.  8 measurements per thread and step (two 16-B loads, one 16-B
 // store); per_frame (= nblk * M) is a multiple of 8.
+// y is walked from its END: the measurement kernel wrote it front to back, so its last tens of MB are
+// still in L2 and are re-read from there; every fully consumed 128-B line of y is then discarded
+// (discard.global.L2: no write-back of a workspace nobody reads again).  y must be 128-B aligned.
 __global__ void q16_requant_kernel(const float4* __restrict__ y, const uint32_t* __restrict__ amax,
-                                   uint4* __restrict__ codes, long long n8, long long per8) {
+                                   uint4* __restrict__ codes, long long n8, long long per8, int discard) {
     const long long step = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += step) {
-        const float inv = csenc::q16_inv(csenc::q16_scale(__ldg(amax + i / per8)));
-        const float4 a = y[2 * i], b = y[2 * i + 1];
-        uint4 w;
-        w.x = csenc::q16_pack(__float_as_uint(a.x), __float_as_uint(a.y), inv);
-        w.y = csenc::q16_pack(__float_as_uint(a.z), __float_as_uint(a.w), inv);
-        w.z = csenc::q16_pack(__float_as_uint(b.x), __float_as_uint(b.y), inv);
-        w.w = csenc::q16_pack(__float_as_uint(b.z), __float_as_uint(b.w), inv);
-        codes[i] = w;
+    const int lane = (int)(threadIdx.x & 31u);
+    const long long start = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long rounds = (n8 + step - 1) / step;   // every thread runs the same trip count (warp-uniform loop)
+    for (long long r = 0; r < rounds; ++r) {
+        const long long i = n8 - 1 - (start + r * step);   // descending with the lane inside a warp
+        if (i >= 0) {
+            const float inv = csenc::q16_inv(csenc::q16_scale(__ldg(amax + i / per8)));
+            const float4 a = y[2 * i], b = y[2 * i + 1];
+            uint4 w;
+            w.x = csenc::q16_pack(__float_as_uint(a.x), __float_as_uint(a.y), inv);
+            w.y = csenc::q16_pack(__float_as_uint(a.z), __float_as_uint(a.w), inv);
+            w.z = csenc::q16_pack(__float_as_uint(b.x), __float_as_uint(b.y), inv);
+            w.w = csenc::q16_pack(__float_as_uint(b.z), __float_as_uint(b.w), inv);
+            codes[i] = w;
+        }
+        __syncwarp();   // the warp's loads have returned (their values were used)
+        // line i/4 (groups i..i+3, 128 B) was read by this lane and its three lower lanes
+        if (discard && i >= 0 && (i & 3) == 0 && lane >= 3 && i + 3 < n8)
+            asm volatile("discard.global.L2 [%0], 128;" ::"l"(y + 2 * i) : "memory");
     }
 }
 
@@ -913,7 +926,8 @@ int cs_encode_batch_q16(cs_encoder* e, const uint8_t* frames, int n_seq, int T, 
     cudaError_t err = cudaMemsetAsync(scales, 0, (size_t)n_cs * sizeof(float), st);
     if (err != cudaSuccess) return cuda_fail(err, "cudaMemsetAsync");
     const long long per_frame = (long long)g.nblk * g.M;
-    if (8 * g.M <= g.N && per_frame % 8 == 0 && env_int("CSENC_Q16_STORE", 1)) {
+    const int store_knob = env_int("CSENC_Q16_STORE", 1);   // (TUNING builds: 0 = never, 2 = for every M)
+    if ((8 * g.M <= g.N || store_knob == 2) && per_frame % 8 == 0 && store_knob) {
         float* ybuf = nullptr;
         err = scratch_alloc(e, (void**)&ybuf, (size_t)(n_cs * per_frame) * sizeof(float), st);
         if (err == cudaSuccess) {
@@ -923,7 +937,8 @@ int cs_encode_batch_q16(cs_encoder* e, const uint8_t* frames, int n_seq, int T, 
                 const long long n8 = n_cs * per_frame / 8;
                 const unsigned blocks = (unsigned)std::min<long long>((n8 + 255) / 256, (long long)e->sms * 16);
                 q16_requant_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(ybuf), q.amax,
-                                                          reinterpret_cast<uint4*>(codes), n8, per_frame / 8);
+                                                          reinterpret_cast<uint4*>(codes), n8, per_frame / 8,
+                                                          (reinterpret_cast<uintptr_t>(ybuf) & 127u) == 0 ? 1 : 0);
                 err = cudaGetLastError();
                 if (err == cudaSuccess) {
                     q16_finalize_kernel<<<(unsigned)((n_cs + 255) / 256), 256, 0, st>>>(q.amax, n_cs);

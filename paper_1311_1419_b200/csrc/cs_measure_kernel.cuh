@@ -496,10 +496,12 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
         if (EPI == EPI_Q16RR || EPI == EPI_Q16RR64)
             for (int i = 0; i < kRowBufs; ++i) ptx::mbar_init(sbase + kRowBarOff + 8 * i, 4);   // row_full
         ptx::fence_mbarrier_init();
+        trace_ev(p, EV_K_START, 1);   // (prologue split: barriers initialised)
     }
     if (warp == kMmaWarp) {
         ptx::tmem_alloc(tmem_slot, kTmemCols);
         ptx::tmem_relinquish();
+        if (lane == 0) trace_ev(p, EV_K_START, 2);   // TMEM allocated
     }
     if (warp < 4) {
         // Per (fold, lane) table: byte offset of the lane's block (its row 0 in the chunk) inside
@@ -520,11 +522,13 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
             const uint32_t e = sbase + p.off_tab + (uint32_t)(f * 128 + lane_idx) * 8u;
             asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(e), "r"(off), "r"(meta));
         }
+        if (threadIdx.x == 0) trace_ev(p, EV_K_START, 4);   // converter offset table written
     }
     if (EPI == EPI_Q16R && threadIdx.x < 3 * kRowSlots) ptx::sts32(sbase + kRowSlotOff + threadIdx.x * 4u, 0u);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
+    if (threadIdx.x == 0) trace_ev(p, EV_K_START, 3);   // all warps through the prologue barrier
     uint32_t tmem_base;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem_base) : "r"(tmem_slot));
 
@@ -545,6 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
             }
             __syncwarp();
         }
+        if (lane == 0) trace_ev(p, EV_K_START, 5);   // producer: Phi issued, schedule walk starts
         int pb = 0;          // KEY_CHUNK phi_slices: slice buffer and its phase
         uint32_t pbph = 0;
         int phi_cur = -1;

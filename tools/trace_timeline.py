@@ -50,7 +50,13 @@ def main(workload="C4", M=None, cap=256, T=None, q16=None):
         "tma latency (c_full - p_issued)": med(d["c_full"] - d["p_issued"]),
         "epilogue (e_done - e_dfull)": med(d["e_done"] - d["e_dfull"]),
     }
-    if (d["e_arrived"] > 0).any():
+    if q16 == 0 and (d["e_rows"] > 0).any():   # q16frame fused (EPI_F32Q): re-quantisation warps
+        ne = int((t[ev.index("e_done")] > 0).sum())
+        ea, er, ed = t[ev.index("e_arrived"), :ne], t[ev.index("e_rows"), :ne], t[ev.index("e_done"), :ne]
+        rep["requant wait (ready - epilogue done)"] = med(ea - ed)
+        rep["requant item (done - ready)"] = med(er - ea)
+        rep["requant lag at the end (last done - last epilogue)"] = float(er[-1] - ed[-1])
+    elif (d["e_arrived"] > 0).any():
         rep["  epilogue ld+reduce (e_arrived - e_dfull)"] = med(d["e_arrived"] - d["e_dfull"])
         rep["  epilogue row wait (e_rows - e_arrived)"] = med(d["e_rows"] - d["e_arrived"])
         rep["  epilogue scale+codes (e_done - e_rows)"] = med(d["e_done"] - d["e_rows"])
@@ -62,6 +68,11 @@ def main(workload="C4", M=None, cap=256, T=None, q16=None):
         rep["  fill (first e_done - first p_issued)"] = float(t[ev.index("e_done"), 0] - d["p_issued"][0])
         rep["  drain (k_end - last e_done)"] = float(ke - t[ev.index("e_done"), ne_ - 1]) if ne_ else float("nan")
         rep["  CS items / epilogue items of CTA 0"] = float(n * 1000 + ne_)
+        kst = t[ev.index("k_start")]
+        for j, what in ((1, "barriers initialised"), (2, "TMEM allocated"), (4, "offset table written"),
+                        (3, "prologue barrier passed"), (5, "producer: Phi issued")):
+            if kst[j] >= 0:
+                rep[f"    prologue: {what} (since k_start)"] = float(kst[j] - ks)
     for k, v in rep.items():
         print(f"  {k:45s} {v:9.0f} cycles")
     # utilisation over the traced window (items 2..n-2 to skip the prologue)
