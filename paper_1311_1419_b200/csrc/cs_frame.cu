@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -19,6 +20,10 @@ struct cs_frame_encoder {
     void* A_dev = nullptr;   // fp16 [m][n], columns permuted within groups of 4 (converter pair order)
     unsigned long long* trace = nullptr;   // debug timeline (cs_frame_encoder_set_trace)
     int trace_cap = 0;
+    // stream-ordered scratch for the stream-K partial tiles: the object's own pool, which keeps its memory
+    // between calls (release threshold = max), created on first use
+    cudaMemPool_t pool = nullptr;
+    std::mutex pool_mu;
 };
 
 extern "C" {
@@ -90,6 +95,7 @@ int cs_frame_encoder_set_trace(cs_frame_encoder* f, unsigned long long* trace_de
 int cs_frame_encoder_destroy(cs_frame_encoder* f) {
     if (!f) return CS_OK;
     if (f->A_dev) cudaFree(f->A_dev);
+    if (f->pool) cudaMemPoolDestroy(f->pool);
     delete f;
     return CS_OK;
 }
@@ -121,22 +127,17 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     if (!enc) return fail(CS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     const int G = f->G;
     const int n_gops = cdiv(T, G);
-    const int gw_max = std::max(1, 256 / G);          // box rows <= 256, CS rows <= 256
+    // window: CS rows <= 256 (MMA N, TMEM columns), frame rows <= 512 (two TMA boxes per chunk)
+    const int gw_max = std::max(1, std::min(G > 1 ? 256 / (G - 1) : 256, 512 / G));
     fp.n_mp = cdiv(f->m, 256);
     if (T % G == 0) {
-        // whole GOPs everywhere: windows over the concatenation, sized so the units fill the SMs in
-        // whole waves (k units per SM, the smallest k whose windows fit a box)
+        // whole GOPs everywhere: windows over the concatenation, as large as the MMA N / TMEM allow (the A
+        // tile is reused across the window's CS frames: A traffic per flop falls with the window; the
+        // stream-K split below balances the SMs whatever the unit count), equal-sized
         fp.global_win = 1;
         fp.total_gops = n_seq * n_gops;
         fp.gw = std::min(gw_max, fp.total_gops);
-        for (int k = 1; k <= 16; ++k) {
-            const long long want = ((long long)k * f->sms + fp.n_mp - 1) / fp.n_mp;
-            const long long gw = (fp.total_gops + want - 1) / want;
-            if (gw <= gw_max) {
-                fp.gw = (int)std::max(1LL, gw);
-                break;
-            }
-        }
+        fp.gw = cdiv(fp.total_gops, cdiv(fp.total_gops, fp.gw));
         if (const int gwf = env_int("CSENC_FRAME_GW", 0)) fp.gw = std::max(1, std::min(gw_max, gwf));   // experiment knob
         fp.n_win_s = 0;
         fp.n_win = cdiv(fp.total_gops, fp.gw);
@@ -150,10 +151,12 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
         fp.n_win = n_seq * fp.n_win_s;
     }
     fp.nf_box = fp.gw * G;
+    fp.n_fbox = cdiv(fp.nf_box, 256);
+    fp.fbox_rows = (int)align_up((uint32_t)cdiv(fp.nf_box, fp.n_fbox), 8);   // 512-B swizzle period per box
     {
         cuuint64_t dims[2] = {(cuuint64_t)f->n, (cuuint64_t)n_seq * T};
         cuuint64_t strides[1] = {(cuuint64_t)f->n};
-        cuuint32_t box[2] = {(cuuint32_t)csenc::frm::kKc, (cuuint32_t)fp.nf_box};
+        cuuint32_t box[2] = {(cuuint32_t)csenc::frm::kKc, (cuuint32_t)fp.fbox_rows};
         cuuint32_t estr[2] = {1, 1};
         CUresult r = enc(&fp.fmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(frames), dims, strides, box,
                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
@@ -177,18 +180,15 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     fp.cs_s = (int)cs_s;
 
     fp.n_chunks = cdiv(f->n, csenc::frm::kKc);
-    const long long n_cl = f->sms;                                      // CTAs resident at once
-    const long long tiles = (long long)fp.n_win * fp.n_mp;              // work units per K split
-    long long ks = (n_cl + tiles - 1) / tiles;                        // K splits to fill the SMs
-    ks = std::max(1LL, std::min(ks, (long long)std::max(1, fp.n_chunks / 8)));
-    if (const int ksf = env_int("CSENC_FRAME_KS", 0)) ks = std::max(1, std::min(ksf, fp.n_chunks));   // experiment knob
-    // no empty K split (every unit must issue at least one chunk): ks = ceil(chunks / per-split)
-    const long long per_split = (fp.n_chunks + ks - 1) / ks;
-    ks = (fp.n_chunks + per_split - 1) / per_split;
-    fp.n_ks = (int)ks;
-    if (tiles * ks > 0x7FFFFFFFLL) return fail(CS_ERR_UNSUPPORTED, "too many work units");
-    fp.n_units = (int)(tiles * ks);
-    fp.fbox_bytes = (uint32_t)fp.nf_box * (uint32_t)csenc::frm::kKc;
+    const long long tiles = (long long)fp.n_win * fp.n_mp;              // work units
+    if (tiles > 0x7FFFFFFFLL / 2) return fail(CS_ERR_UNSUPPORTED, "too many work units");
+    fp.n_units = (int)tiles;
+    fp.total_chunks = tiles * fp.n_chunks;
+    // stream-K grid: every SM, unless that leaves a CTA fewer than 8 chunks (pipeline fill per piece)
+    // (and at most 8 pieces per unit: ranges of >= n_chunks / 7 chunks)
+    const long long n_cl = std::max(1LL, std::min({(long long)f->sms, fp.total_chunks / 8,
+                                                   7 * fp.total_chunks / std::max(1, fp.n_chunks)}));
+    fp.fbox_bytes = (uint32_t)(fp.n_fbox * fp.fbox_rows) * (uint32_t)csenc::frm::kKc;
     fp.stage_bytes = align_up(fp.fbox_bytes, 1024);                    // frames ring slot
     const uint32_t a_slot = 256u * csenc::frm::kKc * 2u;                // A ring slot (32 KB)
     fp.b_bytes = align_up((uint32_t)(fp.gw * (G - 1) + 15) / 16 * 16 * 128u, 1024);
@@ -212,23 +212,46 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     fp.trace_cap = f->trace_cap;
     fp.out_floats = (long long)n_seq * cs_s * f->m;
     fp.smem_bytes = smem - 1024;
-    const long long ny = (long long)n_seq * cs_s * f->m;
+    fp.out = y;
+    const int grid = (int)n_cl;
+    // units cut by a range boundary (each boundary b = 1 .. grid-1 that is not a unit start); their
+    // pieces go to partial tiles (2 per CTA) summed by the fixup kernel
+    csenc::frm::FixupList fl;
+    fl.n = 0;
+    fl.grid = grid;
+    for (long long b = 1; b < grid; ++b) {
+        const long long c = b * fp.total_chunks / grid;
+        if (c % fp.n_chunks == 0) continue;
+        const int u = (int)(c / fp.n_chunks);
+        if (fl.n > 0 && fl.units[fl.n - 1] == u) continue;
+        if (fl.n == (int)(sizeof(fl.units) / sizeof(fl.units[0]))) return fail(CS_ERR_UNSUPPORTED, "too many split units");
+        fl.units[fl.n++] = u;
+    }
     float* part = nullptr;
     cudaError_t err;
-    if (fp.n_ks > 1) {
-        fp.part_stride = (ny + 3) / 4 * 4;
-        err = cudaMallocAsync((void**)&part, (size_t)fp.part_stride * fp.n_ks * sizeof(float), st);
-        if (err != cudaSuccess) return fail(CS_ERR_OOM, std::string("partials: ") + cudaGetErrorString(err));
-        fp.out = part;
-    } else {
-        fp.part_stride = 0;
-        fp.out = y;
+    if (fl.n > 0) {
+        {
+            std::lock_guard<std::mutex> lk(f->pool_mu);
+            if (!f->pool) {
+                cudaMemPoolProps props;
+                std::memset(&props, 0, sizeof(props));
+                props.allocType = cudaMemAllocationTypePinned;
+                props.location.type = cudaMemLocationTypeDevice;
+                props.location.id = f->device;
+                if (cudaMemPoolCreate(&f->pool, &props) != cudaSuccess) f->pool = nullptr;
+                uint64_t keep = ~0ull;
+                if (f->pool) cudaMemPoolSetAttribute(f->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+        }
+        err = f->pool ? cudaMallocFromPoolAsync((void**)&part, (size_t)2 * grid * 65536 * sizeof(float), f->pool, st)
+                      : cudaMallocAsync((void**)&part, (size_t)2 * grid * 65536 * sizeof(float), st);
+        if (err != cudaSuccess) return fail(CS_ERR_OOM, std::string("partial tiles: ") + cudaGetErrorString(err));
     }
-    const int grid = (int)std::max(1LL, std::min(n_cl, (long long)fp.n_units));
+    fp.part = part;
     csenc::frm::cs_frame_measure_kernel<<<grid, csenc::frm::kThreads, smem, st>>>(fp);
     err = cudaGetLastError();
-    if (err == cudaSuccess && fp.n_ks > 1) {
-        csenc::frm::cs_frame_reduce_kernel<<<f->sms * 4, 256, 0, st>>>(part, y, ny, fp.part_stride, fp.n_ks);
+    if (err == cudaSuccess && fl.n > 0) {
+        csenc::frm::cs_frame_fixup_kernel<<<dim3((unsigned)fl.n, 32), 64, 0, st>>>(fp, fl);
         err = cudaGetLastError();
     }
     if (part) cudaFreeAsync(part, st);

@@ -16,11 +16,15 @@
 // 14 A producer.  The frame boxes (from HBM, needed first: by the converters) and the A tiles (from L2,
 // needed last: by the MMA) run in two rings of their own depths, so the frames are fetched far ahead
 // (up to 8 chunks) while A occupies only the slots the MMA is about to use.
-// Unit = (K split, window of whole GOPs of one stream, pair of 128-row m-tiles = one 256-row A box);
-// item = one 64-pixel K chunk: one residual operand feeds both m-tiles' MMAs (D uses all 512 TMEM
-// columns), halving the conversion work and the frame-box traffic per flop.  With more than one K split the units write fp32 partials that a second kernel sums in a
-// fixed order (deterministic).  The epilogue's lane = measurement, so for each CS frame a warp
-// stores 32 consecutive measurements (128 B).
+// Unit = (window of whole GOPs, pair of 128-row m-tiles = one 256-row A box); item = one 64-pixel K
+// chunk: one residual operand feeds both m-tiles' MMAs (D uses all 512 TMEM columns), halving the
+// conversion work and the frame-box traffic per flop.  Work split (stream-K): the (unit, K chunk)
+// sequence is cut into gridDim.x equal ranges, one per CTA, so windows can be as large as a TMA box
+// allows (the per-chunk A traffic per flop falls with the window) while every SM gets the same number
+// of chunks.  A piece = the part of a CTA's range inside one unit; a unit done by one CTA is written
+// to y directly, the pieces of a unit cut by CTA boundaries go to per-CTA partial tiles that
+// cs_frame_fixup_kernel sums in CTA order (deterministic).  The epilogue's lane = measurement, so for
+// each CS frame a warp stores 32 consecutive measurements (128 B).
 #pragma once
 
 #include <cuda.h>
@@ -45,15 +49,20 @@ constexpr uint32_t kOffB = 1024;                 // two residual (B operand) buf
 struct FParams {
     CUtensorMap fmap;         // frames: 2-D [n_seq*T rows][n bytes], box [nf_box][64], SWIZZLE_64B
     CUtensorMap amap;         // A (permuted): 2-D [m rows][n fp16], box [256][64], SWIZZLE_128B
-    float* out;               // y [n_seq*cs_s][m] (n_ks == 1) or partials [n_ks][n_seq*cs_s][m]
+    float* out;               // y [n_seq*cs_s][m]
+    float* part;              // partial tiles [2 * gridDim.x][256 CS][256 rows] fp32: CTA b's first piece
+                              // (if partial) in tile 2b, its last partial piece in tile 2b + 1
     int n, m, G, T, cs_s;     // pixels, measurements, GOP, frames/stream, CS frames/stream
-    int gw, nf_box;           // GOPs per window, frame rows per box (= gw * G)
+    int gw, nf_box;           // GOPs per window, frame rows of a window (= gw * G)
+    int n_fbox, fbox_rows;    // TMA boxes per chunk (box dims <= 256) and rows per box (multiple of 8): the
+                              // boxes land back to back, so row t of the window is at byte 64 t of the slot
     int n_win_s, n_win;       // windows per stream, all windows
     int global_win;           // T % G == 0: windows run over the concatenated GOPs of all streams
     int total_gops;           // n_seq * T / G (global_win)
-    int n_mp, n_ks, n_chunks; // 256-row m-pairs, K splits, 64-pixel chunks
+    int n_mp, n_chunks;       // 256-row m-pairs, 64-pixel chunks
     int n_units;
-    uint32_t fbox_bytes;      // one frame box (nf_box rows x 64 B)
+    long long total_chunks;   // n_units * n_chunks: CTA b takes chunks [b C / grid, (b + 1) C / grid)
+    uint32_t fbox_bytes;      // the chunk's frame boxes (n_fbox * fbox_rows rows x 64 B)
     uint32_t off_a;           // A ring: n_a slots of 256 * kKc fp16 (32 KB), 1024-aligned
     int n_a;
     uint32_t stage_bytes;     // frames ring slot (fbox_bytes rounded up to 1024)
@@ -61,11 +70,10 @@ struct FParams {
     int n_b;                  // residual buffers (2..4)
     uint32_t off_stage;       // frames ring: kOffB + n_b * b_bytes
     int n_stages;             // frames ring slots
-    long long part_stride;    // floats per partial plane (n_seq * cs_s * m rounded up to 4)
     int prefetch;             // frame boxes prefetched into L2 this many chunks ahead (0 = off)
     unsigned long long* trace;   // debug timeline (CTA 0): [4][trace_cap] clock64, nullptr = off
     int trace_cap;
-    long long out_floats;     // floats in one output plane (y, or one partial plane) (CSENC_CHECKS)
+    long long out_floats;     // floats in y (CSENC_CHECKS)
     uint32_t smem_bytes;      // dynamic SMEM from the aligned base (CSENC_CHECKS)
 };
 
@@ -75,19 +83,26 @@ __device__ __forceinline__ void ftrace(const FParams& p, int ev, int i) {
 }
 
 struct FUnit {
-    int s, g0, ngops, n_cs, cs0, mp, ks, kc0, kc1;
+    int u, s, g0, ngops, n_cs, cs0, mp, kc0, kc1;
+    int slot;                 // partial tile of this piece, -1 = whole unit (written to y)
 };
 
-// Unit u = (ks * n_win + win) * n_mp + mp: (K split, window, m-pair); CTAs running together share
-// the K range.
+// Stream-K ranges: CTA b owns chunks [cbeg(b), cbeg(b + 1)); cta_of(c) = the CTA owning chunk c.
+__device__ __forceinline__ long long cbeg(const FParams& p, long long b, long long grid) {
+    return b * p.total_chunks / grid;
+}
+__device__ __forceinline__ int cta_of(const FParams& p, long long c, long long grid) {
+    return (int)(((c + 1) * grid - 1) / p.total_chunks);
+}
+
+// Unit u = win * n_mp + mp: (window, m-pair).
 __device__ __forceinline__ void decode_funit(const FParams& p, int u, FUnit& w) {
+    w.u = u;
     w.mp = u % p.n_mp;
-    const int r = u / p.n_mp;
-    const int win = r % p.n_win;
-    w.ks = r / p.n_win;
-    const int per = (p.n_chunks + p.n_ks - 1) / p.n_ks;
-    w.kc0 = w.ks * per;
-    w.kc1 = min(p.n_chunks, w.kc0 + per);
+    const int win = u / p.n_mp;
+    w.kc0 = 0;
+    w.kc1 = p.n_chunks;
+    w.slot = -1;
     if (win >= p.n_win) {
         w.s = 0;
         w.g0 = 0;
@@ -115,6 +130,16 @@ __device__ __forceinline__ void decode_funit(const FParams& p, int u, FUnit& w) 
     w.cs0 = w.g0 * (p.G - 1);
 }
 
+// The piece of CTA `cid` (range [cb, ce)) that starts at chunk c: its unit and K range, and its partial
+// tile when the unit is cut by a range boundary (tile 2 cid for the CTA's first piece, 2 cid + 1 else).
+__device__ __forceinline__ void piece_at(const FParams& p, long long c, long long cb, long long ce, int cid, FUnit& w) {
+    const int u = (int)(c / p.n_chunks);
+    decode_funit(p, u, w);
+    w.kc0 = (int)(c - (long long)u * p.n_chunks);
+    w.kc1 = (int)min((long long)p.n_chunks, (long long)w.kc0 + (ce - c));
+    if (w.kc0 != 0 || w.kc1 != p.n_chunks) w.slot = 2 * cid + (c == cb ? 0 : 1);
+}
+
 __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __grid_constant__ FParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t sbase = (ptx::smem_addr(smem_raw) + 1023u) & ~1023u;
@@ -132,6 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
     const uint32_t tmem_slot = bar_dempty + 8;
 
     const int cid = (int)blockIdx.x, n_cl = (int)gridDim.x;
+    const long long c_beg = cbeg(p, cid, n_cl), c_end = cbeg(p, cid + 1, n_cl);   // this CTA's chunk range
     if (threadIdx.x == 0) {
         for (int i = 0; i < p.n_stages; ++i) {
             ptx::mbar_init(bar_full + 8 * i, 1);
@@ -170,9 +196,10 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         // ================================================================ producer
         int st = 0, ntr = 0;
         uint32_t ph = 0;
-        for (int u = cid; u < p.n_units; u += n_cl) {
+        for (long long c = c_beg; c < c_end;) {
             FUnit w;
-            decode_funit(p, u, w);
+            piece_at(p, c, c_beg, c_end, cid, w);
+            c += w.kc1 - w.kc0;
             const int row0 = w.s * p.T + w.g0 * p.G;
             if (lane == 0)   // frames stream from HBM: pull the first boxes of the unit into L2 early
                 for (int kc = w.kc0; kc < min(w.kc1, w.kc0 + p.prefetch); ++kc)
@@ -184,7 +211,9 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                 if (lane == 0) {
                     const uint32_t sf = sbase + p.off_stage + (uint32_t)st * p.stage_bytes;
                     ptx::mbar_arrive_expect_tx(bar_full + 8 * st, p.fbox_bytes);
-                    ptx::tma_load_2d(sf, &p.fmap, bar_full + 8 * st, kc * kKc, row0);
+                    for (int j = 0; j < p.n_fbox; ++j)   // rows past the tensor are zero-filled (and counted)
+                        ptx::tma_load_2d(sf + (uint32_t)(j * p.fbox_rows * 64), &p.fmap, bar_full + 8 * st, kc * kKc,
+                                         row0 + j * p.fbox_rows);
                     ftrace(p, 0, ntr);
                 }
                 ++ntr;
@@ -199,9 +228,10 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         // ================================================================ A producer
         int as = 0;
         uint32_t aph = 0;
-        for (int u = cid; u < p.n_units; u += n_cl) {
+        for (long long c = c_beg; c < c_end;) {
             FUnit w;
-            decode_funit(p, u, w);
+            piece_at(p, c, c_beg, c_end, cid, w);
+            c += w.kc1 - w.kc0;
             for (int kc = w.kc0; kc < w.kc1; ++kc) {
                 ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
                 if (lane == 0) {
@@ -231,9 +261,10 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         }
         int st = 0, b = 0, ntr = 0;
         uint32_t ph = 0, bph = 0;
-        for (int u = cid; u < p.n_units; u += n_cl) {
+        for (long long c = c_beg; c < c_end;) {
             FUnit w;
-            decode_funit(p, u, w);
+            piece_at(p, c, c_beg, c_end, cid, w);
+            c += w.kc1 - w.kc0;
             for (int kc = w.kc0; kc < w.kc1; ++kc) {
                 ptx::mbar_wait(bar_full + 8 * st, ph);
                 if (tid == 0) ftrace(p, 1, ntr);
@@ -290,9 +321,10 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         // hundreds of chunks long, the epilogue a few thousand cycles)
         int st = 0, b = 0, ntr = 0;   // st: A ring slot
         uint32_t ph = 0, bph = 0, dph = 0;
-        for (int u = cid; u < p.n_units; u += n_cl) {
+        for (long long c = c_beg; c < c_end;) {
             FUnit w;
-            decode_funit(p, u, w);
+            piece_at(p, c, c_beg, c_end, cid, w);
+            c += w.kc1 - w.kc0;
             const uint32_t nmma = (uint32_t)((w.n_cs + 15) & ~15);
             const uint32_t idesc = (1u << 4) | ((nmma >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
             const bool two = (w.mp * 256 + 128) < p.m;          // second m-tile has rows
@@ -337,26 +369,31 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         const int ew = warp - kEpiWarp0;   // == warp % 4: TMEM lanes 32 ew .. 32 ew + 31
         const uint32_t lane_bits = (uint32_t)(ew * 32) << 16;
         uint32_t dph = 0;
-        for (int u = cid; u < p.n_units; u += n_cl) {
+        for (long long c = c_beg; c < c_end;) {
             FUnit w;
-            decode_funit(p, u, w);
+            piece_at(p, c, c_beg, c_end, cid, w);
+            c += w.kc1 - w.kc0;
             ptx::mbar_wait(bar_dfull, dph);
             ptx::tc_fence_after();
             for (int half = 0; half < 2; ++half) {
-                const int i = w.mp * 256 + half * 128 + ew * 32 + (int)lane;     // measurement index
+                const int il = half * 128 + ew * 32 + (int)lane;                 // row within the m-pair
+                const int i = w.mp * 256 + il;                                      // measurement index
                 if (w.mp * 256 + half * 128 >= p.m) break;                        // warp-uniform
-                float* const dst0 = p.out + (long long)w.ks * p.part_stride +
-                                    ((long long)w.s * p.cs_s + w.cs0) * p.m + i;
+                // whole unit: y rows [cs][m]; a piece of a cut unit: its partial tile [256 CS][256 rows]
+                const long long ld = w.slot < 0 ? (long long)p.m : 256LL;
+                float* const dst0 = w.slot < 0 ? p.out + ((long long)w.s * p.cs_s + w.cs0) * p.m + i
+                                               : p.part + (long long)w.slot * 65536LL + il;
                 const uint32_t d_tm = tmem_base + lane_bits + (uint32_t)half * 256u;
                 for (int j0 = 0; j0 < w.n_cs; j0 += 32) {
                     uint32_t v[32];
                     ptx::tmem_ld_32x32b_x32(d_tm + (uint32_t)j0, v);
                     ptx::tc_wait_ld();
-                    CS_CHECK(i >= p.m || ((long long)w.s * p.cs_s + w.cs0 + w.n_cs - 1) * p.m + i < p.out_floats);
+                    CS_CHECK(i >= p.m || w.slot >= 0 || ((long long)w.s * p.cs_s + w.cs0 + w.n_cs - 1) * p.m + i < p.out_floats);
+                    CS_CHECK(w.slot < 2 * n_cl && w.n_cs <= 256);
                     if (i < p.m) {
 #pragma unroll
                         for (int k = 0; k < 32; ++k)
-                            if (j0 + k < w.n_cs) dst0[(long long)(j0 + k) * p.m] = __uint_as_float(v[k]);
+                            if (j0 + k < w.n_cs) dst0[(long long)(j0 + k) * ld] = __uint_as_float(v[k]);
                     }
                 }
             }
@@ -373,27 +410,48 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
     if (warp == kMmaWarp) ptx::tmem_dealloc(tmem_base, kTmemCols);
 }
 
-// y[i] = sum over the n_ks partial planes (plane k at part + k * stride, stride % 4 == 0), in plane
-// order (deterministic)
-__global__ void cs_frame_reduce_kernel(const float* __restrict__ part, float* __restrict__ y, long long n,
-                                       long long stride, int n_ks) {
-    const long long n4 = n / 4;
-    const long long step = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += step) {
-        float4 a = reinterpret_cast<const float4*>(part)[i];
-        for (int k = 1; k < n_ks; ++k) {
-            const float4 b = reinterpret_cast<const float4*>(part + (long long)k * stride)[i];
+// Units cut by stream-K range boundaries: y = the sum of their pieces' partial tiles in CTA order
+// (deterministic).  Block x handles split unit units[x]; `grid` is the measurement kernel's grid.
+struct FixupList {
+    int n;
+    int grid;
+    int units[256];   // <= grid - 1 split units (grid <= SM count)
+};
+__global__ void __launch_bounds__(64) cs_frame_fixup_kernel(const __grid_constant__ FParams p,
+                                                                const __grid_constant__ FixupList L) {
+    // block (x, y): split unit units[x], CS frames y, y + gridDim.y, ...; thread: 4 rows of the m-pair
+    const int u = L.units[blockIdx.x];
+    FUnit w;
+    decode_funit(p, u, w);
+    const long long grid = L.grid;
+    const long long c0 = (long long)u * p.n_chunks, c1 = c0 + p.n_chunks - 1;
+    const int bf = cta_of(p, c0, grid), bl = cta_of(p, c1, grid);
+    constexpr int kMaxPieces = 8;
+    long long tile[kMaxPieces];
+    const int np = min(kMaxPieces, bl - bf + 1);
+    CS_CHECK(bl - bf + 1 <= kMaxPieces);
+    for (int j = 0; j < np; ++j) {
+        const int b = bf + j;   // b's first piece iff b starts inside u
+        tile[j] = (long long)(2 * b + (cbeg(p, b, grid) >= c0 ? 0 : 1)) * 65536LL;
+    }
+    const int rows = min(256, p.m - w.mp * 256);
+    const int il = (int)threadIdx.x * 4;
+    if (il >= rows) return;
+    float* const y0 = p.out + ((long long)w.s * p.cs_s + w.cs0) * p.m + (long long)w.mp * 256 + il;
+    for (int cs = (int)blockIdx.y; cs < w.n_cs; cs += (int)gridDim.y) {
+        float4 a = *reinterpret_cast<const float4*>(p.part + tile[0] + (long long)cs * 256 + il);
+        for (int j = 1; j < np; ++j) {   // CTA order: deterministic
+            const float4 b = *reinterpret_cast<const float4*>(p.part + tile[j] + (long long)cs * 256 + il);
             a.x += b.x;
             a.y += b.y;
             a.z += b.z;
             a.w += b.w;
         }
-        reinterpret_cast<float4*>(y)[i] = a;
-    }
-    for (long long i = n4 * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += step) {
-        float a = part[i];
-        for (int k = 1; k < n_ks; ++k) a += part[(long long)k * stride + i];
-        y[i] = a;
+        float* const yr = y0 + (long long)cs * p.m;
+        yr[0] = a.x;
+        if (il + 1 < rows) yr[1] = a.y;
+        if (il + 2 < rows) yr[2] = a.z;
+        if (il + 3 < rows) yr[3] = a.w;
     }
 }
 
