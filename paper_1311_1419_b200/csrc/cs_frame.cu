@@ -183,11 +183,13 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     const long long tiles = (long long)fp.n_win * fp.n_mp;              // work units
     if (tiles > 0x7FFFFFFFLL / 2) return fail(CS_ERR_UNSUPPORTED, "too many work units");
     fp.n_units = (int)tiles;
-    fp.total_chunks = tiles * fp.n_chunks;
-    // stream-K grid: every SM, unless that leaves a CTA fewer than 8 chunks (pipeline fill per piece)
-    // (and at most 8 pieces per unit: ranges of >= n_chunks / 7 chunks)
-    const long long n_cl = std::max(1LL, std::min({(long long)f->sms, fp.total_chunks / 8,
-                                                   7 * fp.total_chunks / std::max(1, fp.n_chunks)}));
+    fp.total_chunks = (long long)fp.n_win * fp.n_chunks;   // per m-pair
+    // stream-K grid: n_mp CTAs per range (one per m-pair, same frame boxes at the same time), as many
+    // ranges as SMs allow, unless that leaves a CTA fewer than 8 chunks (pipeline fill per piece) or cuts
+    // a unit into more than 8 pieces (ranges of >= n_chunks / 7 chunks)
+    const long long gj = std::max(1LL, std::min({(long long)f->sms / fp.n_mp, fp.total_chunks / 8,
+                                                 7 * fp.total_chunks / std::max(1, fp.n_chunks)}));
+    const long long n_cl = gj * fp.n_mp;
     fp.fbox_bytes = (uint32_t)(fp.n_fbox * fp.fbox_rows) * (uint32_t)csenc::frm::kKc;
     fp.stage_bytes = align_up(fp.fbox_bytes, 1024);                    // frames ring slot
     const uint32_t a_slot = 256u * csenc::frm::kKc * 2u;                // A ring slot (32 KB)
@@ -219,13 +221,16 @@ int cs_frame_encode_batch(cs_frame_encoder* f, const uint8_t* frames, int n_seq,
     csenc::frm::FixupList fl;
     fl.n = 0;
     fl.grid = grid;
-    for (long long b = 1; b < grid; ++b) {
-        const long long c = b * fp.total_chunks / grid;
+    for (long long j = 1, last = -1; j < gj; ++j) {
+        const long long c = j * fp.total_chunks / gj;
         if (c % fp.n_chunks == 0) continue;
-        const int u = (int)(c / fp.n_chunks);
-        if (fl.n > 0 && fl.units[fl.n - 1] == u) continue;
-        if (fl.n == (int)(sizeof(fl.units) / sizeof(fl.units[0]))) return fail(CS_ERR_UNSUPPORTED, "too many split units");
-        fl.units[fl.n++] = u;
+        const int win = (int)(c / fp.n_chunks);
+        if (win == last) continue;
+        last = win;
+        for (int mp = 0; mp < fp.n_mp; ++mp) {
+            if (fl.n == (int)(sizeof(fl.units) / sizeof(fl.units[0]))) return fail(CS_ERR_UNSUPPORTED, "too many split units");
+            fl.units[fl.n++] = win * fp.n_mp + mp;
+        }
     }
     float* part = nullptr;
     cudaError_t err;

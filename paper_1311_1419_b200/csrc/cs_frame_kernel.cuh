@@ -61,7 +61,9 @@ struct FParams {
     int total_gops;           // n_seq * T / G (global_win)
     int n_mp, n_chunks;       // 256-row m-pairs, 64-pixel chunks
     int n_units;
-    long long total_chunks;   // n_units * n_chunks: CTA b takes chunks [b C / grid, (b + 1) C / grid)
+    long long total_chunks;   // n_win * n_chunks (per m-pair): CTA b = j n_mp + mp takes m-pair mp's chunks
+                              // [j C / gj, (j + 1) C / gj) of the (window, K chunk) sequence, gj = grid / n_mp
+                              // (the n_mp CTAs of one j read the same frame boxes at about the same time)
     uint32_t fbox_bytes;      // the chunk's frame boxes (n_fbox * fbox_rows rows x 64 B)
     uint32_t off_a;           // A ring: n_a slots of 256 * kKc fp16 (32 KB), 1024-aligned
     int n_a;
@@ -87,12 +89,13 @@ struct FUnit {
     int slot;                 // partial tile of this piece, -1 = whole unit (written to y)
 };
 
-// Stream-K ranges: CTA b owns chunks [cbeg(b), cbeg(b + 1)); cta_of(c) = the CTA owning chunk c.
-__device__ __forceinline__ long long cbeg(const FParams& p, long long b, long long grid) {
-    return b * p.total_chunks / grid;
+// Stream-K ranges (per m-pair, gj ranges): range j = chunks [cbeg(j), cbeg(j + 1)) of the (window, K chunk)
+// sequence; range_of(c) = the range holding chunk c.
+__device__ __forceinline__ long long cbeg(const FParams& p, long long j, long long gj) {
+    return j * p.total_chunks / gj;
 }
-__device__ __forceinline__ int cta_of(const FParams& p, long long c, long long grid) {
-    return (int)(((c + 1) * grid - 1) / p.total_chunks);
+__device__ __forceinline__ int range_of(const FParams& p, long long c, long long gj) {
+    return (int)(((c + 1) * gj - 1) / p.total_chunks);
 }
 
 // Unit u = win * n_mp + mp: (window, m-pair).
@@ -130,12 +133,13 @@ __device__ __forceinline__ void decode_funit(const FParams& p, int u, FUnit& w) 
     w.cs0 = w.g0 * (p.G - 1);
 }
 
-// The piece of CTA `cid` (range [cb, ce)) that starts at chunk c: its unit and K range, and its partial
-// tile when the unit is cut by a range boundary (tile 2 cid for the CTA's first piece, 2 cid + 1 else).
-__device__ __forceinline__ void piece_at(const FParams& p, long long c, long long cb, long long ce, int cid, FUnit& w) {
-    const int u = (int)(c / p.n_chunks);
-    decode_funit(p, u, w);
-    w.kc0 = (int)(c - (long long)u * p.n_chunks);
+// The piece of CTA `cid` (m-pair mp, range [cb, ce)) that starts at chunk c: its unit and K range, and its
+// partial tile when the unit is cut by a range boundary (tile 2 cid for the CTA's first piece, 2 cid + 1 else).
+__device__ __forceinline__ void piece_at(const FParams& p, long long c, long long cb, long long ce, int cid, int mp,
+                                         FUnit& w) {
+    const int win = (int)(c / p.n_chunks);
+    decode_funit(p, win * p.n_mp + mp, w);
+    w.kc0 = (int)(c - (long long)win * p.n_chunks);
     w.kc1 = (int)min((long long)p.n_chunks, (long long)w.kc0 + (ce - c));
     if (w.kc0 != 0 || w.kc1 != p.n_chunks) w.slot = 2 * cid + (c == cb ? 0 : 1);
 }
@@ -157,7 +161,9 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
     const uint32_t tmem_slot = bar_dempty + 8;
 
     const int cid = (int)blockIdx.x, n_cl = (int)gridDim.x;
-    const long long c_beg = cbeg(p, cid, n_cl), c_end = cbeg(p, cid + 1, n_cl);   // this CTA's chunk range
+    const int cmp = cid % p.n_mp;                   // this CTA's m-pair and stream-K range
+    const long long gj = n_cl / p.n_mp, cj = cid / p.n_mp;
+    const long long c_beg = cbeg(p, cj, gj), c_end = cbeg(p, cj + 1, gj);
     if (threadIdx.x == 0) {
         for (int i = 0; i < p.n_stages; ++i) {
             ptx::mbar_init(bar_full + 8 * i, 1);
@@ -198,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         uint32_t ph = 0;
         for (long long c = c_beg; c < c_end;) {
             FUnit w;
-            piece_at(p, c, c_beg, c_end, cid, w);
+            piece_at(p, c, c_beg, c_end, cid, cmp, w);
             c += w.kc1 - w.kc0;
             const int row0 = w.s * p.T + w.g0 * p.G;
             if (lane == 0)   // frames stream from HBM: pull the first boxes of the unit into L2 early
@@ -230,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         uint32_t aph = 0;
         for (long long c = c_beg; c < c_end;) {
             FUnit w;
-            piece_at(p, c, c_beg, c_end, cid, w);
+            piece_at(p, c, c_beg, c_end, cid, cmp, w);
             c += w.kc1 - w.kc0;
             for (int kc = w.kc0; kc < w.kc1; ++kc) {
                 ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
@@ -263,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         uint32_t ph = 0, bph = 0;
         for (long long c = c_beg; c < c_end;) {
             FUnit w;
-            piece_at(p, c, c_beg, c_end, cid, w);
+            piece_at(p, c, c_beg, c_end, cid, cmp, w);
             c += w.kc1 - w.kc0;
             for (int kc = w.kc0; kc < w.kc1; ++kc) {
                 ptx::mbar_wait(bar_full + 8 * st, ph);
@@ -323,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         uint32_t ph = 0, bph = 0, dph = 0;
         for (long long c = c_beg; c < c_end;) {
             FUnit w;
-            piece_at(p, c, c_beg, c_end, cid, w);
+            piece_at(p, c, c_beg, c_end, cid, cmp, w);
             c += w.kc1 - w.kc0;
             const uint32_t nmma = (uint32_t)((w.n_cs + 15) & ~15);
             const uint32_t idesc = (1u << 4) | ((nmma >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
@@ -371,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         uint32_t dph = 0;
         for (long long c = c_beg; c < c_end;) {
             FUnit w;
-            piece_at(p, c, c_beg, c_end, cid, w);
+            piece_at(p, c, c_beg, c_end, cid, cmp, w);
             c += w.kc1 - w.kc0;
             ptx::mbar_wait(bar_dfull, dph);
             ptx::tc_fence_after();
@@ -423,16 +429,16 @@ __global__ void __launch_bounds__(64) cs_frame_fixup_kernel(const __grid_constan
     const int u = L.units[blockIdx.x];
     FUnit w;
     decode_funit(p, u, w);
-    const long long grid = L.grid;
-    const long long c0 = (long long)u * p.n_chunks, c1 = c0 + p.n_chunks - 1;
-    const int bf = cta_of(p, c0, grid), bl = cta_of(p, c1, grid);
+    const long long gj = L.grid / p.n_mp;
+    const long long c0 = (long long)(u / p.n_mp) * p.n_chunks, c1 = c0 + p.n_chunks - 1;
+    const int jf = range_of(p, c0, gj), jl = range_of(p, c1, gj);
     constexpr int kMaxPieces = 8;
     long long tile[kMaxPieces];
-    const int np = min(kMaxPieces, bl - bf + 1);
-    CS_CHECK(bl - bf + 1 <= kMaxPieces);
-    for (int j = 0; j < np; ++j) {
-        const int b = bf + j;   // b's first piece iff b starts inside u
-        tile[j] = (long long)(2 * b + (cbeg(p, b, grid) >= c0 ? 0 : 1)) * 65536LL;
+    const int np = min(kMaxPieces, jl - jf + 1);
+    CS_CHECK(jl - jf + 1 <= kMaxPieces);
+    for (int k = 0; k < np; ++k) {
+        const int j = jf + k, b = j * p.n_mp + w.mp;   // range j's CTA of this m-pair; its first piece iff j starts inside u
+        tile[k] = (long long)(2 * b + (cbeg(p, j, gj) >= c0 ? 0 : 1)) * 65536LL;
     }
     const int rows = min(256, p.m - w.mp * 256);
     const int il = (int)threadIdx.x * 4;
