@@ -35,12 +35,17 @@
 namespace csenc {
 namespace frm {
 
-constexpr int kConvWarps = 8;
-constexpr int kEpiWarp0 = 8;
-constexpr int kProducerWarp = 12;   // frame boxes
-constexpr int kMmaWarp = 13;
-constexpr int kAProducerWarp = 14;  // A tiles
-constexpr int kThreads = 15 * 32;
+#ifndef CSENC_FRAME_CONV_WARPS
+#define CSENC_FRAME_CONV_WARPS 16
+#endif
+constexpr int kConvWarps = CSENC_FRAME_CONV_WARPS;   // residual converters (a multiple of 4)
+constexpr int kConvRowGroups = kConvWarps * 4;         // 8-lane row groups: rows c = group + kConvRowGroups i
+constexpr int kConvRows = (256 + kConvRowGroups - 1) / kConvRowGroups;   // CS rows per thread and chunk
+constexpr int kEpiWarp0 = kConvWarps;                  // a warpgroup: TMEM lane quarters = warp % 4
+constexpr int kProducerWarp = kConvWarps + 4;          // frame boxes
+constexpr int kMmaWarp = kConvWarps + 5;
+constexpr int kAProducerWarp = kConvWarps + 6;         // A tiles
+constexpr int kThreads = (kConvWarps + 7) * 32;
 constexpr int kMaxStages = 8;
 constexpr int kKc = 64;                          // pixels per K chunk
 constexpr uint32_t kTmemCols = 512;
@@ -254,14 +259,14 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
         }
     } else if (warp < kConvWarps) {
         // ================================================================ residual -> B operand
-        // thread: 8-pixel group q = tid & 7 of CS rows c = tid/8 + 32 i (i < 8).  Row c of a window
+        // thread: 8-pixel group q = tid & 7 of CS rows c = tid/8 + kConvRowGroups i (i < kConvRows).  Row c of a window
         // is CS frame 1 + c % (G-1) of the window's GOP c / (G-1): frame row and key row packed.
         const int tid = (int)threadIdx.x;
         const int q = tid & 7;
-        uint32_t rows[8];
+        uint32_t rows[kConvRows];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int c = (tid >> 3) + 32 * i;
+        for (int i = 0; i < kConvRows; ++i) {
+            const int c = (tid >> 3) + kConvRowGroups * i;
             const int gl = c / (p.G - 1), pos = c - gl * (p.G - 1);
             rows[i] = (uint32_t)(gl * p.G + 1 + pos) | ((uint32_t)(gl * p.G) << 16);
         }
@@ -278,10 +283,10 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                 const uint32_t sf = sbase + p.off_stage + (uint32_t)st * p.stage_bytes;
                 const uint32_t sb = sbase + kOffB + (uint32_t)b * p.b_bytes;
                 // all loads first (rows past the window read row 0: harmless, not stored), then convert
-                uint2 fv[8], kv[8];
+                uint2 fv[kConvRows], kv[kConvRows];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int c = (tid >> 3) + 32 * i;
+                for (int i = 0; i < kConvRows; ++i) {
+                    const int c = (tid >> 3) + kConvRowGroups * i;
                     const uint32_t rr = c < w.n_cs ? rows[i] : 0u;
                     const uint32_t t = rr & 0xFFFFu, k = rr >> 16;
                     // SWIZZLE_64B box rows of 64 B: 16-B chunk (q/2) ^ ((row/2) & 3), 8-B half q & 1
@@ -291,8 +296,8 @@ __global__ void __launch_bounds__(kThreads, 1) cs_frame_measure_kernel(const __g
                     kv[i] = ptx::lds64(sf + ck);
                 }
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int c = (tid >> 3) + 32 * i;
+                for (int i = 0; i < kConvRows; ++i) {
+                    const int c = (tid >> 3) + kConvRowGroups * i;
                     if (c < w.n_cs) {
                         CS_CHECK((rows[i] & 0xFFFFu) < (uint32_t)p.nf_box && (rows[i] >> 16) < (uint32_t)p.nf_box);
                         CS_CHECK((uint32_t)(c + 1) * 128u <= p.b_bytes);
