@@ -26,4 +26,4 @@ timeout 300 $CMD > $OUT/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launch.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:cs_measure -s 12 -c 4 -o $OUT/prof $CMD > $OUT/ncu_full.log 2>&1
 echo "ncu rc=$?" >> $OUT/ncu_full.log
-[ "${NEXT:-0}" = "1" ] && ONLY="q16row q16frame" bash tools/prof_next.sh $TAG-next
+[ "${NEXT:-0}" = "1" ] && ONLY="${NEXT_ONLY:-q16row q16frame}" bash tools/prof_next.sh $TAG-next
