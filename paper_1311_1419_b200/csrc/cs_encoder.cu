@@ -157,7 +157,7 @@ bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem
         const double key_item = 700.0 + 150.0 * strip_copies + (double)p.stage_cs_bytes / 32.0;
         s = px * U / (U * cycles + key_item);
     }
-    // Measured (tools/sweep10.sh): with >= 3 ring slots the double-buffered SMEM key is ~5% faster
+    // Measured (round 1, a forced-plan sweep since removed): with >= 3 ring slots the double-buffered SMEM key is ~5% faster
     // than the register key (whose load sits in the ring at every unit start); the register key
     // wins when a resident key would leave < 3 slots (C5).
     // B = 8 rows are 8-byte loads, so dropping the per-item key loads matters more there.
