@@ -374,6 +374,21 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.chained = q.chained;
     kp.phis = (const uint16_t*)e->phis_dev;
     kp.n_phis = e->n_phis;
+    // per-GOP Phi resident in SMEM: a second slot behind the ring (one stage fewer if it does not fit), so the
+    // next GOP's matrix loads while the current one is in use
+    uint32_t smem_launch = pl.smem_bytes;
+    kp.off_phi2 = 0;
+    if (e->n_phis > 0 && !pl.phi_stream) {
+        for (int ns = pl.n_stages; ns >= std::max(2, pl.n_stages - 1) && kp.off_phi2 == 0; --ns) {
+            const uint32_t off2 = align_up(pl.off_stage + (uint32_t)ns * pl.stage_bytes, 1024);
+            if (off2 + e->phi_bytes + 1024 <= (uint32_t)e->smem_limit) {
+                kp.off_phi2 = off2;
+                kp.n_stages = ns;
+                smem_launch = off2 + e->phi_bytes + 1024;
+            }
+        }
+    }
+    kp.smem_bytes = smem_launch - 1024;
     kp.n_gops_T = cdiv(T, g.G);
     kp.qmode = q.qmode;
     kp.codes = q.codes;
@@ -414,7 +429,7 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
                    : pl.key_regs ? csenc::KEY_REGS : (pl.key_resident ? csenc::KEY_RESIDENT : csenc::KEY_STREAMED);
     // KEY_STREAMED / KEY_CHUNK kernels take KParamsTS (with the strip tensor map), the others KParams
     auto go = [&](auto kern) {
-        auto run = [&](auto& prm) { kern<<<grid, csenc::kThreads, pl.smem_bytes, stream>>>(prm); };
+        auto run = [&](auto& prm) { kern<<<grid, csenc::kThreads, smem_launch, stream>>>(prm); };
         if constexpr (std::is_invocable_v<decltype(kern), const csenc::KParamsTS&> &&
                       !std::is_invocable_v<decltype(kern), const csenc::KParams&>)
             run(kpt);

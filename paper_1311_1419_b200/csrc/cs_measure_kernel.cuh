@@ -114,6 +114,8 @@ struct KParams {
     // phis[g % n_phis] (each phi_bytes, same layout), reloaded into SMEM when a unit's GOP changes
     const uint16_t* phis;
     int n_phis;
+    uint32_t off_phi2;        // per-GOP Phi, resident: a second Phi slot (0 = one slot): the next GOP's matrix
+                              // loads while the current one is in use
     int W, H, M, Mpad, N;
     int nbx, nby, nblk;
     // tiling
@@ -457,6 +459,10 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
     const uint32_t bar_phi = bar_d_empty + 8 * kMaxTmemBufs;
     const uint32_t tmem_slot = bar_phi + 8;
     const uint32_t bar_phi_empty = bar_phi + 16;   // per-GOP Phi: MMAs on the current Phi done
+    // per-GOP Phi with two resident slots: slot 1's full / empty barriers (bytes 992..1007 of the barrier
+    // page: past the Q_ROW slots)
+    const uint32_t bar_phi2 = sbase + 992, bar_phi_empty2 = sbase + 1000;
+    static_assert(kRowSlotOff + 3 * kRowSlots * 4 <= 992, "row slots overlap the second Phi slot's barriers");
     const uint32_t s_phi = sbase + p.off_phi;
     // Phi streaming and 4-D strip boxes only exist for multi-chunk plans, which never hold the key in
     // registers: compiled out of the KEY_REGS instantiations (their code stays as small as before).
@@ -493,6 +499,8 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
         }
         ptx::mbar_init(bar_phi, 1);
         ptx::mbar_init(bar_phi_empty, 1);
+        ptx::mbar_init(bar_phi2, 1);
+        ptx::mbar_init(bar_phi_empty2, 1);
         if (EPI == EPI_Q16RR || EPI == EPI_Q16RR64)
             for (int i = 0; i < kRowBufs; ++i) ptx::mbar_init(sbase + kRowBarOff + 8 * i, 4);   // row_full
         ptx::fence_mbarrier_init();
@@ -566,11 +574,18 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
             if (p.n_phis > 0 && !phi_stream && !phi_slices) {   // per-GOP Phi: reload when the GOP's matrix differs from the resident one
                 const int gsel = w.g % p.n_phis;
                 if (gsel != phi_cur) {
-                    if (phi_loads > 0) ptx::mbar_wait(bar_phi_empty, (phi_loads - 1u) & 1u);
+                    // load k = phi_loads goes to slot k & 1 (two slots) or slot 0; it waits until the MMAs
+                    // on the slot's previous matrix (load k - 2, or k - 1 with one slot) have completed
+                    const uint32_t k = phi_loads;
+                    const bool two = p.off_phi2 != 0;
+                    const uint32_t slot = two ? (k & 1u) : 0u;
+                    const uint32_t full = slot ? bar_phi2 : bar_phi, empty = slot ? bar_phi_empty2 : bar_phi_empty;
+                    if (two ? k >= 2 : k > 0) ptx::mbar_wait(empty, (two ? (k - 2u) >> 1 : k - 1u) & 1u);
                     if (elect_one()) {
-                        ptx::mbar_arrive_expect_tx(bar_phi, p.phi_bytes);
-                        ptx::bulk_load(s_phi, reinterpret_cast<const uint8_t*>(p.phis) + (size_t)gsel * p.phi_bytes,
-                                       p.phi_bytes, bar_phi);
+                        ptx::mbar_arrive_expect_tx(full, p.phi_bytes);
+                        ptx::bulk_load(slot ? sbase + p.off_phi2 : s_phi,
+                                       reinterpret_cast<const uint8_t*>(p.phis) + (size_t)gsel * p.phi_bytes,
+                                       p.phi_bytes, full);
                     }
                     __syncwarp();
                     phi_cur = gsel;
@@ -691,7 +706,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
         const int ksteps = p.chunk_k / 16;
         // descriptor of Phi's first K step; K step kg starts 2*kg core matrices (2*kg*lbo bytes)
         // further, i.e. +2*lbo>>4 in the 14-bit start-address field (no carry: smem < 256 KB)
-        const uint64_t desc0 = ptx::smem_desc_noswizzle(s_phi, p.lbo, p.sbo);
+        uint64_t desc0 = ptx::smem_desc_noswizzle(s_phi, p.lbo, p.sbo);   // (per-GOP Phi: the current slot's)
         const uint64_t desc_step = (uint64_t)((2u * p.lbo) >> 4);
         const uint64_t desc_chunk = desc_step * (uint64_t)ksteps;
         const uint32_t a_fold = (uint32_t)(p.chunk_k / 2);
@@ -702,14 +717,19 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
             if (p.n_phis > 0 && !phi_stream && !phi_slices) {
                 const int gsel = w.g % p.n_phis;
                 if (gsel != phi_cur) {
-                    // release the resident Phi once every MMA issued so far has completed, then wait
-                    // for the next one
-                    if (phi_waits > 0) {
-                        if (elect_one()) ptx::tc_commit(bar_phi_empty);
+                    // release the slot of the previous matrix once every MMA issued so far has completed,
+                    // then wait for the next one (load k = phi_waits, in slot k & 1 with two slots)
+                    const uint32_t k = phi_waits;
+                    const bool two = p.off_phi2 != 0;
+                    const uint32_t slot = two ? (k & 1u) : 0u;
+                    if (k > 0) {
+                        const uint32_t prev = two ? ((k - 1u) & 1u) : 0u;
+                        if (elect_one()) ptx::tc_commit(prev ? bar_phi_empty2 : bar_phi_empty);
                         __syncwarp();
                     }
-                    ptx::mbar_wait(bar_phi, phi_waits & 1u);
+                    ptx::mbar_wait(slot ? bar_phi2 : bar_phi, (two ? k >> 1 : k) & 1u);
                     ptx::tc_fence_after();
+                    desc0 = ptx::smem_desc_noswizzle(slot ? sbase + p.off_phi2 : s_phi, p.lbo, p.sbo);
                     phi_cur = gsel;
                     ++phi_waits;
                 }
