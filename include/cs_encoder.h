@@ -193,8 +193,9 @@ int cs_encode_batch_q16(cs_encoder* enc, const uint8_t* frames_dev, int n_seq, i
  *     y[cs][i] = sum_{j < n} A[i][j] * (F_cs - F_key)[j / W][j % W]     (row-major vec)
  * with the GOP structure and key reference of the block path (a1, a3).  A is fp16 (e.g. seeded
  * N(0, 1/m), m = round(n / CR); QCIF at CR 50: m = 507); products are exact, accumulation is
- * fp32 on the tensor cores (kind::f16 GEMM, 128 measurements x up to 256 CS frames per tile,
- * split-K with a deterministic second-pass sum when the batch has fewer tiles than SMs).
+ * fp32 on the tensor cores (kind::f16 GEMM, 2 x 128 measurements x up to 256 CS frames per tile; the
+ * (tile, K chunk) sequence is split into equal per-SM ranges (stream-K), and tiles cut by a range
+ * boundary are summed from their pieces' partial tiles in a fixed order by a second kernel).
  * Accuracy contract: |y_gpu - y| <= (n/16 + 16) * 2^-23 * sum_j |A[i][j] r_j| (fp32 accumulation
  * of n/16 tensor-core partial sums; R24). */
 typedef struct cs_frame_encoder cs_frame_encoder;
@@ -213,8 +214,9 @@ int cs_frame_encoder_set_trace(cs_frame_encoder* enc, unsigned long long* trace_
 int64_t cs_frame_measurement_count(const cs_frame_encoder* enc, int n_seq, int T);
 
 /* frames_dev = DEVICE uint8 [n_seq][T][H][W]; y_dev = DEVICE fp32 [n_seq * CS_s][m] (CS frames in
- * the block path's order), both 16-byte aligned.  Asynchronous on `stream` (1 launch, or 2 with
- * split-K, whose partials are stream-ordered allocations freed on the stream). */
+ * the block path's order), both 16-byte aligned.  Asynchronous on `stream` (1 launch, or 2 when a
+ * tile is cut by a stream-K range boundary; the partial tiles are stream-ordered allocations from the
+ * encoder's own pool, freed on the stream). */
 int cs_frame_encode_batch(cs_frame_encoder* enc, const uint8_t* frames_dev, int n_seq, int T, float* y_dev,
                           cs_stream_t stream);
 
