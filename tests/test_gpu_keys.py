@@ -175,3 +175,19 @@ def test_gop_phis_parity(name, M):
     again = enc.encode_batch(fd)
     torch.cuda.synchronize()
     assert torch.equal(again, ref)
+
+
+@pytest.mark.parametrize("M", [16, 64])
+def test_gop_phis_slot_reuse(M):
+    """Per-GOP Phi with the two resident Phi slots: 500 one-CS-frame GOPs of a one-tile frame over 148 CTAs,
+    so every CTA switches matrices at every unit and reuses each slot several times (the slot's previous
+    matrix must be released by the MMA's commit before it is overwritten)."""
+    cfg = synth.CONFIGS["C1"].with_(W=64, H=32, G=2, T=1000, S=1, B=16)
+    frames = synth.gen_video(cfg)
+    phis = [synth.phi_from_seed(synth.phi_seed() ^ (7 * g + 1), M, 256) for g in range(5)]
+    enc = P.Encoder(cfg.W, cfg.H, cfg.G, 16, M, phis[0])
+    enc.set_gop_phis(phis)
+    y_gpu = enc.encode_batch(torch.from_numpy(frames).cuda()).cpu().numpy()
+    y, S = oracle.encode_stream_gop_phis(frames[0], phis, cfg.G, 16)
+    ok, st = oracle.check_tolerance(y_gpu, y, S, REL)
+    assert ok, st
