@@ -424,12 +424,27 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     }
 #endif
     int grid = std::max(1, std::min(e->sms, kp.n_units));
-    cudaError_t err;
+    cudaError_t err, launch_err = cudaSuccess;
     const int km = pl.key_chunk ? csenc::KEY_CHUNK
                    : pl.key_regs ? csenc::KEY_REGS : (pl.key_resident ? csenc::KEY_RESIDENT : csenc::KEY_STREAMED);
     // KEY_STREAMED / KEY_CHUNK kernels take KParamsTS (with the strip tensor map), the others KParams
     auto go = [&](auto kern) {
-        auto run = [&](auto& prm) { kern<<<grid, csenc::kThreads, smem_launch, stream>>>(prm); };
+        // launched with programmatic stream serialization: the kernel's prologue may overlap the tail of
+        // the stream's previous kernel (it waits, griddepcontrol.wait, before touching global memory)
+        auto run = [&](auto& prm) {
+            cudaLaunchConfig_t cfg;
+            std::memset(&cfg, 0, sizeof(cfg));
+            cfg.gridDim = dim3((unsigned)grid);
+            cfg.blockDim = dim3((unsigned)csenc::kThreads);
+            cfg.dynamicSmemBytes = smem_launch;
+            cfg.stream = stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = CSENC_PDL ? 1 : 0;
+            launch_err = cudaLaunchKernelEx(&cfg, kern, prm);
+        };
         if constexpr (std::is_invocable_v<decltype(kern), const csenc::KParamsTS&> &&
                       !std::is_invocable_v<decltype(kern), const csenc::KParams&>)
             run(kpt);
@@ -456,8 +471,8 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     }
 #undef CSENC_CASE
     err = cudaGetLastError();
+    if (err == cudaSuccess) err = launch_err;
     if (err != cudaSuccess) return cuda_fail(err, "kernel launch");
-    (void)err;
     return CS_OK;
 }
 

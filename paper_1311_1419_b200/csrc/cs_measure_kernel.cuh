@@ -536,6 +536,11 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
+    // Programmatic dependent launch: the next kernel of the stream may be scheduled from here on (its CTAs
+    // start as this kernel's CTAs leave their SMs and run their own prologue); this kernel touches global
+    // memory (frames, keys, Phi in; measurements out; trace) only after the previous kernel has completed.
+    ptx::grid_dep_launch();
+    ptx::grid_dep_wait();
     if (threadIdx.x == 0) trace_ev(p, EV_K_START, 3);   // all warps through the prologue barrier
     uint32_t tmem_base;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem_base) : "r"(tmem_slot));

@@ -132,6 +132,25 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     stress_point(bar);
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// A kernel launched with cudaLaunchAttributeProgrammaticStreamSerialization may start while the previous
+// kernel of the stream is still draining.  grid_dep_launch(): this CTA no longer holds back the next
+// kernel's launch.  grid_dep_wait(): returns once the previous kernel has completed and its memory is
+// visible -- it must precede every global-memory access that can depend on, or overwrite, earlier work.
+#ifndef CSENC_PDL
+#define CSENC_PDL 1
+#endif
+__device__ __forceinline__ void grid_dep_launch() {
+#if CSENC_PDL
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void grid_dep_wait() {
+#if CSENC_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 // ------------------------------------------------------------------ TMA
 __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
