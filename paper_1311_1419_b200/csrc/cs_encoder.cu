@@ -21,6 +21,10 @@
 
 using csenc::KParams;
 
+#ifndef CSENC_SWIZZLE_DEFAULT
+#define CSENC_SWIZZLE_DEFAULT 1   // KEY_CHUNK strips through the 128-B-swizzled 5-D box when the shape allows
+#endif
+
 namespace csenc {
 namespace host {
 
@@ -125,9 +129,9 @@ bool try_plan(const Geometry& g, int T_r, int chunk_rows, int key_mode, int smem
         }
         phi_bytes = 0;
     }
-    p.off_tab = 1024;  // barriers live in the first KB, then the converter offset table (8 KB)
-    p.off_epi = 1024 + 8192;  // epilogue staging tiles (4 warps x 4 KB)
-    p.off_phi = 1024 + 8192 + 16384;
+    p.off_tab = 1024;  // barriers live in the first KB, then the converter offset table (1 KB per fold)
+    p.off_epi = 1024 + (uint32_t)p.F * 1024u;  // epilogue staging tiles (4 warps x 4 KB)
+    p.off_phi = p.off_epi + 16384;
     p.off_key = align_up(p.off_phi + phi_bytes, 1024);
     p.off_stage = align_up(p.off_key + 2 * p.key_bytes, 1024);
     const long avail = (long)smem_limit - 1024 /*alignment slack*/ - (long)p.off_stage;
@@ -411,6 +415,25 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
                              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             kpt.tma_strips = (r == CUDA_SUCCESS && pl.T_r <= 256) ? 1 : 0;
+            // KEY_CHUNK (B = 32), W a multiple of 128 and 1024-B stages: the same box as 128-B lines
+            // [W/128][128 B] written with the 128-B swizzle, so the converters' reads of 32-B block rows
+            // are free of bank conflicts (the SMEM image is the 4-D box's with chunk c of line L at c ^ (L & 7))
+            // (decoded keys, f4, come from another buffer by plain bulk copies: unswizzled)
+            if (kpt.tma_strips && pl.key_chunk && q.keys == nullptr && g.W % 128 == 0 && pl.stage_bytes % 1024 == 0 &&
+                pl.off_stage % 1024 == 0 && env_int("CSENC_SWIZZLE", CSENC_SWIZZLE_DEFAULT)) {
+                cuuint64_t dims5[5] = {32, (cuuint64_t)(g.W / 128), (cuuint64_t)g.B, (cuuint64_t)g.nby, (cuuint64_t)n_seq * T};
+                cuuint64_t strides5[4] = {128, (cuuint64_t)g.W, (cuuint64_t)g.B * g.W, (cuuint64_t)g.H * g.W};
+                cuuint32_t box5[5] = {32, (cuuint32_t)(g.W / 128), (cuuint32_t)pl.chunk_rows, (cuuint32_t)pl.T_r, 1u};
+                cuuint32_t estr5[5] = {1, 1, 1, 1, 1};
+                CUtensorMap m5;
+                r = enc(&m5, CU_TENSOR_MAP_DATA_TYPE_UINT32, 5, const_cast<uint8_t*>(frames), dims5, strides5, box5, estr5,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                if (r == CUDA_SUCCESS) {
+                    kpt.smap = m5;
+                    kpt.tma_strips = 2;
+                }
+            }
         }
     }
 #if CSENC_CHECKS
@@ -435,7 +458,7 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
             cudaLaunchConfig_t cfg;
             std::memset(&cfg, 0, sizeof(cfg));
             cfg.gridDim = dim3((unsigned)grid);
-            cfg.blockDim = dim3((unsigned)csenc::kThreads);
+            cfg.blockDim = dim3((unsigned)(km == csenc::KEY_CHUNK ? csenc::kThreadsChunk : csenc::kThreads));
             cfg.dynamicSmemBytes = smem_launch;
             cfg.stream = stream;
             cudaLaunchAttribute attr[1];

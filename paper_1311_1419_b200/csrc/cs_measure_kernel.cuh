@@ -53,6 +53,12 @@ constexpr int kEpiWarp0 = 8;                     // warps 8..11: epilogue warpgr
 constexpr int kProducerWarp = 12;                // TMA producer
 constexpr int kMmaWarp = 13;                     // MMA issuer + TMEM allocator
 constexpr int kThreads = 14 * 32;
+// KEY_CHUNK kernels run a second MMA-issuing warp (warp 14): one thread issues a small-N TS tcgen05.mma every
+// ~49 cycles whatever N <= 64 is, two threads together one every ~30 (the tensor pipe's time for N = 64;
+// tools/mma_microbench3.cu).  The two warps take alternate items, each item whole and in K order.
+constexpr int kThreadsChunk = 15 * 32;
+template <int KM>
+constexpr int threads_for() { return KM == 3 ? kThreadsChunk : kThreads; }
 constexpr int kMaxFolds = 8;
 constexpr int kMaxStages = 8;
 constexpr int kMaxTmemBufs = 8;                  // TMEM A buffers / accumulators (ring depth cap)
@@ -97,8 +103,11 @@ static_assert(kRowBarOff + 8 * kRowBufs <= kRowSlotOff, "row barriers overlap th
 static_assert(kRowSlotTileOff + kRowBufs * kRowRegRows * 4 <= 4096, "row slots overflow the staging tile");
 
 struct KParams {
-    // tma_strips != 0 (KEY_STREAMED multi-piece plans, H % B == 0): the T_r pieces of a strip arrive by
-    // ONE 4-D TMA box of KParamsTS::smap instead of T_r bulk copies
+    // tma_strips != 0 (KEY_STREAMED / KEY_CHUNK multi-piece plans, H % B == 0): the T_r pieces of a strip
+    // arrive by ONE TMA box of KParamsTS::smap instead of T_r bulk copies.  2 (KEY_CHUNK, W % 128 == 0):
+    // the box is written with the 128-B swizzle (16-byte chunk c of 128-B line L lands at chunk c ^ (L & 7)),
+    // so the converters' 16-byte reads of blocks 32 bytes apart spread over all banks (unswizzled, lanes
+    // l and l + 4 of a quarter-warp hit the same banks: every read took two wavefronts)
     int tma_strips;
     // phi_stream != 0 (multi-chunk plans, KM 0/1): Phi is not resident; each stage carries the K-slice
     // of Phi its chunk needs (phi_slice_bytes at stage offset stage_phi_off, a contiguous range of the
@@ -223,7 +232,10 @@ __device__ __forceinline__ void load_strips(const KParams& p, uint32_t dst, cons
                                             uint32_t bar, uint64_t policy, int fidx = -1,
                                             const CUtensorMap* smap = nullptr) {
     if (smap != nullptr && fidx >= 0 && p.tma_strips) {   // all T_r pieces in one box (frame fidx of `frames`)
-        ptx::tma_load_4d(dst, smap, bar, 0, k * p.chunk_rows, t * p.T_r, fidx, policy);
+        if (p.tma_strips == 2)   // 128-B lines, swizzled (KEY_CHUNK, W % 128 == 0)
+            ptx::tma_load_5d(dst, smap, bar, 0, 0, k * p.chunk_rows, t * p.T_r, fidx, policy);
+        else
+            ptx::tma_load_4d(dst, smap, bar, 0, k * p.chunk_rows, t * p.T_r, fidx, policy);
         return;
     }
     for (int pc = 0; pc < p.pieces; ++pc) {
@@ -270,12 +282,14 @@ struct RowConv<32> {
     static constexpr int kWords = 16;
     __device__ __forceinline__ static void run(uint32_t cs, uint32_t key, uint32_t* w, bool half2) {
         RowConv<16>::run(cs, key, w, true);
-        if (half2) {
-            RowConv<16>::run(cs + 16, key + 16, w + 8, true);
-        } else {
-#pragma unroll
-            for (int i = 8; i < 16; ++i) w[i] = 0u;
-        }
+        // a right half beyond W: zeros from both frames (predicated loads), 1024 - 1024 = 0 -- no per-lane
+        // branch (its divergence / reconvergence stalls cost the converters ~20% in the KEY_CHUNK loop)
+        const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+        const uint4 c = half2 ? ptx::lds128(cs + 16) : z, k = half2 ? ptx::lds128(key + 16) : z;
+        ptx::residual4(c.x, k.x, w[8], w[9]);
+        ptx::residual4(c.y, k.y, w[10], w[11]);
+        ptx::residual4(c.z, k.z, w[12], w[13]);
+        ptx::residual4(c.w, k.w, w[14], w[15]);
     }
 };
 
@@ -304,25 +318,22 @@ template <>
 struct RowConvK<32> {
     __device__ __forceinline__ static void run(uint32_t cs, const uint32_t* kw, uint32_t* w, bool half2) {
         RowConvK<16>::run(cs, kw, w, true);
-        if (half2) {
-            RowConvK<16>::run(cs + 16, kw + 4, w + 8, true);
-        } else {
-#pragma unroll
-            for (int i = 8; i < 16; ++i) w[i] = 0u;
-        }
+        const uint4 c = half2 ? ptx::lds128(cs + 16) : make_uint4(0u, 0u, 0u, 0u);
+        ptx::residual4(c.x, half2 ? kw[4] : 0u, w[8], w[9]);
+        ptx::residual4(c.y, half2 ? kw[5] : 0u, w[10], w[11]);
+        ptx::residual4(c.z, half2 ? kw[6] : 0u, w[12], w[13]);
+        ptx::residual4(c.w, half2 ? kw[7] : 0u, w[14], w[15]);
     }
 };
 
 // KEY_CHUNK, B = 32: the residual words of one row of 32 pixels (u8 words cw[0..7], loaded earlier)
-// against the row's pre-expanded key (kx[2q], kx[2q+1] = magic2 of key word q); the right half is zero
-// when it lies beyond W.
-__device__ __forceinline__ void row32_vs_kexp(const uint32_t* cw, const uint32_t* kx, uint32_t (&w)[16], bool half2) {
+// against the row's pre-expanded key (kx[2q], kx[2q+1] = magic2 of key word q).
+// A right half beyond W needs no special case here: the caller loads zeros for it from BOTH frames, and
+// 1024 - 1024 = 0 (a per-lane branch in this loop cost ~20% of the converters' time: divergence and
+// reconvergence stalls around every row).
+__device__ __forceinline__ void row32_vs_kexp(const uint32_t* cw, const uint32_t* kx, uint32_t (&w)[16]) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) ptx::residual4x(cw[q], kx[2 * q], kx[2 * q + 1], w[2 * q], w[2 * q + 1]);
-    if (!half2) {
-#pragma unroll
-        for (int i = 8; i < 16; ++i) w[i] = 0u;
-    }
 }
 
 // u8 words of one row segment of B pixels (B/4 words) from SMEM
@@ -433,7 +444,7 @@ __device__ __forceinline__ float q16_scale(uint32_t amax_bits) {
 __device__ __forceinline__ float q16_inv(float scale) { return __frcp_rn(scale); }
 
 template <int B, int KM, int EPI>
-__global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_constant__ KParamsFor<KM> p) {
+__global__ void __launch_bounds__(threads_for<KM>(), 1) cs_measure_kernel(const __grid_constant__ KParamsFor<KM> p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t sbase = (ptx::smem_addr(smem_raw) + 1023u) & ~1023u;
     const uint8_t* const smem_ptr = smem_raw + (sbase - ptx::smem_addr(smem_raw));   // sbase as a C++ pointer
@@ -489,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(bar_key_full + 8 * i, 1);
-            ptx::mbar_init(bar_key_empty + 8 * i, phi_slices ? 1 : kConvWarps);   // slice freed by the MMA's commit
+            ptx::mbar_init(bar_key_empty + 8 * i, phi_slices ? 2 : kConvWarps);   // slice freed by both MMA warps' commits
         }
         for (int i = 0; i < kMaxTmemBufs; ++i) {
             ptx::mbar_init(bar_a_full + 8 * i, kConvWarps);
@@ -498,9 +509,9 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
             ptx::mbar_init(bar_d_empty + 8 * i, 4);
         }
         ptx::mbar_init(bar_phi, 1);
-        ptx::mbar_init(bar_phi_empty, 1);
+        ptx::mbar_init(bar_phi_empty, KM == KEY_CHUNK ? 2 : 1);   // (KEY_CHUNK: one commit per MMA warp)
         ptx::mbar_init(bar_phi2, 1);
-        ptx::mbar_init(bar_phi_empty2, 1);
+        ptx::mbar_init(bar_phi_empty2, KM == KEY_CHUNK ? 2 : 1);
         if (EPI == EPI_Q16RR || EPI == EPI_Q16RR64)
             for (int i = 0; i < kRowBufs; ++i) ptx::mbar_init(sbase + kRowBarOff + 8 * i, 4);   // row_full
         ptx::fence_mbarrier_init();
@@ -691,10 +702,17 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                 }
             }
         }
-    } else if (warp == kMmaWarp && !dbg_load_only) {
+    } else if ((warp == kMmaWarp || (KM == KEY_CHUNK && warp == kMmaWarp + 1)) && !dbg_load_only) {
         // ================================================================ MMA issuer
         // The whole warp walks the schedule (warp-uniform control flow keeps every operand in
         // uniform registers); one elected lane issues the tcgen05 instructions.
+        // KEY_CHUNK: two issuing warps (mw = 0 / 1) walk the same schedule and take alternate items.  An
+        // accumulator's chunks stay in K order without any handshake between the warps: a frame's next
+        // chunk is the unit's item i + U, converted after item i + 2 was started, which needed item i's
+        // A buffer back, i.e. item i's MMAs completed (n_abuf = 2) -- so it holds whenever U >= n_abuf,
+        // and for even U both chunks belong to the same warp anyway; other units (U = 1 ...) are issued
+        // by warp 0 alone.  The results are bitwise those of one issuing warp.
+        const int mw = warp - kMmaWarp;
         if (p.n_phis == 0 && !phi_stream && !phi_slices) {
             ptx::mbar_wait(bar_phi, 0);
             ptx::tc_fence_after();
@@ -744,6 +762,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                 // chunks; its d_full is committed with its last chunk (the epilogue takes the
                 // frames in the same order as every other mode)
                 const int U = w.c1 - w.c0;
+                const bool two = U >= p.n_abuf || (U & 1) == 0;   // alternate items between the two warps
                 for (int k = 0; k < p.n_chunks; ++k) {
                     uint64_t dk = desc0 + (uint64_t)k * desc_chunk;
                     if (phi_slices) {
@@ -752,9 +771,11 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                     }
                     int dj = db;
                     for (int j = 0; j < U; ++j) {
-                        if (k == 0) {
+                        const bool mine = two ? ((n_items & 1) == mw) : (mw == 0);
+                        if (mine && k == 0) {
                             ptx::mbar_wait(bar_d_empty + 8 * dj, ((d_use >> dj) & 1u) ^ 1u);
                         }
+                        if (mine) {
                         ptx::mbar_wait(bar_a_full + 8 * ab, aph);
                         ptx::tc_fence_after();
                         if (lane == 0) trace_ev(p, EV_M_AFULL, n_items);
@@ -779,8 +800,9 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                             if (k == p.n_chunks - 1) ptx::tc_commit(bar_d_full + 8 * dj);
                         }
                         __syncwarp();
-                        if (k == p.n_chunks - 1) d_use ^= 1u << dj;
                         if (lane == 0) trace_ev(p, EV_M_ISSUED, n_items);
+                        }
+                        if (k == p.n_chunks - 1) d_use ^= 1u << dj;
                         ++n_items;
                         if (++ab == p.n_abuf) {
                             ab = 0;
@@ -869,6 +891,10 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
         uint32_t kreg[2][16];
         uint32_t g_off[2] = {0, 0}, g_acol[2] = {0, 0};
         bool g_half2[2] = {true, true};
+        // KEY_CHUNK with swizzled strips: byte offset of the left 16 bytes of row rr of group j inside a stage
+        // (the right 16 bytes are at offset ^ 16); stages are 1024-B aligned, so the swizzle is a function
+        // of the offset alone
+        uint32_t g_swz[2][2] = {{0, 0}, {0, 0}}, g_swr[2][2] = {{0, 0}, {0, 0}};   // left / right 16 bytes
         if constexpr (KM == KEY_REGS || KM == KEY_CHUNK) {
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
@@ -882,6 +908,15 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                     g_off[j] += (uint32_t)(r0 * p.W);
                     g_half2[j] = (meta >> 16) & 1u;
                     g_acol[j] = (uint32_t)(f * (p.chunk_k / 2) + r0 * kWords);
+                    if constexpr (KM == KEY_CHUNK) {
+#pragma unroll
+                        for (int rr = 0; rr < 2; ++rr) {
+                            const uint32_t lin = g_off[j] + (uint32_t)(rr * p.W);
+                            const uint32_t sw = p.tma_strips == 2 ? ((lin >> 7) & 7u) << 4 : 0u;
+                            g_swz[j][rr] = lin ^ sw;
+                            g_swr[j][rr] = (lin + 16u) ^ sw;
+                        }
+                    }
                 }
             }
         }
@@ -904,7 +939,12 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
 #pragma unroll
                                 for (int rr = 0; rr < kRowsPerSt; ++rr) {
                                     uint32_t kw[8];
-                                    load_row_words<B>(kbase + g_off[j] + (uint32_t)(rr * p.W), kw);
+                                    {
+                                        const uint4 a = ptx::lds128(kbase + g_swz[j][rr]);
+                                        const uint4 b = g_half2[j] ? ptx::lds128(kbase + g_swr[j][rr]) : make_uint4(0u, 0u, 0u, 0u);
+                                        kw[0] = a.x, kw[1] = a.y, kw[2] = a.z, kw[3] = a.w;
+                                        kw[4] = b.x, kw[5] = b.y, kw[6] = b.z, kw[7] = b.w;
+                                    }
 #pragma unroll
                                     for (int q = 0; q < 8; ++q) ptx::magic2(kw[q], kx[j][rr * 16 + 2 * q], kx[j][rr * 16 + 2 * q + 1]);
                                 }
@@ -950,8 +990,9 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
                                 uint32_t cw[kRowsPerSt][8];
 #pragma unroll
                                 for (int rr = 0; rr < kRowsPerSt; ++rr) {
-                                    const uint4* src = reinterpret_cast<const uint4*>(cs_ptr + g_off[j] + (uint32_t)(rr * p.W));
-                                    const uint4 a = src[0], b = g_half2[j] ? src[1] : make_uint4(0u, 0u, 0u, 0u);
+                                    const uint4 a = *reinterpret_cast<const uint4*>(cs_ptr + g_swz[j][rr]);
+                                    const uint4 b = g_half2[j] ? *reinterpret_cast<const uint4*>(cs_ptr + g_swr[j][rr])
+                                                               : make_uint4(0u, 0u, 0u, 0u);
                                     cw[rr][0] = a.x, cw[rr][1] = a.y, cw[rr][2] = a.z, cw[rr][3] = a.w;
                                     cw[rr][4] = b.x, cw[rr][5] = b.y, cw[rr][6] = b.z, cw[rr][7] = b.w;
                                 }
@@ -962,7 +1003,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_measure_kernel(const __grid_co
 #pragma unroll
                                         for (int i = 0; i < 16; ++i) v[i] = 0u;
                                     } else {
-                                        row32_vs_kexp(cw[rr], &kx[j][rr * 16], v, g_half2[j]);
+                                        row32_vs_kexp(cw[rr], &kx[j][rr * 16], v);
                                     }
                                     ptx::tmem_st_32x32b_x16(a_tm + g_acol[j] + (uint32_t)(rr * 16), v);
                                 }
