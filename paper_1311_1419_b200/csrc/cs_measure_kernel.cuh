@@ -640,6 +640,7 @@ __global__ void __launch_bounds__(threads_for<KM>(), 1) cs_measure_kernel(const 
             if constexpr (KM == KEY_CHUNK) {
                 // chunk-outer order: per chunk k, (Phi slice k), key chunk k, then chunk k of every
                 // CS frame of the unit -- the key chunk and the slice cross L2 -> SMEM once per unit
+                if (lane == 0 && n_items == 0) trace_ev(p, EV_K_START, 6);   // first unit decoded
                 for (int k = 0; k < p.n_chunks; ++k) {
                     if (phi_slices && !dbg_load_only) {   // (load-only ablation: no MMA frees the slices)
                         ptx::mbar_wait(bar_key_empty + 8 * pb, pbph ^ 1u);
@@ -649,6 +650,7 @@ __global__ void __launch_bounds__(threads_for<KM>(), 1) cs_measure_kernel(const 
                                            p.phi_slice_bytes, bar_key_full + 8 * pb);
                         }
                         __syncwarp();
+                        if (lane == 0 && n_items == 0 && k == 0) trace_ev(p, EV_K_START, 7);   // first Phi slice issued
                         pb ^= 1;
                         if (pb == 0) pbph ^= 1u;
                     }
@@ -958,9 +960,9 @@ __global__ void __launch_bounds__(threads_for<KM>(), 1) cs_measure_kernel(const 
                         ph ^= 1u;
                     }
                     for (int c = w.c0; c < w.c1; ++c) {
-                        ptx::mbar_wait(bar_stage_full + 8 * st, ph);
-                        if (tr) trace_ev(p, EV_C_FULL, n_items);
                         if (dbg_load_only) {
+                            ptx::mbar_wait(bar_stage_full + 8 * st, ph);
+                            if (tr) trace_ev(p, EV_C_FULL, n_items);
                             __syncwarp();
                             if (lane == 0) ptx::mbar_arrive(bar_stage_empty + 8 * st);
                             if (++st == p.n_stages) {
@@ -970,9 +972,13 @@ __global__ void __launch_bounds__(threads_for<KM>(), 1) cs_measure_kernel(const 
                             ++n_items;
                             continue;
                         }
-#ifndef CSENC_INJECT_RACE
-                        ptx::mbar_wait(bar_a_empty + 8 * ab, aph ^ 1u);
+                        // the strip has usually landed and the A buffer is usually free: probe both at once
+#if defined(CSENC_INJECT_RACE)
+                        ptx::mbar_wait(bar_stage_full + 8 * st, ph);
+#else
+                        ptx::mbar_wait2(bar_stage_full + 8 * st, ph, bar_a_empty + 8 * ab, aph ^ 1u);
 #endif
+                        if (tr) trace_ev(p, EV_C_FULL, n_items);
                         ptx::tc_fence_after();
                         if (tr) trace_ev(p, EV_C_AEMPTY, n_items);
                         const uint32_t cs_base = s_stage + (uint32_t)st * p.stage_bytes;

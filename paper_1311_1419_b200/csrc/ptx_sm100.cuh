@@ -132,6 +132,15 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     stress_point(bar);
 }
 
+// Wait for two barriers whose phases are usually both complete already: both probes are issued before
+// either result is used, so their latencies overlap (a probe's result takes ~60-100 cycles to come back).
+__device__ __forceinline__ void mbar_wait2(uint32_t bar_a, uint32_t parity_a, uint32_t bar_b, uint32_t parity_b) {
+    const bool a = mbar_try_wait(bar_a, parity_a), b = mbar_try_wait(bar_b, parity_b);
+    if (!a) mbar_wait(bar_a, parity_a);
+    if (!b) mbar_wait(bar_b, parity_b);
+    stress_point(bar_a ^ bar_b);
+}
+
 // ------------------------------------------------------------------ programmatic dependent launch
 // A kernel launched with cudaLaunchAttributeProgrammaticStreamSerialization may start while the previous
 // kernel of the stream is still draining.  grid_dep_launch(): this CTA no longer holds back the next

@@ -70,7 +70,8 @@ def main(workload="C4", M=None, cap=256, T=None, q16=None):
         rep["  CS items / epilogue items of CTA 0"] = float(n * 1000 + ne_)
         kst = t[ev.index("k_start")]
         for j, what in ((1, "barriers initialised"), (2, "TMEM allocated"), (4, "offset table written"),
-                        (3, "prologue barrier passed"), (5, "producer: Phi issued")):
+                        (3, "prologue barrier passed"), (5, "producer: Phi issued"),
+                        (6, "producer: first unit decoded"), (7, "producer: first Phi slice issued")):
             if kst[j] >= 0:
                 rep[f"    prologue: {what} (since k_start)"] = float(kst[j] - ks)
     for k, v in rep.items():
@@ -95,7 +96,7 @@ def main(workload="C4", M=None, cap=256, T=None, q16=None):
     print(f"  period/item {per:.0f} cycles = {30720 if False else 0}", " ".join(f"{k}={v:.2f}" for k, v in util.items()))
     print("first 12 items (cycles since first event):")
     print("   i " + " ".join(f"{k:>9s}" for k in ev))
-    for i in range(min(12, n)):
+    for i in range(min(int(os.environ.get("TRACE_ROWS", "12")), n)):
         print(f"{i:4d} " + " ".join(f"{t[j, i]:9d}" for j in range(len(ev))))
     return rep
 
