@@ -56,6 +56,7 @@ def lib() -> ctypes.CDLL:
             "cs_encoder_destroy": (c_int, [vp]),
             "cs_encoder_plan": (c_int, [vp, ctypes.POINTER(PlanInfo)]),
             "cs_encoder_set_trace": (c_int, [vp, vp, c_int]),
+            "cs_encoder_set_stable_inputs": (c_int, [vp, c_int]),
             "cs_encoder_autotune": (c_int, [vp, vp, c_int, c_int, vp, c_int, c_int, vp]),
             "cs_encoder_num_candidates": (c_int, [vp]),
             "cs_encoder_set_candidate": (c_int, [vp, c_int]),
@@ -250,6 +251,12 @@ class Encoder:
     def set_trace(self, buf=None, cap: int = 0):
         """buf: CUDA int64 tensor of len(TRACE_EVENTS) * cap elements (None/0 disables)."""
         _check(lib().cs_encoder_set_trace(self._h, _ptr(buf) if buf is not None else None, cap))
+
+    def set_stable_inputs(self, on: bool = True):
+        """Promise that this encoder's inputs (frames, Phi) are never written by the kernel preceding a call
+        in its stream: the kernel then loads and measures while that kernel drains, and only its output
+        stores wait for it (cs_encoder_set_stable_inputs)."""
+        _check(lib().cs_encoder_set_stable_inputs(self._h, 1 if on else 0))
 
     # -- accounting
     def plan(self) -> dict:

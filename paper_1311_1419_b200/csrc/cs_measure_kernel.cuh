@@ -109,6 +109,9 @@ struct KParams {
     // so the converters' 16-byte reads of blocks 32 bytes apart spread over all banks (unswizzled, lanes
     // l and l + 4 of a quarter-warp hit the same banks: every read took two wavefronts)
     int tma_strips;
+    // pdl_early != 0 (cs_encoder_set_stable_inputs): the inputs do not depend on the stream's previous kernel,
+    // so only the epilogue warps wait for it (before their first store / first read of the frame maxima)
+    int pdl_early;
     // phi_stream != 0 (multi-chunk plans, KM 0/1): Phi is not resident; each stage carries the K-slice
     // of Phi its chunk needs (phi_slice_bytes at stage offset stage_phi_off, a contiguous range of the
     // canonical layout), and the stage is freed only when the converters AND the MMAs are done with it
@@ -551,7 +554,7 @@ __global__ void __launch_bounds__(threads_for<KM>(), 1) cs_measure_kernel(const 
     // start as this kernel's CTAs leave their SMs and run their own prologue); this kernel touches global
     // memory (frames, keys, Phi in; measurements out; trace) only after the previous kernel has completed.
     ptx::grid_dep_launch();
-    ptx::grid_dep_wait();
+    if (!p.pdl_early) ptx::grid_dep_wait();   // (pdl_early: the epilogue warps wait, before their first global access)
     if (threadIdx.x == 0) trace_ev(p, EV_K_START, 3);   // all warps through the prologue barrier
     uint32_t tmem_base;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem_base) : "r"(tmem_slot));
@@ -1165,6 +1168,7 @@ __global__ void __launch_bounds__(threads_for<KM>(), 1) cs_measure_kernel(const 
         // (Q_FRAME) codes with the frame's scale; (Q_ROW) pass A: per-block-row max reduced across
         // the 4 epilogue warps in SMEM slots (triple-buffered, one named barrier per item), pass B:
         // re-read the accumulators from TMEM and store codes with the row's scale.
+        if (p.pdl_early) ptx::grid_dep_wait();
         const int ew = warp - kEpiWarp0;
         const int lane_idx = ew * 32 + (int)lane;
         const uint32_t lane_bits = (uint32_t)(ew * 32) << 16;
@@ -1436,6 +1440,7 @@ __global__ void __launch_bounds__(threads_for<KM>(), 1) cs_measure_kernel(const 
         // M % 4 == 0 each 32-row x (16|32)-column accumulator chunk goes through a 4 KB
         // XOR-swizzled SMEM tile so that every st.global.v4 instruction writes whole 64/128-byte
         // row segments (bank-conflict-free on both sides).  Other M: scalar stores.
+        if (p.pdl_early) ptx::grid_dep_wait();
         const int ew = warp - kEpiWarp0;
         const uint32_t lane_bits = (uint32_t)(ew * 32) << 16;
         const uint32_t stage_tile = sbase + p.off_epi + (uint32_t)ew * 4096u;
