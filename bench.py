@@ -140,10 +140,11 @@ def load_traffic(workload):
 
 # ------------------------------------------------------------------------------------------ ours
 def timed_steps(args, launch, n_launch, stream, dev, world, flush=None):
-    """W untimed warm-up steps, then K timed steps of n_launch launches each between one CUDA-event pair on
-    the launching stream (barrier + synchronize on both sides, clocks sampled during the region, device
-    time = max over ranks), then the same K steps again with an event pair around every launch (per-launch
-    attribution).  With an L2 flush before every launch there is one pass, timed by the launches' pairs."""
+    """W untimed warm-up steps, then K timed steps of n_launch launches each between ONE CUDA-event pair on the
+    launching stream (barrier + synchronize on both sides, clocks sampled during the region, device time = max
+    over ranks), then -- after a 0.5 s pause -- a per-launch attribution pass: min(K, 20) steps with an event
+    pair around every launch.  With an L2 flush before every launch there is one pass of K steps, timed by the
+    launches' pairs.  Returns (ms_total, launch_ms[i] = the pair times of launch i, clk)."""
     import torch
     import torch.distributed as dist
 
@@ -161,15 +162,16 @@ def timed_steps(args, launch, n_launch, stream, dev, world, flush=None):
         step()
     torch.cuda.synchronize(dev)
     K = args.steps
+    Kp = K if flush is not None else min(K, 20)   # steps of the per-launch-event pass
     evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in range(n_launch)]
-           for _ in range(K)]
+           for _ in range(Kp)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     # The timed region: K steps queued back to back, one event pair around them.  (An event record between
     # two kernels keeps the second one's prologue from overlapping the first one's tail -- the K1 kernels are
-    # launched with programmatic dependent launch -- so the per-launch events live in a second pass below.
+    # launched with programmatic dependent launch -- so the per-launch events live in a pass of their own below.
     # Inputs smaller than L2 are flushed before every launch, which needs the per-launch events: one pass.)
     with ClockSampler(dev.index or 0) as clk:
         t0.record(stream)
@@ -180,12 +182,13 @@ def timed_steps(args, launch, n_launch, stream, dev, world, flush=None):
     if world > 1:
         dist.barrier()
     ms_total = t0.elapsed_time(t1)
-    if flush is None:   # second pass, same K steps, an event pair around every launch: per-launch attribution
-        for k in range(K):
+    if flush is None:   # per-launch attribution pass (an event pair around every launch), after the timed region
+        time.sleep(0.5)   # and after a pause: sustained load lowers the throughput, and the
+        for k in range(Kp):   # attribution should see the launches as the first steps of the region did
             step(evs[k])
         torch.cuda.synchronize(dev)
-    launch_ms = [[evs[k][i][0].elapsed_time(evs[k][i][1]) for k in range(K)] for i in range(n_launch)]
-    if flush is not None:   # the step time excludes the flushes: sum of the launches' own event times
+    launch_ms = [[evs[k][i][0].elapsed_time(evs[k][i][1]) for k in range(Kp)] for i in range(n_launch)]
+    if flush is not None:   # the step time excludes the flushes: sum of the launches' own event times (Kp == K)
         ms_total = sum(sum(col) for col in launch_ms)
     if world > 1:
         tt = torch.tensor([ms_total], device=dev)
@@ -365,7 +368,7 @@ def run_ours(args, cfg, Ms):
         clean_ms = clean_ms[1:]
     key_ms = None
     if closed:
-        key_ms = sum(launch_ms[0]) / K
+        key_ms = statistics.mean(launch_ms[0])
         launch_ms = launch_ms[1:]
 
     # ---- end to end through the public host-buffer C-ABI call (copies inside the timed region)
@@ -419,7 +422,7 @@ def run_ours(args, cfg, Ms):
     tot_bytes, tot_ms = 0.0, 0.0
     for i, M in enumerate(Ms):
         med = statistics.median(launch_ms[i])
-        avg = sum(launch_ms[i]) / K
+        avg = statistics.mean(launch_ms[i])
         b = alg_bytes(cfg, M, n_seq, args.output)
         per_m[str(M)] = {"ms_median": med, "ms_mean": avg, "ms_mean_l2clean": clean_ms[i],
                          "frac_of_peak_l2clean": alg_bytes(cfg, M, n_seq, args.output) / (clean_ms[i] * 1e-3) / 1e9 / peak,
@@ -457,7 +460,7 @@ def run_ours(args, cfg, Ms):
                      "achieved_event_pairs": achieved_pairs,
                      "time_base": ("event pair around every launch (sum of the launches' mean times)" if (small or closed) else
                                    "the timed region: K steps queued back to back between one event pair; "
-                                   "achieved_event_pairs = the same bytes over the second pass's per-launch event times "
+                                   "achieved_event_pairs = the same bytes over the attribution pass's per-launch event times (min(K, 20) steps after the region and a 0.5 s pause) "
                                    "(each pair adds the launch latency an event record exposes: ~6.6 us for a K1-shaped launch)"),
                      "traffic": (traffic or {}).get("mean_bytes_per_launch"),
                      "alg_bytes_per_launch": tot_bytes / len(Ms), "traffic_detail": traffic, "peak_source": peak_src,
@@ -510,6 +513,9 @@ def run_adjoint(args, cfg, Ms):
         xs.append(torch.empty((y.shape[0], cfg.H, cfg.W), dtype=torch.float32, device=dev))
     del frames
     torch.cuda.synchronize(dev)
+    if os.environ.get("BENCH_STABLE_INPUTS", "1") != "0":   # the measurements are resident and nothing writes them
+        for e in encs:
+            e.set_stable_inputs(True)
     torch.cuda.empty_cache()
     stream = torch.cuda.current_stream(dev)
 
@@ -527,7 +533,7 @@ def run_adjoint(args, cfg, Ms):
     px = n_cs * cfg.W * cfg.H
     per_m, tot_b, tot_ms = {}, 0.0, 0.0
     for i, M in enumerate(Ms):
-        avg = sum(launch_ms[i]) / K
+        avg = statistics.mean(launch_ms[i])
         b = ys[i].numel() * 4 + xs[i].numel() * 4          # y read once + x written once
         per_m[str(M)] = {"ms_median": statistics.median(launch_ms[i]), "ms_mean": avg,
                          "gpix_s": px / (avg * 1e-3) / 1e9, "alg_gbs": b / (avg * 1e-3) / 1e9,
@@ -535,8 +541,9 @@ def run_adjoint(args, cfg, Ms):
                          "tflops_tf32": 2 * 2 * n_cs * encs[i].nblk * M * cfg.B ** 2 / (avg * 1e-3) / 1e12}
         tot_b += b
         tot_ms += avg
-    achieved = tot_b / (tot_ms * 1e-3) / 1e9
+    achieved_pairs = tot_b / (tot_ms * 1e-3) / 1e9
     ms_step = ms_total / K
+    achieved = tot_b / (ms_step * 1e-3) / 1e9   # time base: the timed region (as the encode op)
     line = {
         "metric": "CS-frame Gpixels/s back-projected (x0 = Phi^T y per block, frame layout)",
         "value": world * len(Ms) * px / (ms_step * 1e-3) / 1e9, "unit": "Gpixel/s", "n_gpus": world, "steps": K,
@@ -548,6 +555,9 @@ def run_adjoint(args, cfg, Ms):
                    "l2": "outputs larger than L2 (x is n_cs*H*W*4 bytes per launch); no flush",
                    "parallelism": f"dp{world} (independent sequences per GPU, no collective)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "achieved_event_pairs": achieved_pairs,
+                     "time_base": "the timed region (K steps back to back between one event pair); "
+                                  "achieved_event_pairs: the attribution pass's per-launch event pairs",
                      "traffic": None, "peak_source": peak_src,
                      "kernel": "cs_adjoint_kernel (alg bytes = fp32 y read once + fp32 x written once)"},
         "per_M": per_m,
@@ -601,15 +611,16 @@ def run_frame(args):
             dist.destroy_process_group()
         return None
     n_cs = y.shape[0]
-    avg = sum(launch_ms[0]) / K
+    avg = statistics.mean(launch_ms[0])
     flop = 2.0 * m * n * n_cs
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             peak, peak_src = float(json.load(f)["bf16_tflops"]), "measured bf16 dense burst (MEASURED_PEAKS.json); fp16 rate = bf16 rate"
     except Exception:
         peak, peak_src = 2250.0, "fallback nominal dense fp16 (B200_PROFILING.md)"
-    achieved = flop / (avg * 1e-3) / 1e12
+    achieved_pairs = flop / (avg * 1e-3) / 1e12
     ms_step = ms_total / K
+    achieved = flop / (ms_step * 1e-3) / 1e12   # time base: the timed region (one launch per step)
     px = n_cs * n
     line = {
         "metric": "CS-frame Gpixels/s measured with one frame-level A (Eq. 1, m = n/50)",
@@ -622,6 +633,9 @@ def run_frame(args):
                    "l2": f"frames {S * T * n / 2**20:.0f} MiB per launch (> 126 MiB L2); A {m * n * 2 / 2**20:.1f} MiB L2-resident",
                    "parallelism": f"dp{world} (independent sequences per GPU, no collective)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "achieved_event_pairs": achieved_pairs,
+                     "time_base": "the timed region (K steps back to back between one event pair); "
+                                  "achieved_event_pairs: the attribution pass's per-launch event pairs",
                      "traffic": None, "peak_source": peak_src,
                      "kernel": "cs_frame_measure_kernel (algorithmic flop = 2 m n per CS frame)"},
         "per_launch_ms": {"mean": avg, "median": statistics.median(launch_ms[0])},

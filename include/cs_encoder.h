@@ -136,8 +136,8 @@ int cs_encoder_set_trace(cs_encoder* enc, unsigned long long* trace_dev, int cap
  * start while the stream's previous KERNEL is still draining (they take an SM as soon as that kernel's CTA
  * there has exited).  By default the kernel then waits for the previous kernel to complete before it
  * touches global memory at all, so only its prologue overlaps.  on != 0 is the caller's promise that the
- * INPUTS of this encoder's calls (frames, and Phi) are never written by the kernel that precedes the call
- * in the stream -- e.g. they arrive by cudaMemcpyAsync, which is ordered as usual, or were finished
+ * INPUTS of this encoder's calls (frames and Phi; for cs_adjoint the measurements) are never written by the
+ * kernel that precedes the call in the stream -- e.g. they arrive by cudaMemcpyAsync, which is ordered as usual, or were finished
  * earlier: the frame loads, conversion and MMAs then start at once and only the output stores (and the
  * reads of the per-frame maxima of a two-pass quantisation) wait for the previous kernel, which keeps
  * write-after-write order on a reused output buffer.  Calls whose inputs come from the preceding kernel

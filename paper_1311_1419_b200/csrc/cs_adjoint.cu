@@ -102,13 +102,28 @@ int launch_adjoint(cs_encoder* e, const float* meas, long long n_frames, float* 
     ap.x_floats = n_frames * (long long)g.W * g.H;
     ap.smem_bytes = e->adj_smem - 1024;
     const int grid = std::max(1, std::min(e->sms, ap.n_units));
+    ap.pdl_early = e->stable_inputs ? 1 : 0;
+    // programmatic dependent launch, as the measurement kernel (cs_encoder.cu launch())
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)csenc::adj::kThreads);
+    cfg.dynamicSmemBytes = (size_t)e->adj_smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = CSENC_PDL ? 1 : 0;
+    cudaError_t lerr = cudaSuccess;
     switch (g.B) {
-        case 8: csenc::adj::cs_adjoint_kernel<8><<<grid, csenc::adj::kThreads, e->adj_smem, stream>>>(ap); break;
-        case 16: csenc::adj::cs_adjoint_kernel<16><<<grid, csenc::adj::kThreads, e->adj_smem, stream>>>(ap); break;
-        case 32: csenc::adj::cs_adjoint_kernel<32><<<grid, csenc::adj::kThreads, e->adj_smem, stream>>>(ap); break;
+        case 8: lerr = cudaLaunchKernelEx(&cfg, csenc::adj::cs_adjoint_kernel<8>, ap); break;
+        case 16: lerr = cudaLaunchKernelEx(&cfg, csenc::adj::cs_adjoint_kernel<16>, ap); break;
+        case 32: lerr = cudaLaunchKernelEx(&cfg, csenc::adj::cs_adjoint_kernel<32>, ap); break;
         default: return fail(CS_ERR_UNSUPPORTED, "block size");
     }
     cudaError_t err = cudaGetLastError();
+    if (err == cudaSuccess) err = lerr;
     return err == cudaSuccess ? CS_OK : cuda_fail(err, "adjoint launch");
 }
 

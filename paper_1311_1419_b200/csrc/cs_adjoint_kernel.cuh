@@ -51,6 +51,10 @@ struct AParams {
     // flat != 0 (nbx % 32 == 0): a tile is 128 consecutive blocks of the frame's raster order, across
     // block rows (each epilogue warp's 32 blocks still lie in one block row); tiles_pf per frame
     int flat, tiles_pf;
+    // programmatic dependent launch (as K1): 0 = the whole kernel waits for the stream's previous kernel before
+    // touching global memory; 1 (cs_encoder_set_stable_inputs: y and Phi^T not written by that kernel) = only
+    // the epilogue warps wait, before their first store
+    int pdl_early;
     int Kc, n_kc;             // K per stage (8/16/32), K chunks
     int Nc, n_nc;             // output columns per item (<= 256), items per tile
     uint32_t a_bytes, chunk_bytes, stage_bytes;
@@ -119,6 +123,8 @@ __global__ void __launch_bounds__(kThreads, 1) cs_adjoint_kernel(const __grid_co
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
+    ptx::grid_dep_launch();
+    if (!p.pdl_early) ptx::grid_dep_wait();
     uint32_t tmem_base;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tmem_base) : "r"(tmem_slot));
 
@@ -222,6 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1) cs_adjoint_kernel(const __grid_co
         }
     } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
         // ================================================================ epilogue
+        if (p.pdl_early) ptx::grid_dep_wait();
         const int ew = warp - kEpiWarp0;   // == warp % 4: TMEM lanes 32*ew .. 32*ew+31
         const uint32_t lane_bits = (uint32_t)(ew * 32) << 16;
         const uint32_t tile = sbase + kOffEpi + (uint32_t)ew * 4096u;

@@ -18,6 +18,7 @@
 //   warp 13       MMA issuer (a4) + TMEM allocator: D[tmem, fp32] += A[tmem, fp16] x
 //                 Phi^T[smem, fp16], one tcgen05.mma.kind::f16 (M=128 lanes, N=Mpad, K=16) per
 //                 16 pixels; commit -> mbarriers.  Warp-uniform loop, one elected issuing lane.
+//   warp 14       (KEY_CHUNK kernels only) second MMA issuer: the two warps take alternate items.
 //   warps 8..11   epilogue (a6): tcgen05.ld of the fp32 accumulators -> (swizzled SMEM tile) ->
 //                 row-contiguous vector stores of y[s][g][c][by][bx][0..M) (block-major).
 //
@@ -29,6 +30,11 @@
 // Pipelines (mbarrier parity rings): stage_full/empty (TMA <-> converters), key_full/empty
 // (KM=1), a_full/empty (converters <-> MMA, TMEM A buffers), d_full/empty (MMA <-> epilogue,
 // TMEM accumulators).  Paper passages: Eq.(1) P:83-85, P:87 and Eq.(2)-(3) P:89-91.
+//
+// Launch overlap: the kernel is launched with programmatic stream serialization; it releases the next
+// kernel's launch in its prologue and waits for the previous kernel (griddepcontrol.wait) before it touches
+// global memory -- the whole CTA by default, only the epilogue warps when the caller has promised stable
+// inputs (KParams::pdl_early, cs_encoder_set_stable_inputs).
 #pragma once
 #include <cuda.h>
 #include <type_traits>

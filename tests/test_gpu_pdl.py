@@ -104,3 +104,26 @@ def test_q16_two_pass_and_store_paths_back_to_back_with_stable_inputs():
             r1, t1 = e2.encode_batch_q16(fd, P.Encoder.Q16_ROW)
         torch.cuda.synchronize()
         assert torch.equal(c0, c1) and torch.equal(s0, s1) and torch.equal(r0, r1) and torch.equal(t0, t1), M
+
+
+def test_adjoint_back_to_back_with_stable_inputs():
+    cfg = synth.CONFIGS["C4"].with_(T=19, S=1)
+    fd = torch.from_numpy(synth.gen_video(cfg)).cuda()
+    (e,) = _encoders(cfg, (32,), False)
+    y = e.encode_batch(fd)
+    x0 = e.adjoint(y).clone()
+    torch.cuda.synchronize()
+    e.set_stable_inputs(True)
+    x = torch.empty_like(x0)
+    for _ in range(6):
+        e.adjoint(y, x)
+    torch.cuda.synchronize()
+    assert torch.equal(x, x0)
+    # default setting, y produced by the kernel right before the adjoint
+    e.set_stable_inputs(False)
+    y2 = torch.empty_like(y)
+    for _ in range(3):
+        e.encode_batch(fd, y2)
+        e.adjoint(y2, x)
+    torch.cuda.synchronize()
+    assert torch.equal(x, x0)

@@ -8,5 +8,5 @@ python tools/summarize_next.py gpurun_out/$TAG-next $TAG >> gpurun_out/$TAG/summ
 python tools/tabulate_bench.py gpurun_out/$TAG > gpurun_out/$TAG/bench_table.md 2>&1
 mkdir -p gpurun_out/$TAG/profiles && cp profiles/${TAG}_* profiles/ncu_traffic.json gpurun_out/$TAG/profiles/ 2>/dev/null
 du -sh gpurun_out/$TAG/*.ncu-rep gpurun_out/$TAG-next/*/*.ncu-rep > gpurun_out/$TAG/rep_sizes.txt 2>&1
-find gpurun_out -name "*.ncu-rep" -size +20M -delete
+find gpurun_out -name "*.ncu-rep" -size +8M -delete
 du -sh gpurun_out >> gpurun_out/$TAG/rep_sizes.txt
