@@ -343,18 +343,20 @@ def run_ours(args, cfg, Ms):
 
     # L2 between iterations (contract: flush it, or use inputs larger than it):
     #  * inputs >= 2 x L2 (C4, C5): nothing to do;
-    #  * L2 <= inputs < 2 x L2 (C3), fp32 open-loop encode: the steps ROTATE over n_rot copies of the frames and
+    #  * inputs < 2 x L2 but >= 2 x L2 / 11 (C3, C2), fp32 open-loop encode: the steps ROTATE over n_rot copies of the frames and
     #    n_rot output buffers (n_rot x input >= 2 x L2 + input), so a launch never finds its frames in L2 and the
     #    previous launches' dirty output is written back inside the region -- a stream of new data, no flush
     #    (back-to-back launches on ONE copy re-read 6% of the input from L2 and leave 36 of the 43 MB output
     #    dirty in L2: ncu --cache-control none; --no-rotate times that config with flushes instead);
-    #  * smaller inputs (C1, C2), or other ops / outputs below 2 x L2: L2 flushed before every launch, outside
+    #  * smaller inputs (C1), or other ops / outputs below 2 x L2: L2 flushed before every launch, outside
     #    its event pair.
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
     n_rot = 1
-    if (l2_bytes <= frames.numel() < 2 * l2_bytes and gran is None and args.op == "encode" and not args.gop_phis
+    if (frames.numel() < 2 * l2_bytes and gran is None and args.op == "encode" and not args.gop_phis
             and not args.no_rotate):
         n_rot = -(-2 * l2_bytes // frames.numel()) + 1
+        if n_rot > 12:   # tiny inputs (C1): that many copies still fit in L2 together -- flush instead
+            n_rot = 1
     frames_r = [frames] + [frames.clone() for _ in range(n_rot - 1)]
     outs_r = [[o] + [torch.empty_like(o) for _ in range(n_rot - 1)] for o in outs] if gran is None else None
     rot = [0]
@@ -833,7 +835,7 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-rotate", action="store_true",
-                    help="inputs between 1x and 2x L2 (C3): flush L2 before every launch instead of rotating copies")
+                    help="inputs below 2x L2 (C3, C2): flush L2 before every launch instead of rotating copies")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-autotune", action="store_true")
