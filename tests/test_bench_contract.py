@@ -48,6 +48,10 @@ def test_device_arm_contract():
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5
     assert abs(r["achieved"] / r["peak"] - r["frac"]) < 1e-9
     assert r["traffic"] is None or r["traffic"] > 0
+    # time base: the timed region (step bytes / step time); the per-launch event pairs are reported beside it
+    alg = sum(m["alg_bytes"] for m in d["per_M"].values())
+    assert abs(r["achieved"] - alg / (d["ms_per_step"] * 1e-3) / 1e9) < 1e-6 * r["achieved"]
+    assert 0 < r["achieved_event_pairs"] < 1.5 * r["peak"] and "timed region" in r["time_base"]
     c = d["clocks"]
     assert c["sm_mhz"] > 0 and c["sm_max_mhz"] > 0 and isinstance(c["reasons"], list)
     e = d["e2e"]
