@@ -124,7 +124,10 @@ int cs_encoder_plan(const cs_encoder* enc, cs_plan_info* info);
  * buffer free, 4 converter A written, 5 MMA A ready, 6 MMA issued+committed, 7 epilogue
  * accumulator ready, 8 epilogue done, 9 converter tcgen05.st issued, 10 / 11 (q16 row-scale register
  * path) epilogue row maxima published / all four warps' maxima present, 12 kernel entry and 13 CTA
- * exit (one occurrence each).  cap = 0 disables (default).
+ * exit (one occurrence each; occurrences 1..7 of event 12 are start-up marks: barriers initialised,
+ * TMEM allocated, prologue barrier passed, offset table written, producer started, producer's first
+ * unit decoded, first Phi slice issued).  cap = 0 disables (default).  While a trace buffer is set the
+ * kernels do not overlap their predecessors (cs_encoder_set_stable_inputs is ignored).
  * Not thread-safe with concurrent encodes of the same encoder. */
 #define CS_TRACE_EVENTS 14
 /* Profiling ranges: with CSENC_NVTX=1 in the environment (read once per process), every encode /
