@@ -69,7 +69,7 @@ def load_peaks():
 class ClockSampler:
     """Samples SM clock and throttle reasons with NVML while the timed region runs."""
 
-    def __init__(self, device_index: int, period_s: float = 0.01):
+    def __init__(self, device_index: int, period_s: float = 0.002):
         self.samples, self.reasons = [], set()
         self.max_mhz = None
         self._stop = threading.Event()
