@@ -537,7 +537,7 @@ def run_adjoint(args, cfg, Ms):
     torch.cuda.synchronize(dev)
     if os.environ.get("BENCH_STABLE_INPUTS", "1") != "0":   # the measurements are resident and nothing writes them
         for e in encs:
-            e.set_stable_inputs(True)
+            e.set_stable_inputs(frames=False, measurements=True)
     torch.cuda.empty_cache()
     stream = torch.cuda.current_stream(dev)
 

@@ -135,18 +135,24 @@ int cs_encoder_plan(const cs_encoder* enc, cs_plan_info* info);
  * nsys); header-only nvtx3, a no-op when no tool is attached. */
 int cs_encoder_set_trace(cs_encoder* enc, unsigned long long* trace_dev, int cap);
 
-/* Launch overlap (programmatic dependent launch).  Every encode kernel is launched so that its CTAs may
- * start while the stream's previous KERNEL is still draining (they take an SM as soon as that kernel's CTA
- * there has exited).  By default the kernel then waits for the previous kernel to complete before it
- * touches global memory at all, so only its prologue overlaps.  on != 0 is the caller's promise that the
- * INPUTS of this encoder's calls (frames and Phi; for cs_adjoint the measurements) are never written by the
- * kernel that precedes the call in the stream -- e.g. they arrive by cudaMemcpyAsync, which is ordered as usual, or were finished
- * earlier: the frame loads, conversion and MMAs then start at once and only the output stores (and the
- * reads of the per-frame maxima of a two-pass quantisation) wait for the previous kernel, which keeps
- * write-after-write order on a reused output buffer.  Calls whose inputs come from the preceding kernel
- * by construction (cs_encode_batch_keys: the decoded keys) ignore the setting.  Default 0.  Worth ~3 us
- * per launch back to back (SURVEY.md sec.8 d: short launches, C2 / C3). */
-int cs_encoder_set_stable_inputs(cs_encoder* enc, int on);
+/* Launch overlap (programmatic dependent launch).  Every encode / adjoint kernel is launched so that its
+ * CTAs may start while the stream's previous KERNEL is still draining (they take an SM as soon as that
+ * kernel's CTA there has exited).  By default the kernel then waits for the previous kernel to complete
+ * before it touches global memory at all, so only its prologue overlaps.  `flags` is the caller's promise
+ * about INPUTS (bit mask, default 0):
+ *   CS_STABLE_FRAMES (1): the frames (and Phi) of this encoder's ENCODE calls are never written by the
+ *     kernel that precedes the call in the stream -- e.g. they arrive by cudaMemcpyAsync, which is ordered
+ *     as usual, or were finished earlier;
+ *   CS_STABLE_MEASUREMENTS (2): the same for the measurements given to cs_adjoint (NOT true for
+ *     cs_adjoint right after the encode that produced them).
+ * With the promise, loads, conversion and MMAs start at once and only the output stores (and the reads of
+ * the per-frame maxima of a two-pass quantisation) wait for the previous kernel, which keeps
+ * write-after-write order on a reused output buffer.  Calls whose inputs come from the preceding kernel by
+ * construction (cs_encode_batch_keys: the decoded keys) ignore the setting.  Worth ~3 us per launch back
+ * to back (C4 step -4%; short launches, C2 / C3, more). */
+#define CS_STABLE_FRAMES 1
+#define CS_STABLE_MEASUREMENTS 2
+int cs_encoder_set_stable_inputs(cs_encoder* enc, int flags);
 
 /* ---- encode (device buffers; asynchronous) ---------------------------------------------- */
 

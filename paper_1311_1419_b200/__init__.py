@@ -252,11 +252,12 @@ class Encoder:
         """buf: CUDA int64 tensor of len(TRACE_EVENTS) * cap elements (None/0 disables)."""
         _check(lib().cs_encoder_set_trace(self._h, _ptr(buf) if buf is not None else None, cap))
 
-    def set_stable_inputs(self, on: bool = True):
-        """Promise that this encoder's inputs (frames, Phi) are never written by the kernel preceding a call
-        in its stream: the kernel then loads and measures while that kernel drains, and only its output
-        stores wait for it (cs_encoder_set_stable_inputs)."""
-        _check(lib().cs_encoder_set_stable_inputs(self._h, 1 if on else 0))
+    def set_stable_inputs(self, frames: bool = True, measurements: bool = False):
+        """Promise that the frames of this encoder's encode calls (`frames`) / the measurements given to its
+        adjoint (`measurements`) are never written by the kernel preceding the call in its stream: the
+        kernel then loads and computes while that kernel drains, and only its output stores wait for it
+        (cs_encoder_set_stable_inputs).  Do not promise `measurements` for adjoint(encode(x)) chains."""
+        _check(lib().cs_encoder_set_stable_inputs(self._h, (1 if frames else 0) | (2 if measurements else 0)))
 
     # -- accounting
     def plan(self) -> dict:

@@ -102,7 +102,7 @@ int launch_adjoint(cs_encoder* e, const float* meas, long long n_frames, float* 
     ap.x_floats = n_frames * (long long)g.W * g.H;
     ap.smem_bytes = e->adj_smem - 1024;
     const int grid = std::max(1, std::min(e->sms, ap.n_units));
-    ap.pdl_early = e->stable_inputs ? 1 : 0;
+    ap.pdl_early = (e->stable_inputs & CS_STABLE_MEASUREMENTS) ? 1 : 0;
     // programmatic dependent launch, as the measurement kernel (cs_encoder.cu launch())
     cudaLaunchConfig_t cfg;
     std::memset(&cfg, 0, sizeof(cfg));

@@ -375,7 +375,7 @@ int launch(cs_encoder* e, const uint8_t* frames, int n_seq, int T, int g0, int g
     kp.trace_cap = e->trace_cap;
     // loads before the previous kernel completes: only when the caller vouches for the inputs, and never when
     // the keys come from the key-codec kernel or a trace buffer is shared between launches
-    kp.pdl_early = (e->stable_inputs && q.keys == nullptr && e->trace == nullptr) ? 1 : 0;
+    kp.pdl_early = ((e->stable_inputs & CS_STABLE_FRAMES) && q.keys == nullptr && e->trace == nullptr) ? 1 : 0;
     kp.keys = q.keys;
     kp.keys_bytes = (long long)n_seq * cdiv(T, g.G) * g.W * g.H;
     kp.chained = q.chained;
@@ -775,9 +775,10 @@ int cs_encoder_set_trace(cs_encoder* e, unsigned long long* trace_dev, int cap) 
     return CS_OK;
 }
 
-int cs_encoder_set_stable_inputs(cs_encoder* e, int on) {
+int cs_encoder_set_stable_inputs(cs_encoder* e, int flags) {
     if (!e) return fail(CS_ERR_ARG, "encoder is NULL");
-    e->stable_inputs = on ? 1 : 0;
+    if (flags & ~(CS_STABLE_FRAMES | CS_STABLE_MEASUREMENTS)) return fail(CS_ERR_ARG, "unknown stable-input flags");
+    e->stable_inputs = flags;
     return CS_OK;
 }
 

@@ -123,7 +123,7 @@ struct cs_encoder {
     size_t zeros_bytes = 0;
     unsigned long long* trace = nullptr;  // device buffer (debug timeline), caller-owned
     int trace_cap = 0;
-    int stable_inputs = 0;         // cs_encoder_set_stable_inputs: loads may start before the previous kernel completes
+    int stable_inputs = 0;         // cs_encoder_set_stable_inputs flags: loads may start before the previous kernel completes
     std::vector<cudaEvent_t> hev;
     // stream-ordered scratch (q16 workspaces): the encoder's own memory pool, created on first use,
     // that keeps its memory between calls (release threshold = max) so repeated calls do not map

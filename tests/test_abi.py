@@ -34,6 +34,9 @@ def test_library_exports_every_declared_symbol():
 def test_version_and_error_string():
     assert "sm_100a" in P.version()
     assert P.lib().cs_encoder_destroy(None) == P.CS_OK
+    # setters validate before touching the device
+    assert P.lib().cs_encoder_set_stable_inputs(None, 1) == P.CS_ERR_ARG
+    assert b"NULL" in P.lib().cs_last_error()
 
 
 @pytest.mark.parametrize("args,code", [

@@ -21,7 +21,7 @@ def _encoders(cfg, Ms, stable):
     encs = []
     for M in Ms:
         e = P.Encoder(cfg.W, cfg.H, cfg.G, cfg.B, M, synth.phi_from_seed(synth.phi_seed() + M, M, cfg.B ** 2))
-        e.set_stable_inputs(stable)
+        e.set_stable_inputs(frames=stable)
         encs.append(e)
     return encs
 
@@ -57,7 +57,7 @@ def test_shared_output_buffer_keeps_launch_order():
     fd = torch.from_numpy(synth.gen_video(cfg)).cuda()
     a, b = _encoders(cfg, (32, 32), True)
     b2 = P.Encoder(cfg.W, cfg.H, cfg.G, cfg.B, 32, synth.phi_from_seed(synth.phi_seed() + 777, 32, cfg.B ** 2))
-    b2.set_stable_inputs(True)
+    b2.set_stable_inputs(frames=True)
     ra, rb = a.encode_batch(fd).clone(), b2.encode_batch(fd).clone()
     torch.cuda.synchronize()
     assert not torch.equal(ra, rb)
@@ -113,14 +113,14 @@ def test_adjoint_back_to_back_with_stable_inputs():
     y = e.encode_batch(fd)
     x0 = e.adjoint(y).clone()
     torch.cuda.synchronize()
-    e.set_stable_inputs(True)
+    e.set_stable_inputs(frames=True, measurements=True)
     x = torch.empty_like(x0)
     for _ in range(6):
         e.adjoint(y, x)
     torch.cuda.synchronize()
     assert torch.equal(x, x0)
-    # default setting, y produced by the kernel right before the adjoint
-    e.set_stable_inputs(False)
+    # frames promised stable, measurements not: y produced by the kernel right before the adjoint
+    e.set_stable_inputs(frames=True, measurements=False)
     y2 = torch.empty_like(y)
     for _ in range(3):
         e.encode_batch(fd, y2)
