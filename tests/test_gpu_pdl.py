@@ -127,3 +127,29 @@ def test_adjoint_back_to_back_with_stable_inputs():
         e.adjoint(y2, x)
     torch.cuda.synchronize()
     assert torch.equal(x, x0)
+
+
+def test_stable_inputs_inside_a_cuda_graph():
+    """The overlapping launches keep their order when captured into a CUDA graph (programmatic edges)."""
+    cfg = synth.CONFIGS["C4"].with_(T=19, S=1)
+    fd = torch.from_numpy(synth.gen_video(cfg)).cuda()
+    encs = _encoders(cfg, (16, 64), True)
+    ref = [e.encode_batch(fd).clone() for e in encs]
+    torch.cuda.synchronize()
+    outs = [torch.zeros_like(r) for r in ref]
+    shared = torch.zeros_like(ref[1])
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(3):
+            for e, o in zip(encs, outs):
+                e.encode_batch(fd, o)
+        encs[1].encode_batch(fd, shared)
+    for _ in range(3):
+        for o in outs:
+            o.zero_()
+        shared.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        for o, r in zip(outs, ref):
+            assert torch.equal(o, r)
+        assert torch.equal(shared, ref[1])
